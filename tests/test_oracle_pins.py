@@ -1,0 +1,319 @@
+"""Pins for the CPU oracle (oracle/toom_oracle.c) against what the paper and
+the mathematics fix -- never against the oracle itself.
+
+Each test names the oracle function it pins and the independent fact used:
+golden values printed in the paper / SPEC worked examples (tests/golden/),
+closed forms, CPython's own integer multiply (a library routine outside the
+oracle), brute force on tiny inputs, and algebraic invariants (the divided
+difference closed form Eq. 3.2 vs the recurrence Eq. 3.8 the listing runs).
+"""
+import json
+import math
+import os
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def rand_limbs(rng, n):
+    return np.array([rng.getrandbits(32) for _ in range(n)], dtype=np.uint32)
+
+
+I = synth.to_int
+
+# ---------------------------------------------------------------- O1 schoolbook
+
+
+def test_schoolbook_spec_vector():
+    g = gold("paper_facts.json")["schoolbook_vector"]
+    w = oracle.schoolbook([g["u"]], [g["v"]])
+    assert I(w) == g["w"]
+
+
+def test_schoolbook_identities():
+    rng = random.Random(1)
+    x = rand_limbs(rng, 37)
+    assert I(oracle.schoolbook(x, [0])) == 0
+    assert I(oracle.schoolbook(x, [1])) == I(x)
+    assert oracle.schoolbook(np.zeros(0, np.uint32), x).size == 37
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_schoolbook_vs_cpython(seed):
+    rng = random.Random(seed)
+    for _ in range(30):
+        nu, nv = rng.randint(1, 700), rng.randint(1, 700)
+        u, v = rand_limbs(rng, nu), rand_limbs(rng, nv)
+        assert I(oracle.schoolbook(u, v)) == I(u) * I(v)
+
+
+def test_schoolbook_all_ones_closed_form():
+    # (2^N - 1)^2 = 2^(2N) - 2^(N+1) + 1
+    for n in (1, 2, 31, 96, 2048):
+        u = np.full(n, 0xFFFFFFFF, np.uint32)
+        N = 32 * n
+        assert I(oracle.schoolbook(u, u)) == (1 << (2 * N)) - (1 << (N + 1)) + 1
+
+
+# ---------------------------------------------------------------- O2 Toom
+
+
+@pytest.mark.parametrize("B", list(range(2, 17)))
+def test_toom_vs_schoolbook_all_B(B):
+    rng = random.Random(100 + B)
+    for n in (1, 2, B - 1, B, B + 1, 3 * B + 2, 65, 257, 600):
+        if n < 1:
+            continue
+        u = rand_limbs(rng, n)
+        v = rand_limbs(rng, max(1, n - rng.randint(0, 3)))
+        w = oracle.toom(u, v, top_B=B, t4=300, t3=20)
+        assert I(w) == I(u) * I(v)
+        assert np.array_equal(w, oracle.schoolbook(u, v))
+
+
+def test_toom_exhaustive_small():
+    # SPEC.md:366 style exhaustive check below 2^12 (here: all 12-bit values
+    # in 1-limb operands pushed through Karatsuba and Toom-3 on 3-limb forms)
+    vals = list(range(0, 1 << 12, 7)) + [(1 << 12) - 1]
+    for a in vals[::3]:
+        for b in vals[::5]:
+            u = np.array([a, 0, a ^ 0xABC], np.uint32)
+            v = np.array([b, b, 0], np.uint32)
+            for B in (2, 3):
+                assert I(oracle.toom(u, v, top_B=B, t4=10**9, t3=0)) == I(u) * I(v)
+
+
+def test_toom_karatsuba_spec_vector():
+    # Karatsuba shape on u = v = 2^64 - 1
+    u = np.array([0xFFFFFFFF, 0xFFFFFFFF], np.uint32)
+    assert I(oracle.toom(u, u, top_B=2, t4=10**9, t3=0)) == (2**64 - 1) ** 2
+
+
+@pytest.mark.parametrize("B", [2, 3, 4, 8, 16])
+def test_toom_products_per_level(B):
+    g = gold("paper_facts.json")["products_per_level"]
+    assert g["formula"] == "2B-1"
+    rng = random.Random(B)
+    u, v = rand_limbs(rng, 40 * B), rand_limbs(rng, 40 * B)
+    oracle.reset_counters()
+    oracle.toom(u, v, top_B=B, t4=10**9, t3=10**9)   # one level, schoolbook below
+    assert oracle.products_at_depth(0) == 1
+    assert oracle.products_at_depth(1) == 2 * B - 1
+
+
+def test_toom_closed_forms_c3_classes():
+    n = 2048
+    N = 32 * n
+    ones = np.full(n, 0xFFFFFFFF, np.uint32)
+    w = oracle.toom(ones, ones, top_B=8)
+    # (2^N-1)^2 limbs: w[0]=1, w[1..n-1]=0, w[n]=0xFFFFFFFE, rest 0xFFFFFFFF
+    assert w[0] == 1 and not w[1:n].any() and w[n] == 0xFFFFFFFE and (w[n + 1:] == 0xFFFFFFFF).all()
+    alt = np.zeros(n, np.uint32)
+    alt[1::2] = 0xFFFFFFFF
+    w = I(oracle.toom(alt, alt, top_B=8))
+    # alternating u = 2^32 (2^N-1)/(2^32+1), so (2^32+1)^2 w = 2^64 (2^N-1)^2
+    assert (2**32 + 1) ** 2 * w == 2**64 * (2**N - 1) ** 2
+    for a, c in [(0, 0), (5, 65535), (40000, 31), (65535, 65535)]:
+        u = np.zeros(n, np.uint32)
+        v = np.zeros(n, np.uint32)
+        u[a // 32] = 1 << (a % 32)
+        v[c // 32] = 1 << (c % 32)
+        assert I(oracle.toom(u, v, top_B=8)) == 1 << (a + c)
+
+
+def test_toom_c1_edges():
+    for k, expect in enumerate([(2**3072 - 1) ** 2, 0, 1, 2**6142]):
+        e = synth.c1_edge(k)
+        assert I(oracle.toom(e, e, top_B=3, t4=10**9, t3=64)) == expect
+
+
+def test_toom_fault_injection_detected():
+    # skipping one alpha division must be reported as inexact
+    rng = random.Random(7)
+    u, v = rand_limbs(rng, 64), rand_limbs(rng, 64)
+    oracle.set_fault_skip_division(3)
+    try:
+        with pytest.raises(oracle.InexactDivision):
+            oracle.toom(u, v, top_B=8, t4=10**9, t3=10**9)
+    finally:
+        oracle.set_fault_skip_division(-1)
+    assert I(oracle.toom(u, v, top_B=8, t4=10**9, t3=10**9)) == I(u) * I(v)
+
+
+def test_toom_batched_threads_deterministic():
+    u, v = synth.config_inputs(2, batch=24)
+    w1 = oracle.toom_batched(u, v, top_B=4, t4=256, t3=32, threads=1)
+    w4 = oracle.toom_batched(u, v, top_B=4, t4=256, t3=32, threads=4)
+    assert np.array_equal(w1, w4)
+    for i in range(24):
+        assert I(w1[i]) == I(u[i]) * I(v[i])
+
+
+# ---------------------------------------------------------------- §3 listings
+
+
+def test_listing_golden_example():
+    g = gold("listing_example.json")
+    a, c = oracle.interp_listings(g["xs"], g["ys"])
+    assert a == g["alpha"] and c == g["coeffs"]
+
+
+def alpha_closed_form(xs, ys, k):
+    # Eq. 3.2: alpha_k = sum_i y_i / prod_{j != i, j <= k} (x_i - x_j)
+    s = Fraction(0)
+    for i in range(k + 1):
+        d = 1
+        for j in range(k + 1):
+            if j != i:
+                d *= xs[i] - xs[j]
+        s += Fraction(ys[i], d)
+    return s
+
+
+@pytest.mark.parametrize("n", list(range(1, 16)))
+def test_listings_round_trip_paper_points(n):
+    # degree-n integer polynomials with coefficients up to
+    # 2^256 at xs = 0, 1, 2, 4, ..., 2^(n-1) are recovered exactly
+    rng = random.Random(1000 + n)
+    xs = [0] + [1 << j for j in range(n)]
+    for _ in range(6):
+        coeffs = [rng.randrange(-(1 << 256), 1 << 256) for _ in range(n + 1)]
+        ys = [sum(c * x**k for k, c in enumerate(coeffs)) for x in xs]
+        alpha, got = oracle.interp_listings(xs, ys, width=40)
+        assert got == coeffs
+        # listing 1 (recurrence Eq. 3.8, in place) == closed form Eq. 3.2
+        for k in range(n + 1):
+            assert alpha[k] == alpha_closed_form(xs, ys, k)
+
+
+def test_listing_newton_basis_polynomial():
+    # alpha = [0,...,0,1] -> coefficients of prod_{j<n} (x - x_j), brute force
+    xs = [0, 1, 2, 4, 8]
+    n = len(xs) - 1
+    # build the values of q(x) = prod_{j<n}(x - x_j) at xs
+    ys = []
+    for x in xs:
+        p = 1
+        for j in range(n):
+            p *= x - xs[j]
+        ys.append(p)
+    alpha, coeffs = oracle.interp_listings(xs, ys)
+    assert alpha == [0] * n + [1]
+    poly = [1]
+    for j in range(n):
+        nxt = [0] * (len(poly) + 1)
+        for k, c in enumerate(poly):
+            nxt[k + 1] += c
+            nxt[k] -= xs[j] * c
+        poly = nxt
+    assert coeffs == poly
+
+
+def test_listing_constant():
+    a, c = oracle.interp_listings([0, 1], [77, 77])
+    assert a == [77, 0] and c == [77, 0]
+
+
+# ---------------------------------------------------------------- §4 even-odd
+
+
+def test_even_odd_golden_example():
+    g = gold("even_odd_example.json")
+    assert oracle.even_odd_interp(g["y0"], g["yplus"], g["yminus"]) == g["w"]
+
+
+@pytest.mark.parametrize("n", list(range(1, 16)))
+def test_even_odd_equals_direct_and_truth(n):
+    # even-odd == direct interpolation over all 2n+1 points, and
+    # both equal the true product coefficients (convolution, computed here)
+    rng = random.Random(2000 + n)
+    for _ in range(4):
+        U = [rng.getrandbits(256) for _ in range(n + 1)]
+        V = [rng.getrandbits(256) for _ in range(n + 1)]
+        Wc = [sum(U[i] * V[k - i] for i in range(max(0, k - n), min(k, n) + 1)) for k in range(2 * n + 1)]
+        ev = lambda P, x: sum(c * x**k for k, c in enumerate(P))
+        y0 = ev(U, 0) * ev(V, 0)
+        yp = [ev(U, 1 << j) * ev(V, 1 << j) for j in range(n)]
+        ym = [ev(U, -(1 << j)) * ev(V, -(1 << j)) for j in range(n)]
+        got = oracle.even_odd_interp(y0, yp, ym, width=40)
+        assert got == Wc
+        xs = [0]
+        ys = [y0]
+        for j in range(n):
+            xs += [1 << j, -(1 << j)]
+            ys += [yp[j], ym[j]]
+        order = sorted(range(len(xs)), key=lambda i: xs[i])  # any distinct order works
+        _, direct = oracle.interp_listings([xs[i] for i in order], [ys[i] for i in order], width=40)
+        assert direct == Wc
+
+
+def test_max_square_abscissa_fits_word():
+    g = gold("paper_facts.json")["max_square_abscissa"]
+    n = g["B"] - 1
+    assert (1 << (n - 1)) ** 2 == 1 << g["max_x2_log2"] < 2**32
+
+
+# ---------------------------------------------------------------- O3 residues
+
+
+def test_primality_known_values():
+    assert oracle.is_prime(2**61 - 1)          # Mersenne prime M61
+    assert oracle.is_prime(2**31 - 1)
+    assert not oracle.is_prime(561)            # Carmichael number
+    assert not oracle.is_prime(3215031751)     # strong pseudoprime to bases 2,3,5,7
+    assert not oracle.is_prime((2**31 - 1) * (2**29 - 3))
+    assert sum(oracle.is_prime(k) for k in range(10**4)) == 1229   # pi(10^4)
+
+
+def test_seeded_primes():
+    ps = oracle.primes(synth.PRIME_SEED, 8)
+    assert len(set(ps)) == 8
+    for p in ps:
+        assert p.bit_length() == 61
+        assert all(p % q for q in range(3, 2000, 2))
+
+
+def test_residue_vs_cpython_and_homomorphism():
+    rng = random.Random(5)
+    ps = oracle.primes(synth.PRIME_SEED, 8)
+    for _ in range(10):
+        u, v = rand_limbs(rng, rng.randint(1, 3000)), rand_limbs(rng, rng.randint(1, 3000))
+        w = oracle.schoolbook(u, v)
+        for p in ps:
+            assert oracle.residue(u, p) == I(u) % p
+            assert oracle.residue(w, p) == (oracle.residue(u, p) * oracle.residue(v, p)) % p
+
+
+# ---------------------------------------------------------------- Eq. 2.3
+
+
+def test_alpha_exponent_paper_values():
+    g = gold("paper_facts.json")["alpha"]
+    for B, val in g["values"].items():
+        assert abs(oracle.alpha_exponent(int(B)) - val) <= g["tol"]
+
+
+# ---------------------------------------------------------------- inputs
+
+
+def test_synth_golden_first_limbs():
+    # regression pin of the counter-based generator; the GPU
+    # side receives these buffers, so this only guards against silent drift
+    u, v = synth.config_inputs(2, batch=2)
+    assert u.shape == (2, 256) and v.shape == (2, 256)
+    again = synth.uniform_limbs(synth.seed_for(2), 1, 1, 0, 256)[0]
+    assert np.array_equal(again, u[1])
+    s = synth.sm64(0)
+    assert s == 0xE220A8397B1DCDAF   # SplitMix64 first output from state 0 (published test vector)
