@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py -- batched Toom-Cook multiplication on B200 (libtoomgpu).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+One "step" = one pass of the whole hot path (split + evaluate, recursive
+pointwise products, interpolate, recompose -- SURVEY.md §8(a) rows a1-a6)
+over one batch.  At N=1 the workload is BASELINE.json configs[1] (C2):
+65536 products of two 256-limb (8192-bit) operands, Toom-4 (points
+0, +-1, +-2, 1/2, inf) recursing to a 32-limb schoolbook base.  Under
+torchrun (N>1) every rank runs its own C2 batch (weak scaling, no data-path
+collective: the products are independent) on product indices
+rank*65536 .. rank*65536+65535 of the same seeded stream.
+
+Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+C2 = dict(n=256, batch=65536, B=4, t4=32, t3=32)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(u, v, threads, target_s=12.0):
+    """Time the CPU oracle (O2, recursive Toom with the paper's points, as it
+    stands) on a bounded sample of the workload; returns products/s."""
+    import oracle
+    oracle.build()
+    cal = min(64, len(u))
+    t0 = time.perf_counter()
+    oracle.toom_batched(u[:cal], v[:cal], top_B=C2["B"], threads=threads)
+    t_cal = time.perf_counter() - t0
+    k = int(min(len(u), max(cal, cal * target_s / max(t_cal, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.toom_batched(u[:k], v[:k], top_B=C2["B"], threads=threads)
+    dt = time.perf_counter() - t0
+    return k / dt, k, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (this tier's reference arm) on the host."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    u, v = synth.config_inputs(2, batch=4096)
+    times, ks = [], []
+    for s in range(args.warmup + args.steps):
+        rate, k, dt = oracle_sample(u, v, threads, target_s=max(2.0, 60.0 / (args.warmup + args.steps)))
+        if s >= args.warmup:
+            times.append(dt)
+            ks.append(k)
+    value = sum(ks) / sum(times)
+    line = {
+        "metric": "batched products/s", "value": value, "unit": "products/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "C2: Toom-4 batch of 8192-bit products (BASELINE.json configs[1])", "n_limbs": 256,
+                   "B": 4, "per_step_sample_products": ks[0] if ks else 0},
+        "cpu_baseline": {"value": value, "unit": "products/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{ks[0] if ks else 0} C2 products per step (first products of the seeded stream), "
+                                   f"oracle O2 recursive Toom (paper points), {threads} host threads, {cpu_model()}"},
+        "e2e": {"value": value, "unit": "products/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1602_02740_b200 as tg
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+
+    n, B, batch = C2["n"], C2["B"], C2["batch"]
+    first = rank * batch
+    u_np = np.empty((batch, n), np.uint32)
+    v_np = np.empty((batch, n), np.uint32)
+    seed = synth.seed_for(2)
+    for a in range(0, batch, 8192):
+        b = min(batch, a + 8192)
+        u_np[a:b] = synth.uniform_limbs(seed, first + a, b - a, 0, n)
+        v_np[a:b] = synth.uniform_limbs(seed, first + a, b - a, 1, n)
+    u = torch.from_numpy(u_np).cuda()
+    v = torch.from_numpy(v_np).cuda()
+    w = torch.empty((batch, 2 * n), dtype=u.dtype, device="cuda")
+
+    def step():
+        tg.toom_mul_batched(u, v, B=B, t4=C2["t4"], t3=C2["t3"], out=w)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = tg.last_launch_count()
+
+    # timed region
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * batch / (ms_per_step * 1e-3)
+
+    # per-kernel-category durations (separate instrumented pass, CUDA events
+    # on the launching stream) for the roofline of the dominant kernel
+    tg.profile_enable(True)
+    for _ in range(args.steps):
+        step()
+    prof = tg.profile_collect()
+    tg.profile_enable(False)
+    plan = tg.plan_describe(n, batch, B=B, t4=C2["t4"], t3=C2["t3"])
+    lv = plan["levels"]
+    base = lv[-1]
+    E = base["n"]
+    lp_per_launch = base["count"] * E * E                     # algorithmic limb-products of the base case
+    base_ms = prof["base"]["ms"] / max(1, prof["base"]["launches"])
+    lp_rate, _ = tg.probe_limb_products()
+    achieved = lp_per_launch / (base_ms * 1e-3)
+
+    # algorithmic bytes of the streaming stages (each value read once, written once)
+    def stage_bytes():
+        evb = 0
+        itb = 0
+        for i, L in enumerate(lv[:-1]):
+            cc = L["count"] * L["npts"]
+            evb += 2 * (L["count"] * L["n"] + cc * L["e"]) * 4
+            itb += (cc * 2 * L["e"] + L["count"] * 2 * L["n"]) * 4
+        return evb, itb
+    ev_bytes, it_bytes = stage_bytes()
+    ev_ms = prof["eval"]["ms"] / args.steps
+    it_ms = prof["interp"]["ms"] / args.steps
+    pk, pk_kind = peaks()
+    shares = {k: prof[k]["ms"] / args.steps for k in ("eval", "base", "interp")}
+    dominant = max(shares, key=shares.get)
+
+    roofline = {
+        "kernel": "k_base (schoolbook base case, step a3)",
+        "bound": "alu",
+        "achieved": achieved / 1e12,
+        "peak": lp_rate / 1e12,
+        "unit": "T limb-products/s",
+        "frac": achieved / lp_rate,
+        "traffic": None,
+        "peak_kind": "measured on this GPU by toom_probe_limb_products (same mad.lo.cc/madc.hi.cc/addc sequence)",
+        "units_per_launch": lp_per_launch,
+    }
+    stages = {
+        "ms_per_step": {k: round(v, 5) for k, v in shares.items()},
+        "dominant": dominant,
+        "eval_GBps": ev_bytes / (ev_ms * 1e-3) / 1e9 if ev_ms else None,
+        "interp_GBps": it_bytes / (it_ms * 1e-3) / 1e9 if it_ms else None,
+        "hbm_peak_GBps": pk.get("hbm_gbs"), "hbm_peak_kind": pk_kind,
+        "eval_bytes": ev_bytes, "interp_bytes": it_bytes,
+    }
+
+    # end-to-end through the public C ABI with HOST buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        hu = torch.from_numpy(u_np).pin_memory()
+        hv = torch.from_numpy(v_np).pin_memory()
+        hw = torch.empty((batch, 2 * n), dtype=torch.uint32).pin_memory()
+        for _ in range(2):
+            tg.toom_mul_batched_host(hu, hv, B=B, t4=C2["t4"], t3=C2["t3"], out=hw)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            tg.toom_mul_batched_host(hu, hv, B=B, t4=C2["t4"], t3=C2["t3"], out=hw)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": world * batch * args.steps / dt, "unit": "products/s",
+               "h2d_bytes_per_step": 2 * batch * n * 4, "d2h_bytes_per_step": batch * 2 * n * 4,
+               "ms_per_step": 1e3 * dt / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, k, dt = oracle_sample(u_np, v_np, threads)
+        cpu = {"value": rate, "unit": "products/s", "cores": threads, "kind": "oracle",
+               "sample": f"{k} of the 65536 C2 products ({dt:.1f} s), oracle O2 recursive Toom (paper points 0,+-2^j, "
+                         f"§3 listings, §4 even-odd), {threads} host threads, {cpu_model()}"}
+
+    if rank == 0:
+        line = {
+            "metric": "batched products/s", "value": value, "unit": "products/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "C2: Toom-4 (points 0,+-1,+-2,1/2,inf) -> Toom-4 -> 18-limb schoolbook; "
+                                   "batch of 65536 products of two 8192-bit (256-limb) uniform operands per GPU "
+                                   "(BASELINE.json configs[1])",
+                       "per_gpu_batch": batch, "n_limbs": n, "B": B, "plan": {"t4": C2["t4"], "t3": C2["t3"]},
+                       "levels": [{k: L[k] for k in ("B", "count", "n", "e")} for L in lv],
+                       "parallelism": f"batch-sharded x{world} (independent products, no collective)",
+                       "l2": "inputs 134 MB + workspace %.2f GB per step > 126 MB L2 (no flush needed)" % (plan["workspace_bytes"] / 1e9)},
+            "roofline": roofline,
+            "stages": stages,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "us_per_product": 1e3 * ms_per_step / batch,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

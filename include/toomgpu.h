@@ -1,0 +1,150 @@
+/*
+ * libtoomgpu -- B200-native (sm_100a) batched B-way Toom-Cook multiplication.
+ *
+ * The operation (§1, Eqs. 1.1-1.3): for unsigned integers u,
+ * v split into B blocks of b bits, u = U(2^b), v = V(2^b), compute
+ * w = u*v = W(2^b) by (1) evaluating U and V at 2B-1 small points,
+ * (2) forming the 2B-1 products y_k = U(x_k) V(x_k) recursively
+ * (Eq. 2.1; "lower-level products can also be done in parallel"),
+ * (3) interpolating W's coefficients with the even-odd method (§4,
+ * Eqs. 4.5-4.6) and the Newton listings with exact divisions (§3,
+ * PAPER.md:114-120, 154-158), (4) recomposing w = W(2^b) with carries.
+ *
+ * Conventions for every entry point:
+ *   - limbs are uint32_t, little-endian (the paper's 32-bit words);
+ *   - unless a name ends in _host, every pointer is a DEVICE pointer owned by
+ *     the caller; the library never frees caller memory;
+ *   - calls are asynchronous and ordered on `stream` (a cudaStream_t, NULL =
+ *     legacy default stream); argument errors return immediately, before any
+ *     work is enqueued;
+ *   - w must not overlap u or v (TOOM_EINVAL);
+ *   - the output is fixed length (nu+nv, or 2n per batched product), high
+ *     limbs zero, not normalized;
+ *   - no exceptions cross the ABI; all functions are thread-compatible
+ *     (one stream per host thread), not re-entrant on one stream.
+ *
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point returns TOOM_ECUDA.
+ */
+#ifndef TOOMGPU_H
+#define TOOMGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TOOM_OK = 0,
+    TOOM_EINVAL = 1,       /* bad argument (null pointer, aliasing, unsupported B, size) */
+    TOOM_EVERIFY = 2,      /* reserved: verification failure reported by a checker */
+    TOOM_EINEXACT = 3,     /* an exact division was not exact (exit code 3) */
+    TOOM_ENOMEM = 4,       /* device workspace allocation failed */
+    TOOM_ECUDA = 5,        /* a CUDA runtime error (no device, launch failure, ...) */
+    TOOM_EUNSUPPORTED = 6  /* the requested plan needs a path not built yet */
+} toom_status;
+
+/* Recursion plan (SURVEY.md §8 "reference shape"; SPEC.md:315-320 ToomPlan).
+ * top_B: B of the top level: 3 (points 0,1,-1,2,inf), 4 (0,+-1,+-2,1/2,inf)
+ *        or 8 (the paper's points 0,+-1,+-2,...,+-64);
+ * lower levels: Toom-4 while the operand has more than t4 limbs, Toom-3
+ *        while more than t3 limbs, schoolbook base case otherwise (<= 64 limbs);
+ * chunk: products per scheduling chunk (0 = automatic).                     */
+typedef struct {
+    int top_B;
+    size_t t4;
+    size_t t3;
+    size_t chunk;
+} toom_plan_t;
+
+/* Default plan for a given top B: t4 = 256, t3 = 64, chunk automatic. */
+toom_plan_t toom_default_plan(int B);
+
+/* w[i] = u[i] * v[i] for i < batch.
+ * u, v: [batch][n] uint32 (row-major, device); w: [batch][2n] (device).
+ * B: top-level B (see toom_plan_t).  n >= 1, batch >= 0 (batch 0: no-op).
+ * Errors: TOOM_EINVAL (null/aliasing/B), TOOM_ENOMEM, TOOM_ECUDA.           */
+toom_status toom_mul_batched(uint32_t *w, const uint32_t *u, const uint32_t *v,
+                             size_t n, size_t batch, int B, void *stream);
+
+/* As toom_mul_batched with an explicit plan (plan->top_B overrides B). */
+toom_status toom_mul_batched_plan(uint32_t *w, const uint32_t *u, const uint32_t *v,
+                                  size_t n, size_t batch, const toom_plan_t *plan,
+                                  void *stream);
+
+/* w[0 .. nu+nv) = u[0..nu) * v[0..nv) (device pointers).  nu, nv >= 0;
+ * zero-length operands are zero (w is zeroed).  The shorter operand is
+ * zero-padded to a common block width.                        */
+toom_status toom_mul(uint32_t *w, const uint32_t *u, size_t nu, const uint32_t *v, size_t nv,
+                     int B, void *stream);
+
+/* End-to-end variant with HOST buffers (pinned or pageable): copies u, v to
+ * the device, multiplies, copies w back, and synchronizes `stream` before
+ * returning.  Layouts as toom_mul_batched.                                 */
+toom_status toom_mul_batched_host(uint32_t *w_host, const uint32_t *u_host, const uint32_t *v_host,
+                                  size_t n, size_t batch, const toom_plan_t *plan, void *stream);
+
+/* Device workspace the batched call needs for this shape (bytes). */
+size_t toom_workspace_bytes(size_t n, size_t batch, const toom_plan_t *plan);
+
+/* Provide a caller-owned device workspace (NULL, 0 = let the library
+ * allocate and cache its own).  The library uses it until replaced.        */
+toom_status toom_set_workspace(void *dev_ptr, size_t bytes);
+
+/* Sticky status of the last failed call on this host thread (TOOM_OK if none);
+ * reading it clears it.                                                     */
+toom_status toom_last_error(void);
+
+/* Human-readable name of a status code (static string). */
+const char *toom_status_string(toom_status s);
+
+/* Number of kernels the last compute call launched (instrumentation for
+ * bench.py's "gpu_launches"). */
+size_t toom_last_launch_count(void);
+
+/* ---- instrumentation (bench.py) ---------------------------------------- */
+
+/* When enabled, every kernel the library launches on this host thread is
+ * bracketed by CUDA events on its stream (adds a little overhead; bench.py
+ * uses it in a separate pass after the timed region). */
+void toom_profile_enable(int on);
+
+/* Synchronizes the device and sums, per kernel category (0 evaluation,
+ * 1 base case, 2 interpolation+recomposition, 3 other), the event-timed
+ * milliseconds and launch counts recorded since the last collect.  Writes
+ * ncat entries; returns the number of categories the library knows. */
+int toom_profile_collect(double *ms, size_t *launches, int ncat);
+
+/* JSON description of the recursion plan for this shape (levels: B, count,
+ * n, b, e, Lw, npts; workspace bytes).  Writes at most len bytes to buf
+ * (NUL-terminated); returns the length needed including the NUL, 0 on error. */
+size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t *plan, char *buf, size_t len);
+
+/* Microbenchmark of the integer-MAD limb-product rate (the base case's inner
+ * operation: mad.lo.cc / madc.hi.cc / addc), used as the "alu" roofline
+ * peak.  Runs on `stream`, synchronizes, returns limb-products per second
+ * (and the elapsed ms in *ms), or a negative value on error. */
+double toom_probe_limb_products(double *ms, void *stream);
+
+/* ---- stage exports (tests, bench) ------------------------------------- */
+
+/* Base case alone (step a3): batched schoolbook of signed two's-complement
+ * operands.  u, v: INTERLEAVED [E][count] (limb-major: limb i of instance c
+ * at i*count + c), w: [2E][count] interleaved; 1 <= E <= 64.               */
+toom_status toom_base_interleaved(uint32_t *w, const uint32_t *u, const uint32_t *v,
+                                  size_t E, size_t count, void *stream);
+
+/* Evaluation alone (step a2) at the top level: for each of the `batch`
+ * unsigned operands a[batch][n], the 2B-1 values at the point set of B,
+ * written INTERLEAVED as out[e][npoints*batch] (value of point k of operand
+ * i at column k*batch + i), two's complement, e = toom_eval_width(n, B).    */
+toom_status toom_eval_top(uint32_t *out, const uint32_t *a, size_t n, size_t batch, int B, void *stream);
+size_t toom_eval_width(size_t n, int B);
+int toom_npoints(int B);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOOMGPU_H */

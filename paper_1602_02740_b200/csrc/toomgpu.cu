@@ -1,0 +1,836 @@
+// libtoomgpu: batched B-way Toom-Cook multiplication on B200 (sm_100a).
+//
+// Data path (DESIGN.md §"Kernels"):
+//   level 0 eval   k_eval<PS, TOP=true>   row-major u, v -> child operands   (step a1+a2)
+//   level l eval   k_eval<PS, TOP=false>  interleaved signed parents -> children
+//   base case      k_base<E>              register-resident schoolbook         (step a3)
+//   level l interp k_interp<PS, TOP>      2B-1 child products -> w_k -> parent (steps a4+a5)
+// All intermediate values live in device memory in an INTERLEAVED layout:
+// limb i of instance c of a level at [i * count + c], so that one thread per
+// instance reads and writes fully coalesced across a warp.  Values below the
+// top level are two's-complement integers (the evaluated values U(x_k) can
+// be negative, Eq. 4.4).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <vector>
+#include <mutex>
+#include <string>
+
+#include "../../include/toomgpu.h"
+#include "generated/toom_programs.cuh"
+
+namespace tg {
+
+// ------------------------------------------------------------------------
+// point-set descriptors (the programs themselves are generated, see
+// gen/toomgen.py).  ids: 0 = T3, 1 = T4, 2 = P8
+// ------------------------------------------------------------------------
+struct PSDesc {
+    int B;
+    int npts;
+    uint64_t S;   // max over points of sum_k |p^k q^(n-k)| (value growth factor)
+};
+
+static PSDesc ps_desc(int B) {
+    switch (B) {
+        case 3: return {3, 5, 7};          // points 0,1,-1,2,inf: S = 1+2+4
+        case 4: return {4, 7, 15};         // 0,+-1,+-2,1/2,inf: S = 1+2+4+8
+        case 8: {                          // 0,+-1,...,+-64: S = sum 64^k, k<8
+            uint64_t s = 0, p = 1;
+            for (int k = 0; k < 8; ++k) { s += p; p *= 64; }
+            return {8, 15, s};
+        }
+        default: return {0, 0, 0};
+    }
+}
+
+static int bitlen(uint64_t x) { int b = 0; while (x) { ++b; x >>= 1; } return b; }
+
+// ------------------------------------------------------------------------
+// accessors for the generated streaming programs
+// ------------------------------------------------------------------------
+
+// block k of a top-level (unsigned, row-major) operand row
+struct InTop {
+    const uint32_t* row;
+    int b, lentop, B;
+    __device__ __forceinline__ uint32_t load(int k, int t) const {
+        const int len = (k == B - 1) ? lentop : b;
+        return (t < len) ? __ldg(row + (size_t)k * b + t) : 0u;
+    }
+};
+
+// block k of a signed interleaved parent operand (top block sign-extended)
+struct InLevel {
+    const uint32_t* col;
+    size_t stride;
+    int b, lentop, B;
+    uint32_t fill;
+    __device__ __forceinline__ uint32_t load(int k, int t) const {
+        const int len = (k == B - 1) ? lentop : b;
+        if (t < len) return __ldg(col + (size_t)(k * b + t) * stride);
+        return (k == B - 1) ? fill : 0u;
+    }
+};
+
+struct OutInterleaved {
+    uint32_t* base;      // already offset by the instance column
+    size_t stride_limb;  // distance between limbs of one value
+    size_t stride_val;   // distance between consecutive values (points / coefficients)
+    __device__ __forceinline__ void store(int j, int t, uint32_t x) const {
+        base[(size_t)t * stride_limb + (size_t)j * stride_val] = x;
+    }
+};
+
+// the 2B-1 child products of one parent: y_k limb t at (t*stride_limb + k*stride_val)
+template <int NPTS>
+struct InProducts {
+    const uint32_t* base;
+    size_t stride_limb, stride_val;
+    int width;
+    uint32_t fill[NPTS];
+    __device__ __forceinline__ uint32_t load(int k, int t) const {
+        return (t < width) ? __ldg(base + (size_t)t * stride_limb + (size_t)k * stride_val) : fill[k];
+    }
+};
+
+// ------------------------------------------------------------------------
+// point-set dispatch to the generated programs
+// ------------------------------------------------------------------------
+template <int B> struct PS;
+template <> struct PS<3> {
+    static constexpr int npts = 5;
+    template <class I, class O> __device__ static void eval(const I& i, O& o, int n) { tg_eval_T3(i, o, n); }
+    template <class I, class O> __device__ static void interp(const I& i, O& o, int n) { tg_interp_T3(i, o, n); }
+};
+template <> struct PS<4> {
+    static constexpr int npts = 7;
+    template <class I, class O> __device__ static void eval(const I& i, O& o, int n) { tg_eval_T4(i, o, n); }
+    template <class I, class O> __device__ static void interp(const I& i, O& o, int n) { tg_interp_T4(i, o, n); }
+};
+template <> struct PS<8> {
+    static constexpr int npts = 15;
+    template <class I, class O> __device__ static void eval(const I& i, O& o, int n) { tg_eval_P8(i, o, n); }
+    template <class I, class O> __device__ static void interp_even(const I& i, O& o, int n) { tg_interp_P8_even(i, o, n); }
+    template <class I, class O> __device__ static void interp_odd(const I& i, O& o, int n) { tg_interp_P8_odd(i, o, n); }
+};
+
+// ------------------------------------------------------------------------
+// step a2: evaluation.  One thread per (instance, operand).
+//   TOP:   src = u or v row-major [count][n], unsigned
+//   !TOP:  src = interleaved [n][count] two's complement
+// out: interleaved [e][npts*count]; value of point k for instance c at column k*count + c
+// ------------------------------------------------------------------------
+template <int B, bool TOP>
+__global__ void __launch_bounds__(128) k_eval(const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV,
+                                              uint32_t* __restrict__ outU, uint32_t* __restrict__ outV,
+                                              size_t count, int n, int b, int e) {
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= 2 * count) return;
+    const int which = gid >= count;
+    const size_t c = which ? gid - count : gid;
+    const uint32_t* src = which ? srcV : srcU;
+    uint32_t* out = which ? outV : outU;
+    const int lentop = n - (B - 1) * b;
+    OutInterleaved o{out + c, (size_t)PS<B>::npts * count, count};
+    if (TOP) {
+        InTop in{src + c * (size_t)n, b, lentop, B};
+        PS<B>::eval(in, o, e);
+    } else {
+        const uint32_t top = __ldg(src + (size_t)(n - 1) * count + c);
+        InLevel in{src + c, count, b, lentop, B, (top >> 31) ? 0xFFFFFFFFu : 0u};
+        PS<B>::eval(in, o, e);
+    }
+}
+
+// ------------------------------------------------------------------------
+// step a3: base case.  Register-resident product-scanning (Comba) schoolbook
+// of two E-limb two's-complement operands; magnitudes multiplied with
+// mad.lo.cc / madc.hi.cc / addc carry chains (-> IMAD.WIDE.U32 + IADD3.X),
+// product sign applied while the columns are streamed out.
+// ------------------------------------------------------------------------
+#define TG_MADD(c0, c1, c2, a, b)                                    \
+    asm volatile("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"                 \
+                 "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"                \
+                 "addc.u32 %2, %2, 0;"                               \
+                 : "+r"(c0), "+r"(c1), "+r"(c2) : "r"(a), "r"(b))
+
+template <int E>
+__device__ __forceinline__ uint32_t load_abs(const uint32_t* __restrict__ src, size_t stride, uint32_t (&a)[E]) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) a[i] = __ldg(src + (size_t)i * stride);
+    const uint32_t neg = a[E - 1] >> 31;
+    const uint32_t mask = 0u - neg;
+    uint32_t carry = neg;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        const uint32_t x = (a[i] ^ mask) + carry;
+        carry = (x < carry) ? 1u : 0u;
+        a[i] = x;
+    }
+    return neg;
+}
+
+template <int E>
+__global__ void __launch_bounds__(128) k_base(const uint32_t* __restrict__ U, const uint32_t* __restrict__ V,
+                                              uint32_t* __restrict__ P, size_t count) {
+    const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    uint32_t a[E], b[E];
+    const uint32_t sa = load_abs<E>(U + c, count, a);
+    const uint32_t sb = load_abs<E>(V + c, count, b);
+    const uint32_t neg = sa ^ sb;
+    const uint32_t mask = 0u - neg;
+    uint32_t ncarry = neg;
+    uint32_t c0 = 0, c1 = 0, c2 = 0;
+    uint32_t* out = P + c;
+#pragma unroll
+    for (int k = 0; k < 2 * E - 1; ++k) {
+#pragma unroll
+        for (int i = (k < E ? 0 : k - E + 1); i <= (k < E ? k : E - 1); ++i) {
+            TG_MADD(c0, c1, c2, a[i], b[k - i]);
+        }
+        const uint32_t x = (c0 ^ mask) + ncarry;
+        ncarry = (x < ncarry) ? 1u : 0u;
+        out[(size_t)k * count] = x;
+        c0 = c1;
+        c1 = c2;
+        c2 = 0;
+    }
+    out[(size_t)(2 * E - 1) * count] = (c0 ^ mask) + ncarry;
+}
+
+// generic base case for 40 < E <= 64 (operands staged in local memory)
+__global__ void __launch_bounds__(128) k_base_generic(const uint32_t* __restrict__ U, const uint32_t* __restrict__ V,
+                                                      uint32_t* __restrict__ P, size_t count, int E) {
+    const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    uint32_t a[64], b[64];
+    uint32_t sgn[2];
+    for (int w = 0; w < 2; ++w) {
+        const uint32_t* src = (w ? V : U) + c;
+        uint32_t* d = w ? b : a;
+        for (int i = 0; i < E; ++i) d[i] = __ldg(src + (size_t)i * count);
+        const uint32_t neg = d[E - 1] >> 31, mask = 0u - neg;
+        uint32_t carry = neg;
+        for (int i = 0; i < E; ++i) {
+            const uint32_t x = (d[i] ^ mask) + carry;
+            carry = (x < carry) ? 1u : 0u;
+            d[i] = x;
+        }
+        sgn[w] = neg;
+    }
+    const uint32_t neg = sgn[0] ^ sgn[1], mask = 0u - neg;
+    uint32_t ncarry = neg, c0 = 0, c1 = 0, c2 = 0;
+    for (int k = 0; k < 2 * E - 1; ++k) {
+        const int lo = k < E ? 0 : k - E + 1, hi = k < E ? k : E - 1;
+        for (int i = lo; i <= hi; ++i) TG_MADD(c0, c1, c2, a[i], b[k - i]);
+        const uint32_t x = (c0 ^ mask) + ncarry;
+        ncarry = (x < ncarry) ? 1u : 0u;
+        P[(size_t)k * count + c] = x;
+        c0 = c1; c1 = c2; c2 = 0;
+    }
+    P[(size_t)(2 * E - 1) * count + c] = (c0 ^ mask) + ncarry;
+}
+
+// ------------------------------------------------------------------------
+// step a5: recomposition w = sum_j w_j 2^(32 b j) (Eq. 1.3) with carry
+// propagation.  w_j are two's-complement streams of Lw limbs (sign-extended
+// beyond); the sum is accumulated limb by limb with an unsigned 64-bit
+// accumulator (at most 2B-1 terms per limb), which is exact for infinite
+// two's-complement streams.
+// ------------------------------------------------------------------------
+template <int NPTS, bool TOP>
+__device__ __forceinline__ void recompose(const uint32_t* __restrict__ W, size_t count, int Lw, int b,
+                                          uint32_t* __restrict__ out, size_t out_stride, int wout) {
+    // W: this instance's column: w_j limb t at W[(j*Lw + t)*count]
+    uint32_t fillneg[NPTS];
+#pragma unroll
+    for (int j = 0; j < NPTS; ++j) fillneg[j] = W[((size_t)j * Lw + Lw - 1) * count] >> 31;
+    uint64_t carry = 0;
+    for (int P = 0; P < wout; ++P) {
+        uint64_t acc = carry;
+#pragma unroll
+        for (int j = 0; j < NPTS; ++j) {
+            const int t = P - j * b;
+            if (t >= 0) {
+                if (t < Lw) acc += W[((size_t)j * Lw + t) * count];
+                else acc += fillneg[j] ? 0xFFFFFFFFull : 0ull;
+            }
+        }
+        out[(size_t)P * out_stride] = (uint32_t)acc;
+        carry = acc >> 32;
+    }
+}
+
+// ------------------------------------------------------------------------
+// step a4 (+a5): interpolation of one parent per thread, then recomposition.
+//   Pc:  child products, interleaved [2e][npts*count] (point k of parent c at column k*count + c)
+//   W:   scratch [npts][Lw][count]
+//   out: TOP ? row-major w[count][wout] : interleaved [wout][count]
+// ------------------------------------------------------------------------
+template <int B, bool TOP>
+__global__ void __launch_bounds__(128) k_interp(const uint32_t* __restrict__ Pc, uint32_t* __restrict__ W,
+                                                uint32_t* __restrict__ out, size_t count, int ywidth,
+                                                int Lw, int b, int wout) {
+    constexpr int NP = PS<B>::npts;
+    const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    InProducts<NP> in;
+    in.base = Pc + c;
+    in.stride_limb = (size_t)NP * count;
+    in.stride_val = count;
+    in.width = ywidth;
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+        in.fill[k] = (__ldg(in.base + (size_t)(ywidth - 1) * in.stride_limb + (size_t)k * count) >> 31) ? 0xFFFFFFFFu : 0u;
+    OutInterleaved wo{W + c, count, (size_t)Lw * count};
+    PS<B>::interp(in, wo, Lw);
+    if (TOP) recompose<NP, true>(W + c, count, Lw, b, out + c * (size_t)wout, 1, wout);
+    else recompose<NP, false>(W + c, count, Lw, b, out + c, count, wout);
+}
+
+// P8 (the paper's points, 15 values): the even and odd halves are independent
+// and run on two adjacent lanes; the even lane recomposes.
+template <bool TOP>
+__global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ Pc, uint32_t* __restrict__ W,
+                                                   uint32_t* __restrict__ out, size_t count, int ywidth,
+                                                   int Lw, int b, int wout) {
+    constexpr int NP = 15;
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t c = gid >> 1;
+    const int half = (int)(gid & 1);
+    const bool active = c < count;
+    if (active) {
+        InProducts<NP> in;
+        in.base = Pc + c;
+        in.stride_limb = (size_t)NP * count;
+        in.stride_val = count;
+        in.width = ywidth;
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+            in.fill[k] = (__ldg(in.base + (size_t)(ywidth - 1) * in.stride_limb + (size_t)k * count) >> 31) ? 0xFFFFFFFFu : 0u;
+        OutInterleaved wo{W + c, count, (size_t)Lw * count};
+        if (half == 0) PS<8>::interp_even(in, wo, Lw);
+        else PS<8>::interp_odd(in, wo, Lw);
+    }
+    __syncwarp();
+    if (active && half == 0) {
+        if (TOP) recompose<NP, true>(W + c, count, Lw, b, out + c * (size_t)wout, 1, wout);
+        else recompose<NP, false>(W + c, count, Lw, b, out + c, count, wout);
+    }
+}
+
+// ------------------------------------------------------------------------
+// planner (step a6): the recursion shape and the workspace layout
+// ------------------------------------------------------------------------
+struct Level {
+    int B = 0;          // 0 = base case
+    size_t count = 0;   // instances at this level
+    int n = 0;          // operand width in limbs (unsigned at level 0, signed below)
+    int b = 0, lentop = 0;
+    int e = 0;          // child operand width
+    int Lw = 0;         // interpolation output width per coefficient
+    int npts = 0;
+    size_t offU = 0, offV = 0, offP = 0, offW = 0;   // child operands/products, this level's scratch
+};
+
+struct Plan {
+    std::vector<Level> lv;   // lv[0..L-1] Toom levels, lv[L] = base level
+    size_t bytes = 0;
+};
+
+static int choose_B(const toom_plan_t& p, int depth, int n) {
+    int B;
+    if (depth == 0 && p.top_B) B = p.top_B;
+    else if ((size_t)n > p.t4) B = 4;
+    else if ((size_t)n > p.t3) B = 3;
+    else return 0;
+    const int b = (n + B - 1) / B;
+    if (n < 2 * B || n - (B - 1) * b < 1) return 0;   // top block must be non-empty
+    return B;
+}
+
+static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& plan) {
+    plan.lv.clear();
+    size_t count = batch;
+    int width = n;
+    for (int depth = 0;; ++depth) {
+        Level L;
+        L.count = count;
+        L.n = width;
+        L.B = choose_B(p, depth, width);
+        if (L.B == 0) {
+            if (depth == 0 && p.top_B) return TOOM_EINVAL;
+            if (width > 64) return TOOM_EUNSUPPORTED;
+            plan.lv.push_back(L);
+            break;
+        }
+        const PSDesc d = ps_desc(L.B);
+        if (!d.B) return TOOM_EINVAL;
+        L.npts = d.npts;
+        L.b = (width + L.B - 1) / L.B;
+        L.lentop = width - (L.B - 1) * L.b;
+        L.e = L.b + (bitlen(d.S) + 1 + 31) / 32;
+        L.Lw = 2 * L.b + 1;
+        plan.lv.push_back(L);
+        count *= (size_t)d.npts;
+        width = L.e;
+        if (depth > 40) return TOOM_EUNSUPPORTED;
+    }
+    // workspace layout
+    size_t off = 0;
+    auto take = [&](size_t limbs) { size_t o = off; off += ((limbs * 4 + 255) / 256) * 256; return o; };
+    for (size_t l = 0; l + 1 < plan.lv.size(); ++l) {
+        Level& L = plan.lv[l];
+        const size_t cc = L.count * (size_t)L.npts;
+        L.offU = take((size_t)L.e * cc);
+        L.offV = take((size_t)L.e * cc);
+        L.offP = take((size_t)2 * L.e * cc);
+        L.offW = take((size_t)L.npts * L.Lw * L.count);
+    }
+    plan.bytes = off;
+    return TOOM_OK;
+}
+
+// ------------------------------------------------------------------------
+// workspace + error state
+// ------------------------------------------------------------------------
+static std::mutex g_ws_mu;
+static void* g_ws = nullptr;
+static size_t g_ws_bytes = 0;
+static bool g_ws_owned = true;
+static thread_local toom_status t_last = TOOM_OK;
+static thread_local size_t t_launches = 0;
+
+// ---- optional per-launch CUDA-event profiling (bench.py roofline) ----
+enum { CAT_EVAL = 0, CAT_BASE = 1, CAT_INTERP = 2, CAT_OTHER = 3, NCAT = 4 };
+struct ProfRec { int cat; cudaEvent_t a, b; };
+static thread_local bool t_prof = false;
+static thread_local std::vector<ProfRec> t_prof_recs;
+static thread_local std::vector<cudaEvent_t> t_prof_pool;
+static thread_local cudaStream_t t_prof_stream = nullptr;
+static cudaEvent_t prof_event() {
+    if (!t_prof_pool.empty()) { cudaEvent_t e = t_prof_pool.back(); t_prof_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+struct ProfScope {
+    bool on; ProfRec r;
+    ProfScope(int cat, cudaStream_t st) : on(t_prof) {
+        if (on) { r.cat = cat; r.a = prof_event(); r.b = prof_event(); cudaEventRecord(r.a, st); t_prof_stream = st; }
+    }
+    void done(cudaStream_t st) { if (on) { cudaEventRecord(r.b, st); t_prof_recs.push_back(r); on = false; } }
+};
+
+static toom_status fail(toom_status s) {
+    if (s != TOOM_OK) t_last = s;
+    return s;
+}
+
+static toom_status get_ws(size_t bytes, void** out) {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    if (bytes <= g_ws_bytes && g_ws) { *out = g_ws; return TOOM_OK; }
+    if (!g_ws_owned) return TOOM_ENOMEM;
+    if (g_ws) { cudaDeviceSynchronize(); cudaFree(g_ws); g_ws = nullptr; g_ws_bytes = 0; }
+    if (cudaMalloc(&g_ws, bytes) != cudaSuccess) { cudaGetLastError(); g_ws = nullptr; return TOOM_ENOMEM; }
+    g_ws_bytes = bytes;
+    *out = g_ws;
+    return TOOM_OK;
+}
+
+static inline unsigned nblk(size_t threads, int bs = 128) { return (unsigned)((threads + bs - 1) / bs); }
+
+static toom_status launch_eval(int B, bool top, const uint32_t* su, const uint32_t* sv, uint32_t* ou, uint32_t* ov,
+                               size_t count, int n, int b, int e, cudaStream_t st) {
+    const unsigned g = nblk(2 * count);
+    if (g == 0) return TOOM_OK;
+    ProfScope ps(CAT_EVAL, st);
+#define TG_EV(BB)                                                                          \
+    if (top) k_eval<BB, true><<<g, 128, 0, st>>>(su, sv, ou, ov, count, n, b, e);          \
+    else k_eval<BB, false><<<g, 128, 0, st>>>(su, sv, ou, ov, count, n, b, e);
+    switch (B) {
+        case 3: TG_EV(3); break;
+        case 4: TG_EV(4); break;
+        case 8: TG_EV(8); break;
+        default: return TOOM_EINVAL;
+    }
+#undef TG_EV
+    ps.done(st);
+    ++t_launches;
+    return TOOM_OK;
+}
+
+static toom_status launch_interp(int B, bool top, const uint32_t* Pc, uint32_t* W, uint32_t* out, size_t count,
+                                 int ywidth, int Lw, int b, int wout, cudaStream_t st) {
+    if (count == 0) return TOOM_OK;
+    ProfScope ps(CAT_INTERP, st);
+    switch (B) {
+        case 3:
+            if (top) k_interp<3, true><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
+            else k_interp<3, false><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
+            break;
+        case 4:
+            if (top) k_interp<4, true><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
+            else k_interp<4, false><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
+            break;
+        case 8:
+            if (top) k_interp_p8<true><<<nblk(2 * count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
+            else k_interp_p8<false><<<nblk(2 * count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
+            break;
+        default: return TOOM_EINVAL;
+    }
+    ps.done(st);
+    ++t_launches;
+    return TOOM_OK;
+}
+
+template <int E>
+static void launch_base_E(const uint32_t* U, const uint32_t* V, uint32_t* P, size_t count, cudaStream_t st) {
+    k_base<E><<<nblk(count), 128, 0, st>>>(U, V, P, count);
+}
+
+static toom_status launch_base(int E, const uint32_t* U, const uint32_t* V, uint32_t* P, size_t count, cudaStream_t st) {
+    if (count == 0) return TOOM_OK;
+    ProfScope ps(CAT_BASE, st);
+    switch (E) {
+#define TG_BC(k) case k: launch_base_E<k>(U, V, P, count, st); break;
+        TG_BC(1) TG_BC(2) TG_BC(3) TG_BC(4) TG_BC(5) TG_BC(6) TG_BC(7) TG_BC(8)
+        TG_BC(9) TG_BC(10) TG_BC(11) TG_BC(12) TG_BC(13) TG_BC(14) TG_BC(15) TG_BC(16)
+        TG_BC(17) TG_BC(18) TG_BC(19) TG_BC(20) TG_BC(21) TG_BC(22) TG_BC(23) TG_BC(24)
+        TG_BC(25) TG_BC(26) TG_BC(27) TG_BC(28) TG_BC(29) TG_BC(30) TG_BC(31) TG_BC(32)
+        TG_BC(33) TG_BC(34) TG_BC(35) TG_BC(36) TG_BC(37) TG_BC(38) TG_BC(39) TG_BC(40)
+#undef TG_BC
+        default:
+            if (E < 1 || E > 64) return TOOM_EINVAL;
+            k_base_generic<<<nblk(count), 128, 0, st>>>(U, V, P, count, E);
+    }
+    ps.done(st);
+    ++t_launches;
+    return TOOM_OK;
+}
+
+// base level reached directly (no Toom level): schoolbook on row-major
+// operands via a transposing copy
+__global__ void k_transpose_in(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t count, int n) {
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= count * (size_t)n) return;
+    const size_t c = gid / n;
+    const int i = (int)(gid % n);
+    dst[(size_t)i * count + c] = src[gid];
+}
+__global__ void k_transpose_out(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t count, int n2) {
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= count * (size_t)n2) return;
+    const size_t c = gid / n2;
+    const int i = (int)(gid % n2);
+    dst[gid] = src[(size_t)i * count + c];
+}
+
+static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, const uint32_t* v, int n, size_t batch,
+                            uint8_t* ws, cudaStream_t st) {
+    const size_t L = plan.lv.size() - 1;   // number of Toom levels
+    toom_status s;
+    if (L == 0) {
+        // schoolbook only (n <= 64 after planning)
+        uint32_t* tu = (uint32_t*)ws;
+        uint32_t* tv = tu + ((batch * n + 63) & ~(size_t)63);
+        uint32_t* tp = tv + ((batch * n + 63) & ~(size_t)63);
+        k_transpose_in<<<nblk(batch * n, 256), 256, 0, st>>>(u, tu, batch, n);
+        k_transpose_in<<<nblk(batch * n, 256), 256, 0, st>>>(v, tv, batch, n);
+        if ((s = launch_base(n, tu, tv, tp, batch, st))) return s;
+        k_transpose_out<<<nblk(batch * 2 * n, 256), 256, 0, st>>>(tp, w, batch, 2 * n);
+        t_launches += 3;
+        return TOOM_OK;
+    }
+    // down: evaluation
+    for (size_t l = 0; l < L; ++l) {
+        const Level& Lv = plan.lv[l];
+        const uint32_t* su = l == 0 ? u : (const uint32_t*)(ws + plan.lv[l - 1].offU);
+        const uint32_t* sv = l == 0 ? v : (const uint32_t*)(ws + plan.lv[l - 1].offV);
+        if ((s = launch_eval(Lv.B, l == 0, su, sv, (uint32_t*)(ws + Lv.offU), (uint32_t*)(ws + Lv.offV), Lv.count, Lv.n,
+                             Lv.b, Lv.e, st)))
+            return s;
+    }
+    // bottom: base case on level L-1's children
+    {
+        const Level& Lv = plan.lv[L - 1];
+        if ((s = launch_base(Lv.e, (const uint32_t*)(ws + Lv.offU), (const uint32_t*)(ws + Lv.offV),
+                             (uint32_t*)(ws + Lv.offP), Lv.count * Lv.npts, st)))
+            return s;
+    }
+    // up: interpolation + recomposition
+    for (size_t l = L; l-- > 0;) {
+        const Level& Lv = plan.lv[l];
+        uint32_t* out = l == 0 ? w : (uint32_t*)(ws + plan.lv[l - 1].offP);
+        if ((s = launch_interp(Lv.B, l == 0, (const uint32_t*)(ws + Lv.offP), (uint32_t*)(ws + Lv.offW), out, Lv.count,
+                               2 * Lv.e, Lv.Lw, Lv.b, 2 * Lv.n, st)))
+            return s;
+    }
+    return TOOM_OK;
+}
+
+static bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+    const char* x = (const char*)a;
+    const char* y = (const char*)b;
+    return x < y + bn && y < x + an;
+}
+
+static toom_status check_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return TOOM_ECUDA; }
+    return TOOM_OK;
+}
+
+static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
+                           const toom_plan_t& p, cudaStream_t st) {
+    t_launches = 0;
+    if (!w || !u || !v || n == 0 || n > (1u << 30)) return TOOM_EINVAL;
+    if (batch == 0) return TOOM_OK;
+    const size_t in_bytes = n * batch * 4, out_bytes = 2 * n * batch * 4;
+    if (overlaps(w, out_bytes, u, in_bytes) || overlaps(w, out_bytes, v, in_bytes)) return TOOM_EINVAL;
+    toom_status s = check_device();
+    if (s) return s;
+    size_t chunk = p.chunk ? p.chunk : batch;
+    if (chunk > batch) chunk = batch;
+    Plan plan;
+    if ((s = make_plan((int)n, chunk, p, plan))) return s;
+    size_t need = plan.bytes;
+    if (plan.lv.size() == 1) need = (2 * ((chunk * n + 63) & ~(size_t)63) + 2 * chunk * n) * 4;
+    void* ws = nullptr;
+    if ((s = get_ws(need, &ws))) return s;
+    for (size_t c0 = 0; c0 < batch; c0 += chunk) {
+        const size_t cnt = (batch - c0 < chunk) ? batch - c0 : chunk;
+        if (cnt != chunk) {
+            Plan p2;
+            if ((s = make_plan((int)n, cnt, p, p2))) return s;
+            if ((s = run_plan(p2, w + c0 * 2 * n, u + c0 * n, v + c0 * n, (int)n, cnt, (uint8_t*)ws, st))) return s;
+        } else {
+            if ((s = run_plan(plan, w + c0 * 2 * n, u + c0 * n, v + c0 * n, (int)n, cnt, (uint8_t*)ws, st))) return s;
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return TOOM_ECUDA;
+    return TOOM_OK;
+}
+
+__global__ void k_pad_copy(const uint32_t* __restrict__ src, size_t nsrc, uint32_t* __restrict__ dst, size_t ndst) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ndst) dst[i] = i < nsrc ? src[i] : 0u;
+}
+
+}  // namespace tg
+
+using namespace tg;
+
+extern "C" {
+
+toom_plan_t toom_default_plan(int B) {
+    toom_plan_t p;
+    p.top_B = B;
+    p.t4 = 256;
+    p.t3 = 64;
+    p.chunk = 0;
+    return p;
+}
+
+toom_status toom_mul_batched_plan(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
+                                  const toom_plan_t* plan, void* stream) {
+    if (!plan) return fail(TOOM_EINVAL);
+    return fail(batched(w, u, v, n, batch, *plan, (cudaStream_t)stream));
+}
+
+toom_status toom_mul_batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch, int B,
+                             void* stream) {
+    if (B != 3 && B != 4 && B != 8) return fail(TOOM_EINVAL);
+    toom_plan_t p = toom_default_plan(B);
+    return fail(batched(w, u, v, n, batch, p, (cudaStream_t)stream));
+}
+
+toom_status toom_mul(uint32_t* w, const uint32_t* u, size_t nu, const uint32_t* v, size_t nv, int B, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    t_launches = 0;
+    if (!w || (nu && !u) || (nv && !v)) return fail(TOOM_EINVAL);
+    if (B != 3 && B != 4 && B != 8) return fail(TOOM_EINVAL);
+    if ((nu && overlaps(w, (nu + nv) * 4, u, nu * 4)) || (nv && overlaps(w, (nu + nv) * 4, v, nv * 4)))
+        return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    if (nu == 0 || nv == 0) {
+        if (nu + nv) cudaMemsetAsync(w, 0, (nu + nv) * 4, st);
+        return fail(cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA);
+    }
+    const size_t n = nu > nv ? nu : nv;
+    toom_plan_t p = toom_default_plan(B);
+    if (choose_B(p, 0, (int)n) == 0) p.top_B = 0;   // too small for this B: lower levels' rule
+    // padded operands and a 2n-limb product buffer (separate allocation)
+    uint32_t *pu = nullptr, *pv = nullptr, *pw = nullptr;
+    if (cudaMallocAsync((void**)&pu, n * 4, st) != cudaSuccess || cudaMallocAsync((void**)&pv, n * 4, st) != cudaSuccess ||
+        cudaMallocAsync((void**)&pw, 2 * n * 4, st) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(TOOM_ENOMEM);
+    }
+    k_pad_copy<<<nblk(n, 256), 256, 0, st>>>(u, nu, pu, n);
+    k_pad_copy<<<nblk(n, 256), 256, 0, st>>>(v, nv, pv, n);
+    s = batched(pw, pu, pv, n, 1, p, st);
+    if (s == TOOM_OK) k_pad_copy<<<nblk(nu + nv, 256), 256, 0, st>>>(pw, nu + nv, w, nu + nv);
+    t_launches += 3;
+    cudaFreeAsync(pu, st);
+    cudaFreeAsync(pv, st);
+    cudaFreeAsync(pw, st);
+    if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+    return fail(s);
+}
+
+toom_status toom_mul_batched_host(uint32_t* w_host, const uint32_t* u_host, const uint32_t* v_host, size_t n,
+                                  size_t batch, const toom_plan_t* plan, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!w_host || !u_host || !v_host || !plan) return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    static std::mutex mu;
+    static uint32_t* dbuf = nullptr;
+    static size_t dbytes = 0;
+    std::lock_guard<std::mutex> g(mu);
+    const size_t need = 4 * n * batch * 4;
+    if (need > dbytes) {
+        if (dbuf) { cudaDeviceSynchronize(); cudaFree(dbuf); dbuf = nullptr; dbytes = 0; }
+        if (cudaMalloc((void**)&dbuf, need) != cudaSuccess) { cudaGetLastError(); return fail(TOOM_ENOMEM); }
+        dbytes = need;
+    }
+    uint32_t* du = dbuf;
+    uint32_t* dv = dbuf + n * batch;
+    uint32_t* dw = dbuf + 2 * n * batch;
+    if (cudaMemcpyAsync(du, u_host, n * batch * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(dv, v_host, n * batch * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return fail(TOOM_ECUDA);
+    s = batched(dw, du, dv, n, batch, *plan, st);
+    if (s) return fail(s);
+    if (cudaMemcpyAsync(w_host, dw, 2 * n * batch * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess) return fail(TOOM_ECUDA);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(TOOM_ECUDA);
+    return TOOM_OK;
+}
+
+size_t toom_workspace_bytes(size_t n, size_t batch, const toom_plan_t* plan) {
+    if (!plan || n == 0) return 0;
+    toom_plan_t p = *plan;
+    size_t chunk = p.chunk ? p.chunk : batch;
+    if (chunk > batch) chunk = batch;
+    Plan pl;
+    if (make_plan((int)n, chunk, p, pl) != TOOM_OK) return 0;
+    return pl.bytes;
+}
+
+toom_status toom_set_workspace(void* dev_ptr, size_t bytes) {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    if (g_ws_owned && g_ws) { cudaDeviceSynchronize(); cudaFree(g_ws); }
+    if (dev_ptr) { g_ws = dev_ptr; g_ws_bytes = bytes; g_ws_owned = false; }
+    else { g_ws = nullptr; g_ws_bytes = 0; g_ws_owned = true; }
+    return TOOM_OK;
+}
+
+toom_status toom_last_error(void) {
+    toom_status s = t_last;
+    t_last = TOOM_OK;
+    return s;
+}
+
+const char* toom_status_string(toom_status s) {
+    switch (s) {
+        case TOOM_OK: return "TOOM_OK";
+        case TOOM_EINVAL: return "TOOM_EINVAL";
+        case TOOM_EVERIFY: return "TOOM_EVERIFY";
+        case TOOM_EINEXACT: return "TOOM_EINEXACT";
+        case TOOM_ENOMEM: return "TOOM_ENOMEM";
+        case TOOM_ECUDA: return "TOOM_ECUDA";
+        case TOOM_EUNSUPPORTED: return "TOOM_EUNSUPPORTED";
+    }
+    return "unknown";
+}
+
+size_t toom_last_launch_count(void) { return t_launches; }
+
+toom_status toom_base_interleaved(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t E, size_t count,
+                                  void* stream) {
+    t_launches = 0;
+    if (!w || !u || !v || E < 1 || E > 64) return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    s = launch_base((int)E, u, v, w, count, (cudaStream_t)stream);
+    if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+    return fail(s);
+}
+
+int toom_npoints(int B) { return ps_desc(B).npts; }
+
+void toom_profile_enable(int on) {
+    t_prof = on != 0;
+}
+
+int toom_profile_collect(double* ms, size_t* launches, int ncat) {
+    for (int c = 0; c < ncat; ++c) { ms[c] = 0; launches[c] = 0; }
+    if (t_prof_stream || !t_prof_recs.empty()) cudaDeviceSynchronize();
+    for (auto& r : t_prof_recs) {
+        float t = 0;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        if (r.cat < ncat) { ms[r.cat] += t; launches[r.cat] += 1; }
+        t_prof_pool.push_back(r.a);
+        t_prof_pool.push_back(r.b);
+    }
+    t_prof_recs.clear();
+    return NCAT;
+}
+
+size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t* plan, char* buf, size_t len) {
+    if (!plan || n == 0) return 0;
+    Plan pl;
+    toom_plan_t p = *plan;
+    if (make_plan((int)n, batch, p, pl) != TOOM_OK) return 0;
+    std::string js = "{\"levels\": [";
+    for (size_t l = 0; l < pl.lv.size(); ++l) {
+        const Level& L = pl.lv[l];
+        char tmp[512];
+        snprintf(tmp, sizeof tmp,
+                 "%s{\"B\": %d, \"count\": %zu, \"n\": %d, \"b\": %d, \"lentop\": %d, \"e\": %d, \"Lw\": %d, \"npts\": %d}",
+                 l ? ", " : "", L.B, L.count, L.n, L.b, L.lentop, L.e, L.Lw, L.npts);
+        js += tmp;
+    }
+    char tail[128];
+    snprintf(tail, sizeof tail, "], \"workspace_bytes\": %zu}", pl.bytes);
+    js += tail;
+    if (buf && len) {
+        size_t k = js.size() < len - 1 ? js.size() : len - 1;
+        memcpy(buf, js.data(), k);
+        buf[k] = 0;
+    }
+    return js.size() + 1;
+}
+
+size_t toom_eval_width(size_t n, int B) {
+    const PSDesc d = ps_desc(B);
+    if (!d.B || n == 0) return 0;
+    const size_t b = (n + B - 1) / B;
+    return b + (bitlen(d.S) + 1 + 31) / 32;
+}
+
+toom_status toom_eval_top(uint32_t* out, const uint32_t* a, size_t n, size_t batch, int B, void* stream) {
+    t_launches = 0;
+    const PSDesc d = ps_desc(B);
+    if (!out || !a || !d.B || n < (size_t)(2 * B)) return fail(TOOM_EINVAL);
+    const int b = (int)((n + B - 1) / B);
+    if ((int)n - (B - 1) * b < 1) return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    const int e = (int)toom_eval_width(n, B);
+    // reuse the two-operand kernel with the same source twice: out gets both copies
+    // of the evaluation; only the first half (operand "u") is the requested output.
+    s = launch_eval(B, true, a, a, out, out, batch, (int)n, b, e, (cudaStream_t)stream);
+    if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+    return fail(s);
+}
+
+}  // extern "C"

@@ -1,0 +1,649 @@
+"""toomgen -- build-time generator of the straight-line streaming programs the
+CUDA kernels run for evaluation (step a2) and interpolation (step a4).
+
+This is PRODUCT build tooling (it emits csrc/generated/*.cuh); it shares
+nothing with oracle/.  It uses exact Python integers only to (1) derive each
+program from the paper's method and (2) prove, symbolically, that every
+division in the program is exact for every integer input and that the
+program returns exactly w_0..w_2n.
+
+Method (§3, §4, §6; SURVEY.md §8(c) readings 4, 5, 6, 12):
+  * evaluation at homogeneous points (p:q):  U(p,q) = sum_k u_k p^k q^(n-k);
+    for a +-pair the even and odd sums E, O are formed once and
+    U(+-p/q) = E +- O (Eq. 4.1, 4.3-4.4, SPEC eval_pair);
+  * interpolation:
+      1. even-odd split of each +-pair (Eqs. 4.5-4.6):
+         E = (y+ + y-)/2 = W_e part,  O = (y+ - y-)/2 = odd part;
+      2. even half: W_e(z) of degree n through nodes (0:1) [y_0],
+         (p^2:q^2) [E] and (1:0) [y_inf]; odd half: W_o(z) of degree n-1
+         through nodes (p^2:q^2) [O/(pq)] and the unpaired points, whose
+         even part is subtracted once the even coefficients are known;
+         for the paper's own point set the odd half is aligned as
+         x^2 W_o(x^2) with the extra point (0, 0);
+      3. each half: peel the node at infinity (leading coefficient),
+         substitute x = t/L (L = lcm of the node denominators) so that all
+         nodes are integers, run listing 1 (divided differences,
+         PAPER.md:114-120) and listing 2 (Newton -> monomial,
+         PAPER.md:154-158) unchanged, divide coefficient k by L^(m-k).
+  * every division by d = 2^s * o (o odd) is emitted as an exact 2-adic
+    division by o (multiply by o^-1 mod 2^32 with a borrow chain, ref [4])
+    followed by an exact right shift by s bits.
+
+Streaming model of the emitted code: every variable is an exact integer held
+as an infinite little-endian two's-complement stream of 32-bit limbs.  One
+loop step produces one limb of every variable, LSB first.  Linear
+combinations and 2-adic divisions are causal; a right shift by s = 32a + r
+bits needs a+1 limbs of look-ahead, so its output lags its input by a + (r>0)
+steps ("delay").  Operands of different delay are aligned with small register
+histories.  Because all values are exact integers, no width bookkeeping is
+needed: the first L limbs of an output are its two's-complement
+representation for any L.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from fractions import Fraction
+from math import gcd
+from functools import reduce
+import random
+
+# ----------------------------------------------------------------- point sets
+
+
+def _lcm(a, b):
+    return a * b // gcd(a, b)
+
+
+@dataclass
+class PointSet:
+    name: str
+    B: int
+    points: list          # list of (p, q), q >= 0, gcd(p, q) = 1; (1, 0) is infinity
+    mode: str = "h4"      # "h4" or "paper" (aligned odd half)
+
+    @property
+    def n(self):
+        return self.B - 1
+
+    @property
+    def npoints(self):
+        return len(self.points)
+
+
+def pointset_T3():
+    # {0, 1, -1, 2, inf}  (BASELINE.json configs[0])
+    return PointSet("T3", 3, [(0, 1), (1, 1), (-1, 1), (2, 1), (1, 0)])
+
+
+def pointset_T4():
+    # {0, +-1, +-2, 1/2 (homogeneous (1:2)), inf}  (BASELINE.json configs[1])
+    return PointSet("T4", 4, [(0, 1), (1, 1), (-1, 1), (2, 1), (-2, 1), (1, 2), (1, 0)])
+
+
+def pointset_paper(B):
+    # the paper's own points 0, +-1, +-2, ..., +-2^(n-1)  (§4)
+    pts = [(0, 1)]
+    for j in range(B - 1):
+        pts += [(1 << j, 1), (-(1 << j), 1)]
+    return PointSet(f"P{B}", B, pts, mode="paper")
+
+
+def pointset_T16_31():
+    """The 31-point set of configs[4] (SURVEY §8(c) reading 5): 0, inf and
+    the 29 smallest-height +-p/q (height max(|p|,q)); within a height by
+    min(|p|,q) ascending, |p| > q first, + before -; last point +2/5."""
+    cand = []
+    for h in range(1, 6):
+        fr = []
+        for p in range(0, h + 1):
+            for q in range(1, h + 1):
+                if max(p, q) != h or gcd(p, q) != 1 or p == 0:
+                    continue
+                fr.append((p, q))
+        fr.sort(key=lambda pq: (min(pq), 0 if pq[0] > pq[1] else 1))
+        for p, q in fr:
+            cand += [(p, q), (-p, q)]
+    pts = [(0, 1), (1, 0)] + cand[:29]
+    return PointSet("T16", 16, pts)
+
+
+# ------------------------------------------------------------ program model
+
+
+@dataclass
+class Term:
+    var: str
+    m: int          # small signed multiplier
+    s: int = 0      # left shift in bits (term = m * (var << s))
+
+
+@dataclass
+class Op:
+    dst: str
+    terms: list
+    odiv: int = 1   # exact division by this odd number
+    shr: int = 0    # then exact right shift by this many bits
+    note: str = ""
+
+
+@dataclass
+class Program:
+    name: str
+    inputs: list                         # input stream names, in accessor order
+    ops: list = field(default_factory=list)
+    outputs: list = field(default_factory=list)   # variable names, in output order
+    nunk: int = 0                        # number of unknowns the forms are over
+    forms: dict = field(default_factory=dict)     # var -> list[int] (linear form)
+
+    def add(self, dst, terms, d=1, note=""):
+        """dst = (sum m*var*2^s) / d, d > 0 integer; checks exactness of the
+        linear form symbolically and records the op."""
+        assert d > 0
+        s = (d & -d).bit_length() - 1
+        o = d >> s
+        form = [0] * self.nunk
+        for t in terms:
+            f = self.forms[t.var]
+            for j in range(self.nunk):
+                form[j] += t.m * (f[j] << t.s)
+        for j in range(self.nunk):
+            if form[j] % d:
+                raise AssertionError(f"{self.name}: inexact division by {d} in {dst} ({note})")
+            form[j] //= d
+        self.forms[dst] = form
+        self.ops.append(Op(dst, [Term(t.var, t.m, t.s) for t in terms if t.m != 0], o, s, note))
+        return dst
+
+
+def _norm_terms(terms):
+    """Merge identical (var, s) terms; drop zero multipliers; turn large
+    power-of-two multipliers into shifts (streams stay 32-bit per term)."""
+    acc = {}
+    for t in terms:
+        m, s = t.m, t.s
+        while m != 0 and m % 2 == 0 and abs(m) >= (1 << 20):
+            m //= 2
+            s += 1
+        acc[(t.var, s)] = acc.get((t.var, s), 0) + m
+    out = [Term(v, m, s) for (v, s), m in acc.items() if m != 0]
+    return out
+
+
+class _Gen:
+    def __init__(self, prog):
+        self.p = prog
+        self.k = 0
+
+    def new(self, base):
+        self.k += 1
+        return f"{base}_{self.k}"
+
+    def op(self, base, terms, d=1, note=""):
+        terms = _norm_terms(terms)
+        # a plain copy needs no op
+        if d == 1 and len(terms) == 1 and terms[0].m == 1 and terms[0].s == 0:
+            return terms[0].var
+        # factor d so that each emitted odd divisor fits one 32-bit word
+        s = (d & -d).bit_length() - 1
+        o = d >> s
+        if o < (1 << 32):
+            return self.p.add(self.new(base), terms, d, note)
+        # split o into word-sized factors (exact at every stage: all factors
+        # divide every coefficient of the form, checked by Program.add)
+        facs = _word_factors(o)
+        cur = self.p.add(self.new(base), terms, facs[0] << s, note)
+        for f in facs[1:]:
+            cur = self.p.add(self.new(base), [Term(cur, 1)], f, note + " (cont.)")
+        return cur
+
+
+def _word_factors(o):
+    fs = []
+    x = o
+    p = 3
+    primes = []
+    while p * p <= x:
+        while x % p == 0:
+            primes.append(p)
+            x //= p
+        p += 2
+    if x > 1:
+        primes.append(x)
+    cur = 1
+    for q in primes:
+        if cur * q >= (1 << 32):
+            fs.append(cur)
+            cur = 1
+        cur *= q
+    fs.append(cur)
+    return fs
+
+
+# ------------------------------------------------------------- evaluation
+
+
+def build_eval(ps: PointSet) -> Program:
+    """Evaluate the B blocks u_0..u_n at every point of ps (homogeneous),
+    sharing the even and odd sums of each +-pair (Eq. 4.1)."""
+    n = ps.n
+    prog = Program(f"eval_{ps.name}", [f"u{k}" for k in range(ps.B)], nunk=ps.B)
+    for k in range(ps.B):
+        prog.forms[f"u{k}"] = [1 if j == k else 0 for j in range(ps.B)]
+    g = _Gen(prog)
+    pts = ps.points
+    done = {}
+    for idx, (p, q) in enumerate(pts):
+        if idx in done:
+            continue
+        c = [p**k * q ** (n - k) for k in range(ps.B)]
+        partner = None
+        if p > 0:
+            for j2, (p2, q2) in enumerate(pts):
+                if p2 == -p and q2 == q:
+                    partner = j2
+        if partner is not None:
+            E = g.op("E", [Term(f"u{k}", c[k]) for k in range(0, ps.B, 2)], note=f"E({p}/{q})")
+            O = g.op("O", [Term(f"u{k}", c[k]) for k in range(1, ps.B, 2)], note=f"O({p}/{q})")
+            done[idx] = g.op("Up", [Term(E, 1), Term(O, 1)], note=f"U(+{p}/{q}) = E + O")
+            done[partner] = g.op("Um", [Term(E, 1), Term(O, -1)], note=f"U(-{p}/{q}) = E - O")
+        else:
+            done[idx] = g.op("U", [Term(f"u{k}", c[k]) for k in range(ps.B)], note=f"U({p}:{q})")
+    prog.outputs = [done[i] for i in range(len(pts))]
+    for i, (p, q) in enumerate(pts):
+        assert prog.forms[prog.outputs[i]] == [p**k * q ** (n - k) for k in range(ps.B)]
+    return prog
+
+
+# ---------------------------------------------------------- interpolation
+
+
+def _solve_half(g: _Gen, nodes, m, tag):
+    """nodes: list of (a, b, var) with homogeneous node (a:b) and var holding
+    P_h(a, b) = sum_k c_k a^k b^(m-k).  Returns vars c_0..c_m.  (H4 reading
+    + the paper's listings.)"""
+    assert len(nodes) == m + 1, (tag, len(nodes), m)
+    inf = [nd for nd in nodes if nd[1] == 0]
+    fin = [nd for nd in nodes if nd[1] != 0]
+    cm = None
+    if inf:
+        assert len(inf) == 1
+        cm = inf[0][2]                       # leading coefficient c_m
+        peeled = []
+        for a, b, v in fin:                  # (v - c_m a^m) / b = P'_h(a, b), degree m-1
+            nv = g.op(f"{tag}pk", [Term(v, 1), Term(cm, -(a**m))], b, note=f"peel inf at ({a}:{b})")
+            peeled.append((a, b, nv))
+        fin = peeled
+        m = m - 1
+    if m < 0:
+        return [cm]
+    L = reduce(_lcm, [b for _, b, _ in fin], 1)
+    pts = []
+    for a, b, v in fin:
+        t = a * (L // b)
+        f = (L // b) ** m
+        if f != 1:
+            v = g.op(f"{tag}sc", [Term(v, f)], note=f"scale (L/b)^m at t={t}")
+        pts.append((t, v))
+    pts.sort(key=lambda tv: tv[0])
+    x = [t for t, _ in pts]
+    coeff = [v for _, v in pts]
+    # listing 1: divided differences, in place, m descending
+    for k in range(1, m + 1):
+        for mm in range(m, k - 1, -1):
+            den = x[mm] - x[mm - k]
+            assert den > 0
+            coeff[mm] = g.op(f"{tag}a", [Term(coeff[mm], 1), Term(coeff[mm - 1], -1)], den,
+                             note=f"listing1 k={k} m={mm}: /(x[{mm}]-x[{mm - k}])")
+    # listing 2: Newton -> monomial
+    for mm in range(m - 1, -1, -1):
+        for k in range(mm, m):
+            if x[mm] != 0:
+                coeff[k] = g.op(f"{tag}b", [Term(coeff[k], 1), Term(coeff[k + 1], -x[mm])],
+                                note=f"listing2 m={mm} k={k}: -= x[{mm}]*coeff[{k + 1}]")
+    # undo the substitution x = t/L
+    res = []
+    for k in range(m + 1):
+        dk = L ** (m - k)
+        res.append(coeff[k] if dk == 1 else g.op(f"{tag}c", [Term(coeff[k], 1)], dk, note=f"/L^{m - k}"))
+    if cm is not None:
+        res.append(cm)
+    return res
+
+
+def build_interp(ps: PointSet) -> Program:
+    n = ps.n
+    d = 2 * n
+    pts = ps.points
+    prog = Program(f"interp_{ps.name}", [f"y{k}" for k in range(len(pts))], nunk=d + 1)
+    for k, (p, q) in enumerate(pts):
+        prog.forms[f"y{k}"] = [p**j * q ** (d - j) for j in range(d + 1)]
+    g = _Gen(prog)
+    zero = [k for k, pq in enumerate(pts) if pq == (0, 1)]
+    inf = [k for k, pq in enumerate(pts) if pq == (1, 0)]
+    pairs, unpaired = [], []
+    used = set(zero + inf)
+    for k, (p, q) in enumerate(pts):
+        if k in used or p <= 0:
+            continue
+        m = [j for j, pq in enumerate(pts) if pq == (-p, q)]
+        if m:
+            pairs.append((k, m[0], p, q))
+            used |= {k, m[0]}
+    unpaired = [k for k in range(len(pts)) if k not in used]
+
+    # 1. even-odd split (Eqs. 4.5-4.6)
+    EO = []
+    for kp, km, p, q in pairs:
+        E = g.op("E", [Term(f"y{kp}", 1), Term(f"y{km}", 1)], 2, note=f"W_e: (W({p}/{q})+W(-{p}/{q}))/2 (Eq. 4.5)")
+        EO.append((p, q, E, kp, km))
+
+    # 2. even half: c_k = w_{2k}, degree n
+    nodes = []
+    if zero:
+        nodes.append((0, 1, f"y{zero[0]}"))
+    for p, q, E, _, _ in EO:
+        nodes.append((p * p, q * q, E))
+    if inf:
+        nodes.append((1, 0, f"y{inf[0]}"))
+    even = _solve_half(g, nodes, n, "e")
+
+    # 3. odd half: c'_k = w_{2k+1}, degree n-1
+    if ps.mode == "paper":
+        assert not unpaired and not inf
+        # x^2 W_o(x^2) = x (W(x) - W(-x)) / 2, plus the point (0, 0)
+        nodes = []
+        for p, q, E, kp, km in EO:
+            assert q == 1
+            v = g.op("Ox", [Term(f"y{kp}", p), Term(f"y{km}", -p)], 2, note=f"x^2 W_o(x^2) at x={p} (Eq. 4.6 * x^2)")
+            nodes.append((p * p, 1, v))
+        # the extra point (0, 0): a zero stream
+        prog.forms["ZERO"] = [0] * (d + 1)
+        nodes.insert(0, (0, 1, "ZERO"))
+        odd_aligned = _solve_half(g, nodes, n, "o")
+        odd = odd_aligned[1:]      # "the resulting coefficients move one place higher"
+    else:
+        nodes = []
+        for p, q, E, kp, km in EO:
+            v = g.op("O", [Term(f"y{kp}", 1), Term(f"y{km}", -1)], 2 * p * q, note=f"W_o node: (W(+)-W(-))/(2pq) at {p}/{q}")
+            nodes.append((p * p, q * q, v))
+        for k in unpaired:
+            p, q = pts[k]
+            # y - even part, divided by p q: the odd polynomial's homogeneous value
+            terms = [Term(f"y{k}", 1)]
+            for kk in range(n + 1):
+                terms.append(Term(even[kk], -(p ** (2 * kk)) * q ** (d - 2 * kk)))
+            v = g.op("U", terms, p * q, note=f"unpaired {p}/{q}: (y - even part)/(pq)")
+            assert p > 0, "unpaired points must be positive"
+            nodes.append((p * p, q * q, v))
+        odd = _solve_half(g, nodes, n - 1, "o")
+
+    outs = []
+    for j in range(d + 1):
+        outs.append(even[j // 2] if j % 2 == 0 else odd[j // 2])
+    prog.outputs = outs
+    for j in range(d + 1):
+        f = prog.forms[outs[j]]
+        assert f == [1 if i == j else 0 for i in range(d + 1)], (ps.name, j, f)
+    return prog
+
+
+# --------------------------------------------------------- exact simulation
+
+
+def run_program(prog: Program, inputs: dict) -> list:
+    """Execute the program on exact Python ints (whole values, not streams)."""
+    env = dict(inputs)
+    env["ZERO"] = 0
+    for op in prog.ops:
+        s = 0
+        for t in op.terms:
+            s += t.m * (env[t.var] << t.s)
+        d = op.odiv << op.shr
+        assert s % d == 0, f"inexact {op.dst}"
+        env[op.dst] = s // d
+    return [env[v] for v in prog.outputs]
+
+
+def selfcheck(ps: PointSet, trials=20, bits=300, seed=1):
+    """Round trip on random signed block polynomials: eval -> products ->
+    interp must return the block convolution w_k = sum u_i v_j."""
+    rng = random.Random(seed)
+    ev, it = build_eval(ps), build_interp(ps)
+    for _ in range(trials):
+        U = [rng.randrange(-(1 << bits), 1 << bits) for _ in range(ps.B)]
+        V = [rng.randrange(-(1 << bits), 1 << bits) for _ in range(ps.B)]
+        EU = run_program(ev, {f"u{k}": U[k] for k in range(ps.B)})
+        EV = run_program(ev, {f"u{k}": V[k] for k in range(ps.B)})
+        Y = {f"y{k}": EU[k] * EV[k] for k in range(ps.npoints)}
+        W = run_program(it, Y)
+        conv = [sum(U[i] * V[k - i] for i in range(ps.B) if 0 <= k - i < ps.B) for k in range(2 * ps.B - 1)]
+        assert W == conv, ps.name
+    return True
+
+
+# ------------------------------------------------------------------ emitter
+
+
+def _inv32(o):
+    return pow(o, -1, 1 << 32)
+
+
+def _live_ops(prog, outputs):
+    need = set(outputs)
+    ops = []
+    for op in reversed(prog.ops):
+        if op.dst in need:
+            ops.append(op)
+            for t in op.terms:
+                need.add(t.var)
+    ops.reverse()
+    return ops
+
+
+def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None) -> str:
+    """Emit a __host__ __device__ template that streams the program LSB-first.
+
+    template <class In, class Out>
+    TG_HD void fname(const In& in, Out& out, int nsteps)
+
+    in.load(k, i)   -> uint32 limb i of input k (sign/zero extension done by In)
+    out.store(j, i, x) stores limb i of output j; called for i in [0, nsteps - delay_j),
+                    with i ascending; Out decides how many limbs to keep.
+    The function runs `nsteps + maxdelay` loop steps, so every output gets
+    exactly `nsteps` limbs.  constexpr `fname_maxdelay` is emitted too.
+    """
+    outputs = list(prog.outputs if outputs is None else outputs)
+    out_index = list(range(len(outputs))) if out_index is None else out_index
+    ops = _live_ops(prog, outputs)
+    for op in ops:
+        # 64-bit accumulator bound: |carry + sum m_j x_j| < 2^63 for 32-bit x_j
+        assert sum(abs(t.m) for t in op.terms) < (1 << 30), (prog.name, op.dst, op.terms)
+    delay = {v: 0 for v in prog.inputs}
+    delay["ZERO"] = 0
+    opD = {}
+    for op in ops:
+        D = max(delay[t.var] for t in op.terms)
+        opD[op.dst] = D
+        a, r = op.shr // 32, op.shr % 32
+        delay[op.dst] = D + a + (1 if r else 0)
+    # history needs: lag of each use
+    hist = {v: 0 for v in delay}
+
+    def lagof(var, D, s):
+        a, r = s // 32, s % 32
+        return D - delay[var] + a + (1 if r else 0)
+
+    for op in ops:
+        D = opD[op.dst]
+        for t in op.terms:
+            hist[t.var] = max(hist[t.var], lagof(t.var, D, t.s))
+    used_inputs = sorted({t.var for op in ops for t in op.terms if t.var in prog.inputs} |
+                         {v for v in outputs if v in prog.inputs}, key=lambda v: prog.inputs.index(v))
+    maxdelay = max([delay[v] for v in outputs] + [0])
+
+    def cname(v):
+        return v.replace("-", "m")
+
+    L = []
+    L.append(f"// generated by toomgen.py from {prog.name}; {len(ops)} ops, max delay {maxdelay}")
+    L.append(f"constexpr int {fname}_maxdelay = {maxdelay};")
+    L.append("template <class In, class Out>")
+    L.append(f"TG_HD TG_INLINE void {fname}(const In& in, Out& out, int nsteps) {{")
+    vars_all = used_inputs + [op.dst for op in ops]
+    for v in vars_all:
+        for h in range(1, hist[v] + 1):
+            L.append(f"  uint32_t {cname(v)}_h{h} = 0u;")
+    for op in ops:
+        L.append(f"  uint64_t {cname(op.dst)}_acc = 0ull;")
+        if op.odiv != 1:
+            L.append(f"  uint32_t {cname(op.dst)}_bor = 0u;")
+        if op.shr % 32:
+            L.append(f"  uint32_t {cname(op.dst)}_qp = 0u;")
+    L.append(f"  const int total = nsteps + {maxdelay};")
+    L.append("  #pragma unroll 1")
+    L.append("  for (int i = 0; i < total; ++i) {")
+    for v in used_inputs:
+        L.append(f"    const uint32_t {cname(v)}_h0 = in.load({prog.inputs.index(v)}, i);")
+    for op in ops:
+        D = opD[op.dst]
+        dn = cname(op.dst)
+        L.append(f"    // {op.dst} = ({' + '.join(f'{t.m}*{t.var}<<{t.s}' for t in op.terms)}) / {op.odiv << op.shr}   [{op.note}]")
+        L.append(f"    uint32_t {dn}_h0;")
+        L.append("    {")
+        L.append(f"      uint64_t lin = {dn}_acc;")
+        for t in op.terms:
+            lag = lagof(t.var, D, t.s)
+            a, r = t.s // 32, t.s % 32
+            vn = cname(t.var)
+            if t.var == "ZERO":
+                continue
+            if r == 0:
+                src = f"{vn}_h{lag}"
+            else:
+                # (x << s)[limb] = (x[limb-a] << r) | (x[limb-a-1] >> (32-r))
+                src = f"tg_shl_limb({vn}_h{lag}, {vn}_h{lag - 1}, {r})"
+            m = t.m
+            if m == 1:
+                L.append(f"      lin += (uint64_t){src};")
+            elif m == -1:
+                L.append(f"      lin -= (uint64_t){src};")
+            elif m > 0:
+                L.append(f"      lin += (uint64_t){m}u * (uint64_t){src};")
+            else:
+                L.append(f"      lin -= (uint64_t){-m}u * (uint64_t){src};")
+        L.append(f"      uint32_t t = (uint32_t)lin;")
+        L.append(f"      {dn}_acc = (uint64_t)((int64_t)lin >> 32);")
+        if op.odiv != 1:
+            L.append(f"      const uint32_t x = t - {dn}_bor;")
+            L.append(f"      const uint32_t b1 = (t < {dn}_bor) ? 1u : 0u;")
+            L.append(f"      t = x * 0x{_inv32(op.odiv):08X}u;   // * {op.odiv}^-1 mod 2^32")
+            L.append(f"      {dn}_bor = tg_mulhi(t, {op.odiv}u) + b1;")
+        r = op.shr % 32
+        if r:
+            L.append(f"      {dn}_h0 = tg_shr_limb({dn}_qp, t, {r});")
+            L.append(f"      {dn}_qp = t;")
+        else:
+            L.append(f"      {dn}_h0 = t;")
+        L.append("    }")
+    for j, v in zip(out_index, outputs):
+        dv = delay[v]
+        vn = cname(v)
+        if v == "ZERO":
+            L.append(f"    if (i < nsteps) out.store({j}, i, 0u);")
+        elif dv == 0:
+            L.append(f"    if (i < nsteps) out.store({j}, i, {vn}_h0);")
+        else:
+            L.append(f"    if (i >= {dv} && i - {dv} < nsteps) out.store({j}, i - {dv}, {vn}_h0);")
+    for v in vars_all:
+        for h in range(hist[v], 0, -1):
+            L.append(f"    {cname(v)}_h{h} = {cname(v)}_h{h - 1};")
+    L.append("  }")
+    L.append("}")
+    return "\n".join(L)
+
+
+def stats(prog: Program):
+    nterms = sum(len(op.terms) for op in prog.ops)
+    ndiv = sum(1 for op in prog.ops if op.odiv != 1)
+    nshr = sum(1 for op in prog.ops if op.shr)
+    return dict(ops=len(prog.ops), terms=nterms, odd_divisions=ndiv, shifts=nshr)
+
+
+HEADER = """// AUTO-GENERATED by paper_1602_02740_b200/gen/toomgen.py -- do not edit.
+// Streaming evaluation / interpolation programs (PAPER.md §3, §4, §6;
+// see toomgen.py docstring for the method and the streaming model).
+#pragma once
+#include <stdint.h>
+#ifndef TG_HD
+#  ifdef __CUDACC__
+#    define TG_HD __host__ __device__
+#    define TG_INLINE __forceinline__
+#  else
+#    define TG_HD
+#    define TG_INLINE inline
+#  endif
+#endif
+#ifndef TG_HELPERS_DEFINED
+#define TG_HELPERS_DEFINED
+TG_HD TG_INLINE uint32_t tg_mulhi(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+// limb of (x >> r) given consecutive limbs lo = x[i], hi = x[i+1], 0 < r < 32
+TG_HD TG_INLINE uint32_t tg_shr_limb(uint32_t lo, uint32_t hi, int r) {
+#ifdef __CUDA_ARCH__
+  return __funnelshift_r(lo, hi, r);
+#else
+  return (lo >> r) | (hi << (32 - r));
+#endif
+}
+// limb of (x << r) given lo = x[i-1], hi = x[i], 0 < r < 32
+TG_HD TG_INLINE uint32_t tg_shl_limb(uint32_t lo, uint32_t hi, int r) {
+#ifdef __CUDA_ARCH__
+  return __funnelshift_l(lo, hi, r);
+#else
+  return (hi << r) | (lo >> (32 - r));
+#endif
+}
+#endif
+"""
+
+
+def generate_all():
+    # T16 (31 points, C5's top level) runs through the long-vector path, not
+    # the streaming emitter (its multipliers exceed one word).
+    sets = [pointset_T3(), pointset_T4(), pointset_paper(8)]
+    parts = [HEADER]
+    meta = {}
+    for ps in sets:
+        selfcheck(ps, trials=8)
+        ev = build_eval(ps)
+        it = build_interp(ps)
+        parts.append(f"// ===== point set {ps.name}: B={ps.B}, points {ps.points}")
+        parts.append(f"constexpr int {ps.name}_B = {ps.B};")
+        parts.append(f"constexpr int {ps.name}_npoints = {ps.npoints};")
+        parts.append(emit_stream_function(ev, f"tg_eval_{ps.name}"))
+        parts.append(emit_stream_function(it, f"tg_interp_{ps.name}"))
+        # the two halves separately (independent, run in parallel)
+        d = 2 * ps.n
+        ev_idx = [j for j in range(d + 1) if j % 2 == 0]
+        od_idx = [j for j in range(d + 1) if j % 2 == 1]
+        parts.append(emit_stream_function(it, f"tg_interp_{ps.name}_even", [it.outputs[j] for j in ev_idx], ev_idx))
+        parts.append(emit_stream_function(it, f"tg_interp_{ps.name}_odd", [it.outputs[j] for j in od_idx], od_idx))
+        meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
+    return "\n\n".join(parts) + "\n", meta
+
+
+if __name__ == "__main__":
+    import json
+    import os
+    import sys
+    out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(os.path.dirname(__file__), "..", "csrc", "generated", "toom_programs.cuh")
+    code, meta = generate_all()
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    with open(out, "w") as f:
+        f.write(code)
+    print(json.dumps(meta, indent=1))

@@ -1,0 +1,232 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle,
+element by element on the same seeded inputs.  Integer work: the bar is
+bit-exact.  Run on a B200 with  python -m pytest tests -m gpu.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+tg = pytest.importorskip("paper_1602_02740_b200")
+I = synth.to_int
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: GPU tests must run on the B200 box")
+    tg.lib()
+
+
+PRIMES = None
+
+
+def primes():
+    global PRIMES
+    if PRIMES is None:
+        PRIMES = oracle.primes(synth.PRIME_SEED, 8)
+    return PRIMES
+
+
+def check_residues(u, v, w):
+    for p in primes():
+        assert oracle.residue(w, p) == oracle.residue(u, p) * oracle.residue(v, p) % p
+
+
+# ------------------------------------------------------------ stage a3 alone
+
+
+@pytest.mark.parametrize("E", [1, 2, 5, 17, 18, 23, 33, 40, 41, 64])
+def test_base_case_signed_interleaved(E):
+    rng = np.random.default_rng(E)
+    count = 1000 + E
+    a = rng.integers(0, 2**32, (E, count), dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 2**32, (E, count), dtype=np.uint64).astype(np.uint32)
+    a[:, 0] = 0xFFFFFFFF            # -1
+    b[:, 1] = 0                     # 0
+    a[:, 2] = 0
+    a[E - 1, 2] = 0x80000000        # most negative
+    b[:, 2] = a[:, 2]
+    w = host(tg.base_interleaved(dev(a), dev(b)))
+
+    def sval(col):
+        x = I(col)
+        return x - (1 << (32 * len(col))) if x >> (32 * len(col) - 1) else x
+
+    for c in list(range(8)) + list(rng.integers(0, count, 64)):
+        x, y = sval(a[:, c]), sval(b[:, c])
+        # oracle: schoolbook on the magnitudes, sign applied
+        mag = I(oracle.schoolbook(synth.from_int(abs(x), E), synth.from_int(abs(y), E)))
+        want = mag if (x < 0) == (y < 0) else -mag
+        assert sval(w[:, c]) == want
+
+
+# ------------------------------------------------------------ stage a2 alone
+
+
+@pytest.mark.parametrize("B,n", [(3, 96), (4, 256), (4, 250), (8, 2048), (3, 7), (8, 100)])
+def test_eval_top_matches_definition(B, n):
+    pts = {3: [(0, 1), (1, 1), (-1, 1), (2, 1), (1, 0)],
+           4: [(0, 1), (1, 1), (-1, 1), (2, 1), (-2, 1), (1, 2), (1, 0)],
+           8: [(0, 1)] + [(s * (1 << j), 1) for j in range(7) for s in (1, -1)]}[B]
+    batch = 37
+    u, _ = synth.config_inputs(2, batch=batch)
+    u = np.ascontiguousarray(np.resize(u, (batch, n)))
+    u[0] = 0xFFFFFFFF
+    out = host(tg.eval_top(dev(u), B))
+    e = out.shape[0]
+    b = -(-n // B)
+    for i in (0, 1, batch - 1):
+        blocks = [I(u[i, k * b:min(n, (k + 1) * b)]) for k in range(B)]
+        for k, (p, q) in enumerate(pts):
+            want = sum(x * p**j * q ** (B - 1 - j) for j, x in enumerate(blocks))
+            col = out[:, k * batch + i]
+            got = I(col)
+            if got >> (32 * e - 1):
+                got -= 1 << (32 * e)
+            assert got == want
+
+
+# ------------------------------------------------------------ configs
+
+
+def run_batched(u, v, B, t4=256, t3=64, chunk=0):
+    w = tg.toom_mul_batched(dev(u), dev(v), B=B, t4=t4, t3=t3, chunk=chunk)
+    torch.cuda.synchronize()
+    return host(w)
+
+
+def test_c1_full_bit_exact():
+    u, v = synth.config_inputs(1)
+    w = run_batched(u, v, 3, t4=10**9, t3=10**9)       # one Toom-3 level, schoolbook base
+    want = oracle.toom_batched(u, v, top_B=3, t4=10**9, t3=64, threads=8)
+    assert np.array_equal(w, want)
+    # edge pairs (SURVEY §8(c) reading 16): closed forms
+    for k, expect in enumerate([(2**3072 - 1) ** 2, 0, 1, 2**6142]):
+        assert I(w[256 + k]) == expect
+
+
+C2_PLAN = dict(t4=32, t3=32)   # "Toom-4 ... recursing to a 32-limb schoolbook base"
+
+
+def test_c2_slice_bit_exact():
+    u, v = synth.config_inputs(2, batch=3000, first=1000)
+    w = run_batched(u, v, 4, **C2_PLAN)
+    want = oracle.toom_batched(u, v, top_B=4, threads=8)
+    assert np.array_equal(w, want)
+
+
+def test_c2_full_batch_sampled_and_residues():
+    # the bench launch configuration: all 65536 products in one call
+    u, v = synth.config_inputs(2)
+    w = run_batched(u, v, 4, **C2_PLAN)
+    rng = np.random.default_rng(2)
+    idx = np.unique(np.concatenate([[0, 65535], rng.integers(0, 65536, 254)]))
+    want = oracle.toom_batched(u[idx], v[idx], top_B=4, threads=8)
+    assert np.array_equal(w[idx], want)
+    for i in rng.integers(0, 65536, 64):
+        check_residues(u[i], v[i], w[i])
+
+
+def test_c2_chunked_equals_unchunked():
+    u, v = synth.config_inputs(2, batch=5000)
+    a = run_batched(u, v, 4, **C2_PLAN)
+    b = run_batched(u, v, 4, chunk=1024, **C2_PLAN)
+    assert np.array_equal(a, b)
+
+
+def test_c3_classes_closed_forms_and_oracle():
+    u, v = synth.config_inputs(3)
+    w = run_batched(u, v, 8)
+    n, N = 2048, 65536
+    ones = (1 << (2 * N)) - (1 << (N + 1)) + 1
+    for i in range(0, 1024, 97):
+        assert I(w[i]) == ones
+    alt_u = I(u[1024])
+    for i in range(1024, 2048, 101):
+        assert (2**32 + 1) ** 2 * I(w[i]) == 2**64 * (2**N - 1) ** 2
+        assert I(w[i]) == alt_u * alt_u
+    for i in range(2048, 3072, 37):
+        a, c = synth.c3_bits(synth.seed_for(3), i)
+        assert I(w[i]) == 1 << (a + c)
+    sample = list(range(3072, 4096, 64)) + [4095]
+    want = oracle.toom_batched(u[sample], v[sample], top_B=8, threads=8)
+    assert np.array_equal(w[sample], want)
+    # every product: residues mod 8 seeded 61-bit primes
+    for i in range(0, 4096, 7):
+        check_residues(u[i], v[i], w[i])
+
+
+def test_c3_small_slice_bit_exact_all_classes():
+    idx = [0, 1, 1024, 1025, 2048, 2049, 4094, 4095]
+    u, v = synth.config_inputs(3)
+    u, v = u[idx], v[idx]
+    w = run_batched(u, v, 8)
+    assert np.array_equal(w, oracle.toom_batched(u, v, top_B=8, threads=8))
+
+
+# ------------------------------------------------------------ edge cases
+
+
+@pytest.mark.parametrize("B", [3, 4, 8])
+@pytest.mark.parametrize("n", [16, 17, 31, 65, 100, 129, 257, 300])
+def test_ragged_sizes(B, n):
+    if n < 2 * B:
+        pytest.skip("below the smallest Toom split")
+    rng = np.random.default_rng(n * 10 + B)
+    batch = 33
+    u = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    v = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    u[0] = 0xFFFFFFFF
+    v[0] = 0xFFFFFFFF
+    u[1] = 0
+    for t4, t3 in [(256, 64), (8, 8)]:
+        w = run_batched(u, v, B, t4=t4, t3=t3)
+        assert np.array_equal(w, oracle.schoolbook_batched(u, v)), (B, n, t4, t3)
+
+
+def test_empty_batch_and_errors():
+    u = torch.zeros((0, 96), dtype=torch.uint32, device="cuda")
+    w = tg.toom_mul_batched(u, u, B=3)
+    assert w.shape == (0, 192)
+    x = torch.zeros((4, 96), dtype=torch.uint32, device="cuda")
+    with pytest.raises(tg.ToomError) as ei:
+        tg.toom_mul_batched(x, x, B=5)
+    assert ei.value.status == tg.TOOM_EINVAL
+    with pytest.raises(tg.ToomError):
+        tg.toom_mul_batched(x, x, B=3, out=x.view(2, 192))   # aliasing
+    with pytest.raises(TypeError):
+        tg.toom_mul_batched(x.cpu(), x.cpu(), B=3)            # no CPU fallback
+
+
+def test_toom_mul_unbalanced_and_zero_length():
+    rng = np.random.default_rng(9)
+    for nu, nv in [(300, 120), (97, 1000), (1, 64), (500, 500)]:
+        a = rng.integers(0, 2**32, nu, dtype=np.uint64).astype(np.uint32)
+        b = rng.integers(0, 2**32, nv, dtype=np.uint64).astype(np.uint32)
+        for B in (3, 4, 8):
+            w = host(tg.toom_mul(dev(a), dev(b), B=B))
+            assert np.array_equal(w, oracle.schoolbook(a, b))
+    z = torch.zeros(0, dtype=torch.uint32, device="cuda")
+    a = dev(np.arange(5, dtype=np.uint32))
+    assert not host(tg.toom_mul(a, z, B=4)).any()
+
+
+@pytest.mark.slow
+def test_c4_single_large_product():
+    u, v = synth.config_inputs(4)
+    w = host(tg.toom_mul(dev(u), dev(v), B=4))
+    check_residues(u, v, w)
+    assert np.array_equal(w, oracle.toom(u, v))
