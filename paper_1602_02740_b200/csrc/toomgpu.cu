@@ -246,23 +246,61 @@ __global__ void __launch_bounds__(128) k_base_generic(const uint32_t* __restrict
 template <int NPTS, bool TOP>
 __device__ __forceinline__ void recompose(const uint32_t* __restrict__ W, size_t count, int Lw, int b,
                                           uint32_t* __restrict__ out, size_t out_stride, int wout) {
-    // W: this instance's column: w_j limb t at W[(j*Lw + t)*count]
-    uint32_t fillneg[NPTS];
+    // W: this instance's column: w_j limb t at W[(j*Lw + t)*count]; Lw = 2b+1.
+    // Output limb P = s*b + r receives w_s[r], w_{s-1}[b+r], w_{s-2}[2b] (r = 0
+    // only) and the sign fills of every w_j with j <= s-2 that has ended.
+    uint32_t negfill[NPTS];
 #pragma unroll
-    for (int j = 0; j < NPTS; ++j) fillneg[j] = W[((size_t)j * Lw + Lw - 1) * count] >> 31;
+    for (int j = 0; j < NPTS; ++j) negfill[j] = W[((size_t)j * Lw + Lw - 1) * count] >> 31;
+    const size_t sj = (size_t)Lw * count;
     uint64_t carry = 0;
-    for (int P = 0; P < wout; ++P) {
-        uint64_t acc = carry;
+    uint32_t lowfills = 0;   // number of negative w_j with j <= s-3
+    const int nseg = (wout + b - 1) / b;
+    for (int s = 0; s < nseg; ++s) {
+        const bool hasA = s < NPTS, hasB = s >= 1 && s - 1 < NPTS, hasC = s >= 2 && s - 2 < NPTS;
+        const uint32_t* pA = W + (size_t)(hasA ? s : 0) * sj;
+        const uint32_t* pB = W + (size_t)(hasB ? s - 1 : 0) * sj + (size_t)b * count;
+        uint32_t fillC = 0;
+        if (hasC) {
 #pragma unroll
-        for (int j = 0; j < NPTS; ++j) {
-            const int t = P - j * b;
-            if (t >= 0) {
-                if (t < Lw) acc += W[((size_t)j * Lw + t) * count];
-                else acc += fillneg[j] ? 0xFFFFFFFFull : 0ull;
+            for (int j = 0; j < NPTS; ++j) if (j == s - 2) fillC = negfill[j];
+        }
+        const uint64_t lowconst = (uint64_t)lowfills * 0xFFFFFFFFull;
+        const int rmax = min(b, wout - s * b);
+        // r = 0: w_{s-2}[2b] is the last limb of w_{s-2}
+        int r = 0;
+        {
+            uint64_t acc = carry + lowconst;
+            if (hasA) acc += pA[0];
+            if (hasB) acc += pB[0];
+            if (hasC) acc += W[(size_t)(s - 2) * sj + (size_t)(2 * b) * count];
+            out[(size_t)(s * b) * out_stride] = (uint32_t)acc;
+            carry = acc >> 32;
+            r = 1;
+        }
+        const uint64_t cconst = lowconst + (fillC ? 0xFFFFFFFFull : 0ull);
+        for (; r + 4 <= rmax; r += 4) {
+            uint32_t a[4], bb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a[q] = hasA ? pA[(size_t)(r + q) * count] : 0u;
+                bb[q] = hasB ? pB[(size_t)(r + q) * count] : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t acc = carry + cconst + a[q] + bb[q];
+                out[(size_t)(s * b + r + q) * out_stride] = (uint32_t)acc;
+                carry = acc >> 32;
             }
         }
-        out[(size_t)P * out_stride] = (uint32_t)acc;
-        carry = acc >> 32;
+        for (; r < rmax; ++r) {
+            uint64_t acc = carry + cconst;
+            if (hasA) acc += pA[(size_t)r * count];
+            if (hasB) acc += pB[(size_t)r * count];
+            out[(size_t)(s * b + r) * out_stride] = (uint32_t)acc;
+            carry = acc >> 32;
+        }
+        if (hasC) lowfills += fillC;
     }
 }
 
@@ -343,14 +381,21 @@ struct Plan {
     size_t bytes = 0;
 };
 
+static bool split_ok(int n, int B) {
+    const int b = (n + B - 1) / B;
+    return n >= 2 * B && n - (B - 1) * b >= 1;   // top block must be non-empty
+}
+
+// B of the level at `depth` for an n-limb operand (0 = schoolbook base case).
+// A requested top-level B that cannot split n (top block empty) falls back to
+// the lower levels' size rule.
 static int choose_B(const toom_plan_t& p, int depth, int n) {
+    if (depth == 0 && p.top_B && split_ok(n, p.top_B)) return p.top_B;
     int B;
-    if (depth == 0 && p.top_B) B = p.top_B;
-    else if ((size_t)n > p.t4) B = 4;
+    if ((size_t)n > p.t4) B = 4;
     else if ((size_t)n > p.t3) B = 3;
     else return 0;
-    const int b = (n + B - 1) / B;
-    if (n < 2 * B || n - (B - 1) * b < 1) return 0;   // top block must be non-empty
+    if (!split_ok(n, B)) return (B == 4 && split_ok(n, 3)) ? 3 : 0;
     return B;
 }
 
@@ -364,7 +409,6 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         L.n = width;
         L.B = choose_B(p, depth, width);
         if (L.B == 0) {
-            if (depth == 0 && p.top_B) return TOOM_EINVAL;
             if (width > 64) return TOOM_EUNSUPPORTED;
             plan.lv.push_back(L);
             break;
@@ -666,7 +710,6 @@ toom_status toom_mul(uint32_t* w, const uint32_t* u, size_t nu, const uint32_t* 
     }
     const size_t n = nu > nv ? nu : nv;
     toom_plan_t p = toom_default_plan(B);
-    if (choose_B(p, 0, (int)n) == 0) p.top_B = 0;   // too small for this B: lower levels' rule
     // padded operands and a 2n-limb product buffer (separate allocation)
     uint32_t *pu = nullptr, *pv = nullptr, *pw = nullptr;
     if (cudaMallocAsync((void**)&pu, n * 4, st) != cudaSuccess || cudaMallocAsync((void**)&pv, n * 4, st) != cudaSuccess ||

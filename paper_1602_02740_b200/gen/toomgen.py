@@ -440,33 +440,90 @@ def _live_ops(prog, outputs):
     return ops
 
 
-def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None) -> str:
+def fuse_single_use(prog: Program, max_mult=1 << 24) -> Program:
+    """Inline every op whose result is used exactly once (and is not an
+    output) into its consumer:  Y = (c*X*2^t + R)/dY with X = N_X/dX  becomes
+    Y = (c*2^t*N_X + dX*R)/(dX*dY).  The merged op is re-checked for exactness
+    by Program.add's symbolic form test; merges that would need a divisor odd
+    part >= 2^32 or multipliers above `max_mult` are skipped."""
+    ops = list(prog.ops)
+    changed = True
+    while changed:
+        changed = False
+        uses = {}
+        for op in ops:
+            for t in op.terms:
+                uses[t.var] = uses.get(t.var, 0) + 1
+        outs = set(prog.outputs)
+        byname = {op.dst: op for op in ops}
+        for y in ops:
+            for t in y.terms:
+                x = byname.get(t.var)
+                if x is None or t.var in outs or uses.get(t.var, 0) != 1:
+                    continue
+                dX = x.odiv << x.shr
+                terms = []
+                for u in y.terms:
+                    if u is t:
+                        for a in x.terms:
+                            terms.append(Term(a.var, t.m * a.m, t.s + a.s))
+                    else:
+                        terms.append(Term(u.var, u.m * dX, u.s))
+                terms = _norm_terms(terms)
+                o = x.odiv * y.odiv
+                if o >= (1 << 32) or any(abs(u.m) > max_mult for u in terms):
+                    continue
+                if sum(abs(u.m) for u in terms) >= (1 << 30):
+                    continue
+                # exactness re-check through the symbolic forms
+                form = [0] * prog.nunk
+                for u in terms:
+                    f = prog.forms[u.var]
+                    for j in range(prog.nunk):
+                        form[j] += u.m * (f[j] << u.s)
+                d = (o << (x.shr + y.shr))
+                if any(v % d for v in form) or [v // d for v in form] != prog.forms[y.dst]:
+                    continue
+                new = Op(y.dst, terms, o, x.shr + y.shr, y.note + " <- " + x.note)
+                ops = [new if op is y else op for op in ops if op is not x]
+                changed = True
+                break
+            if changed:
+                break
+    out = Program(prog.name, prog.inputs, ops, prog.outputs, prog.nunk, prog.forms)
+    return out
+
+
+def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None, prefetch=2) -> str:
     """Emit a __host__ __device__ template that streams the program LSB-first.
 
     template <class In, class Out>
     TG_HD void fname(const In& in, Out& out, int nsteps)
 
     in.load(k, i)   -> uint32 limb i of input k (sign/zero extension done by In)
-    out.store(j, i, x) stores limb i of output j; called for i in [0, nsteps - delay_j),
-                    with i ascending; Out decides how many limbs to keep.
-    The function runs `nsteps + maxdelay` loop steps, so every output gets
-    exactly `nsteps` limbs.  constexpr `fname_maxdelay` is emitted too.
+                       (called for i up to nsteps + maxdelay + prefetch)
+    out.store(j, i, x) stores limb i of output j; called for i in [0, nsteps),
+                    with i ascending.
+    Inputs are software-prefetched `prefetch` steps ahead in registers so the
+    global-memory latency overlaps the arithmetic of the current step.
+    Per op:  lin (int64, two's complement in a uint64) = carry + sum m_j x_j,
+    one IMAD.WIDE.U32 per positive term (tg_madw), IMAD.WIDE + IADD per
+    negative term; t = lo(lin), carry = lin >> 32 (arithmetic); then the 2-adic
+    exact division by the odd part and the funnel-shift right.
     """
     outputs = list(prog.outputs if outputs is None else outputs)
     out_index = list(range(len(outputs))) if out_index is None else out_index
     ops = _live_ops(prog, outputs)
     for op in ops:
-        # 64-bit accumulator bound: |carry + sum m_j x_j| < 2^63 for 32-bit x_j
         assert sum(abs(t.m) for t in op.terms) < (1 << 30), (prog.name, op.dst, op.terms)
     delay = {v: 0 for v in prog.inputs}
     delay["ZERO"] = 0
     opD = {}
     for op in ops:
-        D = max(delay[t.var] for t in op.terms)
+        D = max(delay[t.var] for t in op.terms) if op.terms else 0
         opD[op.dst] = D
         a, r = op.shr // 32, op.shr % 32
         delay[op.dst] = D + a + (1 if r else 0)
-    # history needs: lag of each use
     hist = {v: 0 for v in delay}
 
     def lagof(var, D, s):
@@ -499,11 +556,20 @@ def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None
             L.append(f"  uint32_t {cname(op.dst)}_bor = 0u;")
         if op.shr % 32:
             L.append(f"  uint32_t {cname(op.dst)}_qp = 0u;")
+    # prefetch registers
+    for v in used_inputs:
+        k = prog.inputs.index(v)
+        for p in range(prefetch):
+            L.append(f"  uint32_t {cname(v)}_pf{p} = in.load({k}, {p});")
     L.append(f"  const int total = nsteps + {maxdelay};")
     L.append("  #pragma unroll 1")
     L.append("  for (int i = 0; i < total; ++i) {")
     for v in used_inputs:
-        L.append(f"    const uint32_t {cname(v)}_h0 = in.load({prog.inputs.index(v)}, i);")
+        k = prog.inputs.index(v)
+        L.append(f"    const uint32_t {cname(v)}_h0 = {cname(v)}_pf0;")
+        for p in range(prefetch - 1):
+            L.append(f"    {cname(v)}_pf{p} = {cname(v)}_pf{p + 1};")
+        L.append(f"    {cname(v)}_pf{prefetch - 1} = in.load({k}, i + {prefetch});")
     for op in ops:
         D = opD[op.dst]
         dn = cname(op.dst)
@@ -512,32 +578,24 @@ def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None
         L.append("    {")
         L.append(f"      uint64_t lin = {dn}_acc;")
         for t in op.terms:
-            lag = lagof(t.var, D, t.s)
-            a, r = t.s // 32, t.s % 32
-            vn = cname(t.var)
             if t.var == "ZERO":
                 continue
+            lag = lagof(t.var, D, t.s)
+            r = t.s % 32
+            vn = cname(t.var)
             if r == 0:
                 src = f"{vn}_h{lag}"
             else:
-                # (x << s)[limb] = (x[limb-a] << r) | (x[limb-a-1] >> (32-r))
                 src = f"tg_shl_limb({vn}_h{lag}, {vn}_h{lag - 1}, {r})"
             m = t.m
-            if m == 1:
-                L.append(f"      lin += (uint64_t){src};")
-            elif m == -1:
-                L.append(f"      lin -= (uint64_t){src};")
-            elif m > 0:
-                L.append(f"      lin += (uint64_t){m}u * (uint64_t){src};")
+            if m > 0:
+                L.append(f"      lin = tg_madw({m}u, {src}, lin);")
             else:
-                L.append(f"      lin -= (uint64_t){-m}u * (uint64_t){src};")
+                L.append(f"      lin = tg_msubw({-m}u, {src}, lin);")
         L.append(f"      uint32_t t = (uint32_t)lin;")
         L.append(f"      {dn}_acc = (uint64_t)((int64_t)lin >> 32);")
         if op.odiv != 1:
-            L.append(f"      const uint32_t x = t - {dn}_bor;")
-            L.append(f"      const uint32_t b1 = (t < {dn}_bor) ? 1u : 0u;")
-            L.append(f"      t = x * 0x{_inv32(op.odiv):08X}u;   // * {op.odiv}^-1 mod 2^32")
-            L.append(f"      {dn}_bor = tg_mulhi(t, {op.odiv}u) + b1;")
+            L.append(f"      t = tg_divexact_step(t, {dn}_bor, 0x{_inv32(op.odiv):08X}u, {op.odiv}u);   // / {op.odiv}")
         r = op.shr % 32
         if r:
             L.append(f"      {dn}_h0 = tg_shr_limb({dn}_qp, t, {r});")
@@ -592,6 +650,39 @@ TG_HD TG_INLINE uint32_t tg_mulhi(uint32_t a, uint32_t b) {
   return (uint32_t)(((uint64_t)a * b) >> 32);
 #endif
 }
+// lin + m*x (64-bit accumulate; one IMAD.WIDE.U32 on the device)
+TG_HD TG_INLINE uint64_t tg_madw(uint32_t m, uint32_t x, uint64_t lin) {
+#ifdef __CUDA_ARCH__
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(m), "r"(x), "l"(lin));
+  return r;
+#else
+  return lin + (uint64_t)m * x;
+#endif
+}
+// lin - m*x (mod 2^64): (2^32 - m)*x + lin - x*2^32
+TG_HD TG_INLINE uint64_t tg_msubw(uint32_t m, uint32_t x, uint64_t lin) {
+#ifdef __CUDA_ARCH__
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(0u - m), "r"(x), "l"(lin));
+  return r - ((uint64_t)x << 32);
+#else
+  return lin - (uint64_t)m * x;
+#endif
+}
+// one limb of the 2-adic exact division by odd o (ref [4]): q = (t - bor) * o^-1,
+// bor' = hi(q*o) + (t < bor)
+TG_HD TG_INLINE uint32_t tg_divexact_step(uint32_t t, uint32_t& bor, uint32_t oinv, uint32_t o) {
+  const uint32_t x = t - bor;
+  const uint32_t b1 = (t < bor) ? 1u : 0u;
+  const uint32_t q = x * oinv;
+#ifdef __CUDA_ARCH__
+  bor = __umulhi(q, o) + b1;
+#else
+  bor = (uint32_t)(((uint64_t)q * o) >> 32) + b1;
+#endif
+  return q;
+}
 // limb of (x >> r) given consecutive limbs lo = x[i], hi = x[i+1], 0 < r < 32
 TG_HD TG_INLINE uint32_t tg_shr_limb(uint32_t lo, uint32_t hi, int r) {
 #ifdef __CUDA_ARCH__
@@ -620,8 +711,8 @@ def generate_all():
     meta = {}
     for ps in sets:
         selfcheck(ps, trials=8)
-        ev = build_eval(ps)
-        it = build_interp(ps)
+        ev = fuse_single_use(build_eval(ps))
+        it = fuse_single_use(build_interp(ps))
         parts.append(f"// ===== point set {ps.name}: B={ps.B}, points {ps.points}")
         parts.append(f"constexpr int {ps.name}_B = {ps.B};")
         parts.append(f"constexpr int {ps.name}_npoints = {ps.npoints};")
