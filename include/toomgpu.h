@@ -128,6 +128,12 @@ size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t *plan, char 
  * (and the elapsed ms in *ms), or a negative value on error. */
 double toom_probe_limb_products(double *ms, void *stream);
 
+/* Enable (default) or disable the fused bottom-level kernel (evaluation,
+ * base-case products, interpolation and recomposition of the last Toom level
+ * in one kernel, in shared memory).  Disabled, that level runs as separate
+ * staged launches through HBM; results are identical (tests compare both). */
+void toom_set_fused(int on);
+
 /* ---- stage exports (tests, bench) ------------------------------------- */
 
 /* Base case alone (step a3): batched schoolbook of signed two's-complement

@@ -58,6 +58,7 @@ SIGNATURES = {
     "toom_eval_width": (_SZ, [_SZ, _I]),
     "toom_npoints": (_I, [_I]),
     "toom_profile_enable": (None, [_I]),
+    "toom_set_fused": (None, [_I]),
     "toom_profile_collect": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_size_t), _I]),
     "toom_plan_describe": (_SZ, [_SZ, _SZ, ctypes.POINTER(ToomPlan), ctypes.c_char_p, _SZ]),
     "toom_probe_limb_products": (ctypes.c_double, [ctypes.POINTER(ctypes.c_double), _P]),
@@ -185,6 +186,11 @@ def plan_describe(n: int, batch: int, B: int = 4, t4: int = 256, t3: int = 64, c
 
 
 CATEGORIES = ("eval", "base", "interp", "other")
+
+
+def set_fused(on: bool = True):
+    """Use (default) or bypass the fused bottom-level kernel."""
+    lib().toom_set_fused(1 if on else 0)
 
 
 def profile_enable(on: bool = True):

@@ -1,0 +1,278 @@
+// Fused bottom Toom level (steps a2 + a3 + a4 + a5 of one
+// recursion level whose children are base-case products), all in shared
+// memory: no child operand, child product or coefficient ever touches HBM.
+//
+// CTA = G = 32 instances (one per lane) x NP = 2B-1 warps.
+//   phase A  warp k  : evaluate U(x_k), V(x_k) for the 32 instances straight
+//                      from the parent limbs (registers, E limbs each), multiply
+//                      (register Comba, IMAD.WIDE.U32 carry chains), store the
+//                      signed 2E-limb product y_k in smem Y[k][t][lane]
+//   phase B  warp j  : stream the coefficient w_j = (sum_k A_jk y_k) / D_j
+//                      (the even-odd + Newton listing program composed into one
+//                      row per coefficient; exact 2-adic division
+//                      by the odd part of D_j, then the exact shift) into smem
+//                      W[j][t][lane]
+//   phase C  warp w  : recompose w = sum_j w_j 2^(32 b j) (Eq. 1.3) segment by
+//                      segment (segment s = limbs [s b, s b + b)), each with a
+//                      local carry chain; one lane per instance resolves the
+//                      carries between segments; the segments then add their
+//                      carry-in and write out (interleaved, or row-major at the
+//                      top level through a coalesced smem copy)
+#pragma once
+
+namespace tg {
+
+template <int E>
+struct RegOut {
+    uint32_t (&r)[E];
+    __device__ __forceinline__ void store(int, int t, uint32_t x) const { r[t] = x; }
+};
+
+// parent operand accessors: block k limb t
+struct FInTop {          // row-major unsigned parent (user input)
+    const uint32_t* row;
+    int b, lentop, B;
+    __device__ __forceinline__ uint32_t load(int k, int t) const {
+        const int len = (k == B - 1) ? lentop : b;
+        return (t < len) ? __ldg(row + k * b + t) : 0u;
+    }
+};
+
+template <int B, int E, class In>
+__device__ __forceinline__ void eval_point(int k, const In& in, uint32_t (&r)[E]) {
+    RegOut<E> o{r};
+    if constexpr (B == 3) {
+        switch (k) {
+            case 0: tg_evalpt_T3_0<E>(in, o); break;
+            case 1: tg_evalpt_T3_1<E>(in, o); break;
+            case 2: tg_evalpt_T3_2<E>(in, o); break;
+            case 3: tg_evalpt_T3_3<E>(in, o); break;
+            default: tg_evalpt_T3_4<E>(in, o); break;
+        }
+    } else {
+        switch (k) {
+            case 0: tg_evalpt_T4_0<E>(in, o); break;
+            case 1: tg_evalpt_T4_1<E>(in, o); break;
+            case 2: tg_evalpt_T4_2<E>(in, o); break;
+            case 3: tg_evalpt_T4_3<E>(in, o); break;
+            case 4: tg_evalpt_T4_4<E>(in, o); break;
+            case 5: tg_evalpt_T4_5<E>(in, o); break;
+            default: tg_evalpt_T4_6<E>(in, o); break;
+        }
+    }
+}
+
+// products y_k in smem: limb t of y_k at Y[(k*W2 + t)*G]
+template <int NP>
+struct SmemProducts {
+    const uint32_t* Y;
+    int w2;
+    uint32_t fill[NP];
+    __device__ __forceinline__ uint32_t load(int k, int t) const {
+        return (t < w2) ? Y[(k * w2 + t) * 32] : fill[k];
+    }
+};
+
+struct SmemOut {
+    uint32_t* p;
+    __device__ __forceinline__ void store(int, int t, uint32_t x) const { p[t * 32] = x; }
+};
+
+template <int B, class In>
+__device__ __forceinline__ void interp_output(int j, const In& in, SmemOut& o, int Lw) {
+    if constexpr (B == 3) {
+        switch (j) {
+            case 0: tg_interpw_T3_0(in, o, Lw); break;
+            case 1: tg_interpw_T3_1(in, o, Lw); break;
+            case 2: tg_interpw_T3_2(in, o, Lw); break;
+            case 3: tg_interpw_T3_3(in, o, Lw); break;
+            default: tg_interpw_T3_4(in, o, Lw); break;
+        }
+    } else {
+        switch (j) {
+            case 0: tg_interpw_T4_0(in, o, Lw); break;
+            case 1: tg_interpw_T4_1(in, o, Lw); break;
+            case 2: tg_interpw_T4_2(in, o, Lw); break;
+            case 3: tg_interpw_T4_3(in, o, Lw); break;
+            case 4: tg_interpw_T4_4(in, o, Lw); break;
+            case 5: tg_interpw_T4_5(in, o, Lw); break;
+            default: tg_interpw_T4_6(in, o, Lw); break;
+        }
+    }
+}
+
+// |a| * |b| with the product sign applied, 2E limbs streamed to dst[t*32]
+template <int E>
+__device__ __forceinline__ void mul_signed_to_smem(uint32_t (&a)[E], uint32_t (&b)[E], uint32_t* dst) {
+    uint32_t sa = a[E - 1] >> 31, sb = b[E - 1] >> 31;
+    {
+        const uint32_t m = 0u - sa;
+        uint32_t cy = sa;
+#pragma unroll
+        for (int i = 0; i < E; ++i) { const uint32_t x = (a[i] ^ m) + cy; cy = (x < cy) ? 1u : 0u; a[i] = x; }
+    }
+    {
+        const uint32_t m = 0u - sb;
+        uint32_t cy = sb;
+#pragma unroll
+        for (int i = 0; i < E; ++i) { const uint32_t x = (b[i] ^ m) + cy; cy = (x < cy) ? 1u : 0u; b[i] = x; }
+    }
+    const uint32_t neg = sa ^ sb, mask = 0u - neg;
+    uint32_t ncarry = neg, c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * E - 1; ++k) {
+#pragma unroll
+        for (int i = (k < E ? 0 : k - E + 1); i <= (k < E ? k : E - 1); ++i) TG_MADD(c0, c1, c2, a[i], b[k - i]);
+        const uint32_t x = (c0 ^ mask) + ncarry;
+        ncarry = (x < ncarry) ? 1u : 0u;
+        dst[k * 32] = x;
+        c0 = c1; c1 = c2; c2 = 0;
+    }
+    dst[(2 * E - 1) * 32] = (c0 ^ mask) + ncarry;
+}
+
+template <int B, int E>
+struct FusedCfg {
+    static constexpr int NP = 2 * B - 1;
+    static constexpr int G = 32;
+    static constexpr int THREADS = 32 * NP;
+};
+
+// shared memory bytes for a launch (Y | W | per-segment carries)
+__host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nseg) {
+    const int NP = 2 * B - 1;
+    return (size_t)4 * 32 * ((size_t)NP * 2 * E + (size_t)NP * Lw + 4 * (size_t)nseg);
+}
+
+template <int B, int E, bool TOP>
+__global__ void __launch_bounds__(32 * (2 * B - 1)) k_fused_bottom(
+    const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV, uint32_t* __restrict__ out,
+    size_t count, int n, int b, int Lw, int wout, int nseg) {
+    constexpr int NP = 2 * B - 1;
+    constexpr int G = 32;
+    extern __shared__ uint32_t sm[];
+    uint32_t* Y = sm;                          // [NP][2E][G], later OUT [wout][G]
+    uint32_t* Wb = Y + NP * 2 * E * G;         // [NP][Lw][G]
+    uint32_t* CO = Wb + NP * Lw * G;           // [nseg][G] segment carry-out
+    uint32_t* L0 = CO + nseg * G;              // [nseg][G] limb 0 of the segment
+    uint32_t* ON = L0 + nseg * G;              // [nseg][G] limbs 1.. all ones
+    uint32_t* CI = ON + nseg * G;              // [nseg][G] resolved carry-in
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const size_t c = (size_t)blockIdx.x * G + lane;
+    const bool valid = c < count;
+    const int lentop = n - (B - 1) * b;
+
+    // ---- phase A: evaluate point `warp` of both operands, multiply
+    if (valid) {
+        uint32_t a[E], bb[E];
+        if (TOP) {
+            eval_point<B, E>(warp, FInTop{srcU + c * (size_t)n, b, lentop, B}, a);
+            eval_point<B, E>(warp, FInTop{srcV + c * (size_t)n, b, lentop, B}, bb);
+        } else {
+            const uint32_t tu = __ldg(srcU + (size_t)(n - 1) * count + c);
+            const uint32_t tv = __ldg(srcV + (size_t)(n - 1) * count + c);
+            eval_point<B, E>(warp, InLevel{srcU + c, count, b, lentop, B, (tu >> 31) ? 0xFFFFFFFFu : 0u}, a);
+            eval_point<B, E>(warp, InLevel{srcV + c, count, b, lentop, B, (tv >> 31) ? 0xFFFFFFFFu : 0u}, bb);
+        }
+        mul_signed_to_smem<E>(a, bb, Y + (warp * 2 * E) * G + lane);
+    }
+    __syncthreads();
+
+    // ---- phase B: coefficient w_warp
+    if (valid) {
+        SmemProducts<NP> in;
+        in.Y = Y + lane;
+        in.w2 = 2 * E;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) in.fill[k] = (Y[(k * 2 * E + 2 * E - 1) * G + lane] >> 31) ? 0xFFFFFFFFu : 0u;
+        SmemOut o{Wb + (warp * Lw) * G + lane};
+        interp_output<B>(warp, in, o, Lw);
+    }
+    __syncthreads();
+
+    // ---- phase C1: segment sums with local carries (OUT aliases Y)
+    uint32_t* OUT = Y;
+    if (valid) {
+        uint32_t negfill[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) negfill[j] = Wb[(j * Lw + Lw - 1) * G + lane] >> 31;
+        for (int s = warp; s < nseg; s += NP) {
+            uint32_t lowfills = 0;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) if (j <= s - 3) lowfills += negfill[j];
+            uint32_t fillC = 0;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) if (j == s - 2) fillC = negfill[j];
+            const bool hasA = s < NP, hasB = s >= 1 && s - 1 < NP, hasC = s >= 2 && s - 2 < NP;
+            const uint32_t* pA = Wb + ((hasA ? s : 0) * Lw) * G + lane;
+            const uint32_t* pB = Wb + ((hasB ? s - 1 : 0) * Lw + b) * G + lane;
+            const int P0 = s * b;
+            const int len = min(b, wout - P0);
+            uint64_t acc = (uint64_t)lowfills * 0xFFFFFFFFull;
+            if (hasA) acc += pA[0];
+            if (hasB) acc += pB[0];
+            if (hasC) acc += Wb[((s - 2) * Lw + 2 * b) * G + lane];
+            uint32_t limb0 = (uint32_t)acc;
+            OUT[P0 * G + lane] = limb0;
+            uint64_t carry = acc >> 32;
+            const uint64_t cc = (uint64_t)(lowfills + fillC) * 0xFFFFFFFFull;
+            uint32_t ones = 0xFFFFFFFFu;
+            for (int r = 1; r < len; ++r) {
+                uint64_t x = carry + cc;
+                if (hasA) x += pA[r * G];
+                if (hasB) x += pB[r * G];
+                const uint32_t lo = (uint32_t)x;
+                OUT[(P0 + r) * G + lane] = lo;
+                ones &= lo;
+                carry = x >> 32;
+            }
+            CO[s * G + lane] = (uint32_t)carry;
+            L0[s * G + lane] = limb0;
+            ON[s * G + lane] = (ones == 0xFFFFFFFFu) ? 1u : 0u;
+        }
+    }
+    __syncthreads();
+    // ---- phase C2: resolve the carries between segments (one lane per instance)
+    if (valid && warp == 0) {
+        uint32_t cin = 0;
+        for (int s = 0; s < nseg; ++s) {
+            CI[s * G + lane] = cin;
+            uint32_t cout = CO[s * G + lane];
+            if (cin) {
+                const uint32_t l0 = L0[s * G + lane];
+                if (l0 + cin < l0 && ON[s * G + lane]) cout += 1;
+            }
+            cin = cout;
+        }
+    }
+    __syncthreads();
+    // ---- phase C3: apply carry-in, write out
+    if (valid) {
+        for (int s = warp; s < nseg; s += NP) {
+            uint32_t cin = CI[s * G + lane];
+            const int P0 = s * b;
+            const int len = min(b, wout - P0);
+            for (int r = 0; r < len && cin; ++r) {
+                const uint32_t x = OUT[(P0 + r) * G + lane];
+                const uint32_t y = x + cin;
+                cin = (y < x) ? 1u : 0u;
+                OUT[(P0 + r) * G + lane] = y;
+            }
+            if (!TOP)
+                for (int r = 0; r < len; ++r) out[(size_t)(P0 + r) * count + c] = OUT[(P0 + r) * G + lane];
+        }
+    }
+    if (TOP) {
+        __syncthreads();
+        // coalesced row-major copy: w[c0 + i][P]
+        const size_t c0 = (size_t)blockIdx.x * G;
+        const int rows = (int)min((size_t)G, count - c0);
+        for (int idx = threadIdx.x; idx < rows * wout; idx += blockDim.x) {
+            const int i = idx / wout, P = idx - i * wout;
+            out[(c0 + i) * (size_t)wout + P] = OUT[P * G + i];
+        }
+    }
+}
+
+}  // namespace tg

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(128) k_base_generic(const uint32_t* __restrict
                                                       uint32_t* __restrict__ P, size_t count, int E) {
     const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= count) return;
-    uint32_t a[64], b[64];
+    uint32_t a[72], b[72];
     uint32_t sgn[2];
     for (int w = 0; w < 2; ++w) {
         const uint32_t* src = (w ? V : U) + c;
@@ -362,6 +362,10 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
     }
 }
 
+}  // namespace tg
+#include "fused_bottom.cuh"
+namespace tg {
+
 // ------------------------------------------------------------------------
 // planner (step a6): the recursion shape and the workspace layout
 // ------------------------------------------------------------------------
@@ -379,7 +383,14 @@ struct Level {
 struct Plan {
     std::vector<Level> lv;   // lv[0..L-1] Toom levels, lv[L] = base level
     size_t bytes = 0;
+    bool fused = false;      // bottom Toom level runs as k_fused_bottom
 };
+
+// base widths with a fused bottom-level instantiation (C1 33, C2 18, C3/C4/C5 23, ...)
+static bool fused_E_supported(int E) {
+    return E == 6 || E == 9 || E == 18 || E == 23 || E == 27 || E == 33;
+}
+static bool g_disable_fused = false;
 
 static bool split_ok(int n, int B) {
     const int b = (n + B - 1) / B;
@@ -425,10 +436,19 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         width = L.e;
         if (depth > 40) return TOOM_EUNSUPPORTED;
     }
+    // fused bottom level?
+    plan.fused = false;
+    if (plan.lv.size() >= 2 && !g_disable_fused) {
+        const Level& Bt = plan.lv[plan.lv.size() - 2];
+        if ((Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.Lw == 2 * Bt.b + 1 &&
+            2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e)
+            plan.fused = true;
+    }
     // workspace layout
     size_t off = 0;
     auto take = [&](size_t limbs) { size_t o = off; off += ((limbs * 4 + 255) / 256) * 256; return o; };
-    for (size_t l = 0; l + 1 < plan.lv.size(); ++l) {
+    const size_t nstaged = plan.lv.size() - 1 - (plan.fused ? 1 : 0);
+    for (size_t l = 0; l < nstaged; ++l) {
         Level& L = plan.lv[l];
         const size_t cc = L.count * (size_t)L.npts;
         L.offU = take((size_t)L.e * cc);
@@ -550,7 +570,7 @@ static toom_status launch_base(int E, const uint32_t* U, const uint32_t* V, uint
         TG_BC(33) TG_BC(34) TG_BC(35) TG_BC(36) TG_BC(37) TG_BC(38) TG_BC(39) TG_BC(40)
 #undef TG_BC
         default:
-            if (E < 1 || E > 64) return TOOM_EINVAL;
+            if (E < 1 || E > 72) return TOOM_EINVAL;
             k_base_generic<<<nblk(count), 128, 0, st>>>(U, V, P, count, E);
     }
     ps.done(st);
@@ -558,14 +578,47 @@ static toom_status launch_base(int E, const uint32_t* U, const uint32_t* V, uint
     return TOOM_OK;
 }
 
+template <int B, int E, bool TOP>
+static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out, cudaStream_t st) {
+    const int nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
+    const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg);
+    static bool attr_set = false;   // per instantiation
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_fused_bottom<B, E, TOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    const unsigned grid = (unsigned)((Lv.count + 31) / 32);
+    k_fused_bottom<B, E, TOP><<<grid, 32 * (2 * B - 1), smem, st>>>(su, sv, out, Lv.count, Lv.n, Lv.b, Lv.Lw,
+                                                                    2 * Lv.n, nseg);
+}
+
+static toom_status launch_fused(const Level& Lv, bool top, const uint32_t* su, const uint32_t* sv, uint32_t* out,
+                                cudaStream_t st) {
+    if (Lv.count == 0) return TOOM_OK;
+    ProfScope ps(CAT_BASE, st);
+#define TG_F(BB, EE)                                                      \
+    if (Lv.B == BB && Lv.e == EE) {                                       \
+        if (top) launch_fused_t<BB, EE, true>(Lv, su, sv, out, st);       \
+        else launch_fused_t<BB, EE, false>(Lv, su, sv, out, st);          \
+        ps.done(st);                                                      \
+        ++t_launches;                                                     \
+        return TOOM_OK;                                                   \
+    }
+    TG_F(3, 6) TG_F(3, 9) TG_F(3, 18) TG_F(3, 23) TG_F(3, 27) TG_F(3, 33)
+    TG_F(4, 6) TG_F(4, 9) TG_F(4, 18) TG_F(4, 23) TG_F(4, 27) TG_F(4, 33)
+#undef TG_F
+    return TOOM_EUNSUPPORTED;
+}
+
 // base level reached directly (no Toom level): schoolbook on row-major
 // operands via a transposing copy
-__global__ void k_transpose_in(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t count, int n) {
+// row-major [count][n] -> interleaved [E][count], zero rows for n <= i < E
+__global__ void k_transpose_in(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t count, int n, int E) {
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= count * (size_t)n) return;
-    const size_t c = gid / n;
-    const int i = (int)(gid % n);
-    dst[(size_t)i * count + c] = src[gid];
+    if (gid >= count * (size_t)E) return;
+    const size_t c = gid / E;
+    const int i = (int)(gid % E);
+    dst[(size_t)i * count + c] = i < n ? src[c * (size_t)n + i] : 0u;
 }
 __global__ void k_transpose_out(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t count, int n2) {
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -580,19 +633,22 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
     const size_t L = plan.lv.size() - 1;   // number of Toom levels
     toom_status s;
     if (L == 0) {
-        // schoolbook only (n <= 64 after planning)
+        // schoolbook only (n <= 64): the base kernel multiplies signed
+        // operands, so the unsigned inputs get one zero limb on top
+        const int E = n + 1;
         uint32_t* tu = (uint32_t*)ws;
-        uint32_t* tv = tu + ((batch * n + 63) & ~(size_t)63);
-        uint32_t* tp = tv + ((batch * n + 63) & ~(size_t)63);
-        k_transpose_in<<<nblk(batch * n, 256), 256, 0, st>>>(u, tu, batch, n);
-        k_transpose_in<<<nblk(batch * n, 256), 256, 0, st>>>(v, tv, batch, n);
-        if ((s = launch_base(n, tu, tv, tp, batch, st))) return s;
+        uint32_t* tv = tu + ((batch * E + 63) & ~(size_t)63);
+        uint32_t* tp = tv + ((batch * E + 63) & ~(size_t)63);
+        k_transpose_in<<<nblk(batch * E, 256), 256, 0, st>>>(u, tu, batch, n, E);
+        k_transpose_in<<<nblk(batch * E, 256), 256, 0, st>>>(v, tv, batch, n, E);
+        if ((s = launch_base(E, tu, tv, tp, batch, st))) return s;
         k_transpose_out<<<nblk(batch * 2 * n, 256), 256, 0, st>>>(tp, w, batch, 2 * n);
         t_launches += 3;
         return TOOM_OK;
     }
+    const size_t Lt = plan.fused ? L - 1 : L;   // levels run as staged eval/interp launches
     // down: evaluation
-    for (size_t l = 0; l < L; ++l) {
+    for (size_t l = 0; l < Lt; ++l) {
         const Level& Lv = plan.lv[l];
         const uint32_t* su = l == 0 ? u : (const uint32_t*)(ws + plan.lv[l - 1].offU);
         const uint32_t* sv = l == 0 ? v : (const uint32_t*)(ws + plan.lv[l - 1].offV);
@@ -600,15 +656,22 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
                              Lv.b, Lv.e, st)))
             return s;
     }
-    // bottom: base case on level L-1's children
-    {
+    // bottom
+    if (plan.fused) {
+        const Level& Lv = plan.lv[L - 1];
+        const bool top = (L - 1 == 0);
+        const uint32_t* su = top ? u : (const uint32_t*)(ws + plan.lv[L - 2].offU);
+        const uint32_t* sv = top ? v : (const uint32_t*)(ws + plan.lv[L - 2].offV);
+        uint32_t* out = top ? w : (uint32_t*)(ws + plan.lv[L - 2].offP);
+        if ((s = launch_fused(Lv, top, su, sv, out, st))) return s;
+    } else {
         const Level& Lv = plan.lv[L - 1];
         if ((s = launch_base(Lv.e, (const uint32_t*)(ws + Lv.offU), (const uint32_t*)(ws + Lv.offV),
                              (uint32_t*)(ws + Lv.offP), Lv.count * Lv.npts, st)))
             return s;
     }
     // up: interpolation + recomposition
-    for (size_t l = L; l-- > 0;) {
+    for (size_t l = Lt; l-- > 0;) {
         const Level& Lv = plan.lv[l];
         uint32_t* out = l == 0 ? w : (uint32_t*)(ws + plan.lv[l - 1].offP);
         if ((s = launch_interp(Lv.B, l == 0, (const uint32_t*)(ws + Lv.offP), (uint32_t*)(ws + Lv.offW), out, Lv.count,
@@ -644,7 +707,7 @@ static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, si
     Plan plan;
     if ((s = make_plan((int)n, chunk, p, plan))) return s;
     size_t need = plan.bytes;
-    if (plan.lv.size() == 1) need = (2 * ((chunk * n + 63) & ~(size_t)63) + 2 * chunk * n) * 4;
+    if (plan.lv.size() == 1) need = (2 * ((chunk * (n + 1) + 63) & ~(size_t)63) + 2 * chunk * (n + 1)) * 4;
     void* ws = nullptr;
     if ((s = get_ws(need, &ws))) return s;
     for (size_t c0 = 0; c0 < batch; c0 += chunk) {
@@ -810,6 +873,8 @@ toom_status toom_base_interleaved(uint32_t* w, const uint32_t* u, const uint32_t
 
 int toom_npoints(int B) { return ps_desc(B).npts; }
 
+void toom_set_fused(int on) { g_disable_fused = (on == 0); }
+
 void toom_profile_enable(int on) {
     t_prof = on != 0;
 }
@@ -843,7 +908,8 @@ size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t* plan, char*
         js += tmp;
     }
     char tail[128];
-    snprintf(tail, sizeof tail, "], \"workspace_bytes\": %zu}", pl.bytes);
+    snprintf(tail, sizeof tail, "], \"workspace_bytes\": %zu, \"fused_bottom\": %s}", pl.bytes,
+             pl.fused ? "true" : "false");
     js += tail;
     if (buf && len) {
         size_t k = js.size() < len - 1 ? js.size() : len - 1;

@@ -494,7 +494,68 @@ def fuse_single_use(prog: Program, max_mult=1 << 24) -> Program:
     return out
 
 
-def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None, prefetch=2) -> str:
+def input_forms(prog: Program) -> dict:
+    """Symbolic execution over the INPUT streams: var -> {input: Fraction}."""
+    env = {v: {v: Fraction(1)} for v in prog.inputs}
+    env["ZERO"] = {}
+    for op in prog.ops:
+        acc = {}
+        for t in op.terms:
+            for k, c in env[t.var].items():
+                acc[k] = acc.get(k, 0) + c * t.m * (1 << t.s)
+        d = op.odiv << op.shr
+        env[op.dst] = {k: Fraction(c) / d for k, c in acc.items() if c != 0}
+    return env
+
+
+def per_output_programs(prog: Program, name: str) -> list:
+    """PAPER.md:162 ("for specific n the computation of the c_l can be
+    optimized from the entries of this inverse matrix"): compose the whole
+    listing program into ONE op per output, w_j = (sum_k A_jk y_k) / D_j,
+    with the composition done symbolically from the even-odd + Newton
+    program (so A/D are exactly the paper-method's inverse rows).  Each output
+    can then be streamed independently (one thread per coefficient)."""
+    env = input_forms(prog)
+    progs = []
+    for j, v in enumerate(prog.outputs):
+        form = env[v]
+        D = 1
+        for c in form.values():
+            D = _lcm(D, c.denominator)
+        p = Program(f"{name}_w{j}", prog.inputs, nunk=prog.nunk)
+        p.forms = dict(prog.forms)
+        terms = [Term(k, int(c * D)) for k, c in sorted(form.items(), key=lambda kc: prog.inputs.index(kc[0]))]
+        if D == 1 and len(terms) == 1 and terms[0].m == 1:
+            p.outputs = [terms[0].var]
+        else:
+            s = (D & -D).bit_length() - 1
+            assert (D >> s) < (1 << 32) and sum(abs(t.m) for t in terms) < (1 << 30), (name, j)
+            p.add(f"w{j}", terms, D, note=f"w_{j} = (sum A_jk y_k)/{D}")
+            p.outputs = [f"w{j}"]
+        assert p.forms[p.outputs[0]] == prog.forms[v]
+        progs.append(p)
+    return progs
+
+
+def build_eval_direct(ps: PointSet) -> list:
+    """One single-op program per point: U(p:q) = sum_k p^k q^(n-k) u_k."""
+    n = ps.n
+    progs = []
+    for idx, (p, q) in enumerate(ps.points):
+        prog = Program(f"eval_{ps.name}_p{idx}", [f"u{k}" for k in range(ps.B)], nunk=ps.B)
+        for k in range(ps.B):
+            prog.forms[f"u{k}"] = [1 if j == k else 0 for j in range(ps.B)]
+        terms = _norm_terms([Term(f"u{k}", p**k * q ** (n - k)) for k in range(ps.B)])
+        if len(terms) == 1 and terms[0].m == 1 and terms[0].s == 0:
+            prog.outputs = [terms[0].var]
+        else:
+            prog.add(f"U{idx}", terms, 1, note=f"U({p}:{q})")
+            prog.outputs = [f"U{idx}"]
+        progs.append(prog)
+    return progs
+
+
+def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None, prefetch=2, unrolled=False) -> str:
     """Emit a __host__ __device__ template that streams the program LSB-first.
 
     template <class In, class Out>
@@ -544,8 +605,15 @@ def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None
     L = []
     L.append(f"// generated by toomgen.py from {prog.name}; {len(ops)} ops, max delay {maxdelay}")
     L.append(f"constexpr int {fname}_maxdelay = {maxdelay};")
-    L.append("template <class In, class Out>")
-    L.append(f"TG_HD TG_INLINE void {fname}(const In& in, Out& out, int nsteps) {{")
+    if unrolled:
+        # compile-time step count, fully unrolled: outputs may land in registers
+        prefetch = 0
+        L.append("template <int NSTEPS, class In, class Out>")
+        L.append(f"TG_HD TG_INLINE void {fname}(const In& in, Out& out) {{")
+        L.append("  constexpr int nsteps = NSTEPS;")
+    else:
+        L.append("template <class In, class Out>")
+        L.append(f"TG_HD TG_INLINE void {fname}(const In& in, Out& out, int nsteps) {{")
     vars_all = used_inputs + [op.dst for op in ops]
     for v in vars_all:
         for h in range(1, hist[v] + 1):
@@ -561,11 +629,18 @@ def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None
         k = prog.inputs.index(v)
         for p in range(prefetch):
             L.append(f"  uint32_t {cname(v)}_pf{p} = in.load({k}, {p});")
-    L.append(f"  const int total = nsteps + {maxdelay};")
-    L.append("  #pragma unroll 1")
+    if unrolled:
+        L.append(f"  constexpr int total = nsteps + {maxdelay};")
+        L.append("  #pragma unroll")
+    else:
+        L.append(f"  const int total = nsteps + {maxdelay};")
+        L.append("  #pragma unroll 1")
     L.append("  for (int i = 0; i < total; ++i) {")
     for v in used_inputs:
         k = prog.inputs.index(v)
+        if prefetch == 0:
+            L.append(f"    const uint32_t {cname(v)}_h0 = in.load({k}, i);")
+            continue
         L.append(f"    const uint32_t {cname(v)}_h0 = {cname(v)}_pf0;")
         for p in range(prefetch - 1):
             L.append(f"    {cname(v)}_pf{p} = {cname(v)}_pf{p + 1};")
@@ -724,6 +799,12 @@ def generate_all():
         od_idx = [j for j in range(d + 1) if j % 2 == 1]
         parts.append(emit_stream_function(it, f"tg_interp_{ps.name}_even", [it.outputs[j] for j in ev_idx], ev_idx))
         parts.append(emit_stream_function(it, f"tg_interp_{ps.name}_odd", [it.outputs[j] for j in od_idx], od_idx))
+        if ps.B <= 4:
+            # fused bottom-level kernel pieces: one point / one coefficient per thread
+            for k, pe in enumerate(build_eval_direct(ps)):
+                parts.append(emit_stream_function(pe, f"tg_evalpt_{ps.name}_{k}", unrolled=True))
+            for j, pj in enumerate(per_output_programs(build_interp(ps), f"interp_{ps.name}")):
+                parts.append(emit_stream_function(pj, f"tg_interpw_{ps.name}_{j}", prefetch=0))
         meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
     return "\n\n".join(parts) + "\n", meta
 

@@ -230,3 +230,41 @@ def test_c4_single_large_product():
     w = host(tg.toom_mul(dev(u), dev(v), B=4))
     check_residues(u, v, w)
     assert np.array_equal(w, oracle.toom(u, v))
+
+
+# ------------------------------------------------------------ fused bottom level
+
+
+FUSED_SHAPES = [  # (B, n, t4, t3): bottom Toom levels with base widths 6, 9, 18, 23, 27, 33
+    (3, 13, 256, 64), (4, 19, 256, 64), (3, 23, 256, 64), (4, 31, 256, 64), (3, 50, 256, 64),
+    (4, 66, 256, 64), (3, 65, 256, 64), (4, 88, 256, 64), (3, 78, 256, 64), (3, 96, 10**9, 10**9),
+    (4, 256, 32, 32), (4, 1024, 256, 64), (8, 2048, 256, 64), (4, 1040, 256, 64), (3, 500, 256, 20),
+]
+
+
+@pytest.mark.parametrize("B,n,t4,t3", FUSED_SHAPES)
+def test_fused_bottom_equals_staged_and_oracle(B, n, t4, t3):
+    rng = np.random.default_rng(n * 7 + B)
+    batch = 70
+    u = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    v = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    u[0] = 0xFFFFFFFF
+    v[0] = 0xFFFFFFFF
+    u[1] = 0
+    u[2, ::2] = 0
+    v[2] = u[2]
+    info = tg.plan_describe(n, batch, B=B, t4=t4, t3=t3)
+    try:
+        tg.set_fused(False)
+        staged = run_batched(u, v, B, t4=t4, t3=t3)
+    finally:
+        tg.set_fused(True)
+    fused = run_batched(u, v, B, t4=t4, t3=t3)
+    want = oracle.schoolbook_batched(u, v)
+    assert np.array_equal(staged, want), ("staged", info)
+    assert np.array_equal(fused, want), ("fused", info)
+
+
+def test_c2_plan_uses_fused_bottom():
+    info = tg.plan_describe(256, 65536, B=4, t4=32, t3=32)
+    assert info["fused_bottom"] and info["levels"][-1]["n"] == 18
