@@ -4,9 +4,10 @@
 //
 // CTA = G = 32 instances (one per lane) x NP = 2B-1 warps.
 //   phase A  warp k  : evaluate U(x_k), V(x_k) for the 32 instances straight
-//                      from the parent limbs (registers, E limbs each), multiply
-//                      (register Comba, IMAD.WIDE.U32 carry chains), store the
-//                      signed 2E-limb product y_k in smem Y[k][t][lane]
+//                      from the parent limbs (registers, E limbs each; table of
+//                      homogeneous coefficients p^j q^(n-j)), multiply (register
+//                      Comba, IMAD.WIDE.U32 carry chains), store the signed
+//                      2E-limb product y_k in smem Y[k][t][lane]
 //   phase B  warp j  : stream the coefficient w_j = (sum_k A_jk y_k) / D_j
 //                      (the even-odd + Newton listing program composed into one
 //                      row per coefficient; exact 2-adic division
@@ -18,18 +19,14 @@
 //                      carries between segments; the segments then add their
 //                      carry-in and write out (interleaved, or row-major at the
 //                      top level through a coalesced smem copy)
+// Phases A and B are table driven (one code path for every point / row) so the
+// kernel stays small enough for the instruction cache.
 #pragma once
 
 namespace tg {
 
-template <int E>
-struct RegOut {
-    uint32_t (&r)[E];
-    __device__ __forceinline__ void store(int, int t, uint32_t x) const { r[t] = x; }
-};
-
-// parent operand accessors: block k limb t
-struct FInTop {          // row-major unsigned parent (user input)
+// parent operand accessor for the top level: row-major unsigned, block k limb t
+struct FInTop {
     const uint32_t* row;
     int b, lentop, B;
     __device__ __forceinline__ uint32_t load(int k, int t) const {
@@ -38,66 +35,68 @@ struct FInTop {          // row-major unsigned parent (user input)
     }
 };
 
+template <int B>
+__device__ __forceinline__ long long evalc(int k, int j) {
+    if constexpr (B == 3) return tg_evalc_T3[k][j];
+    else return tg_evalc_T4[k][j];
+}
+template <int B>
+__device__ __forceinline__ long long rowA(int j, int k) {
+    if constexpr (B == 3) return tg_rowA_T3[j][k];
+    else return tg_rowA_T4[j][k];
+}
+template <int B> __device__ __forceinline__ uint32_t rowO(int j) { if constexpr (B == 3) return tg_rowO_T3[j]; else return tg_rowO_T4[j]; }
+template <int B> __device__ __forceinline__ uint32_t rowInv(int j) { if constexpr (B == 3) return tg_rowInv_T3[j]; else return tg_rowInv_T4[j]; }
+template <int B> __device__ __forceinline__ int rowS(int j) { if constexpr (B == 3) return tg_rowS_T3[j]; else return tg_rowS_T4[j]; }
+
+// evaluation of point k: r = sum_j c[k][j] * block_j, E limbs, LSB first with a
+// signed 64-bit carry (two's-complement result)
 template <int B, int E, class In>
 __device__ __forceinline__ void eval_point(int k, const In& in, uint32_t (&r)[E]) {
-    RegOut<E> o{r};
-    if constexpr (B == 3) {
-        switch (k) {
-            case 0: tg_evalpt_T3_0<E>(in, o); break;
-            case 1: tg_evalpt_T3_1<E>(in, o); break;
-            case 2: tg_evalpt_T3_2<E>(in, o); break;
-            case 3: tg_evalpt_T3_3<E>(in, o); break;
-            default: tg_evalpt_T3_4<E>(in, o); break;
-        }
-    } else {
-        switch (k) {
-            case 0: tg_evalpt_T4_0<E>(in, o); break;
-            case 1: tg_evalpt_T4_1<E>(in, o); break;
-            case 2: tg_evalpt_T4_2<E>(in, o); break;
-            case 3: tg_evalpt_T4_3<E>(in, o); break;
-            case 4: tg_evalpt_T4_4<E>(in, o); break;
-            case 5: tg_evalpt_T4_5<E>(in, o); break;
-            default: tg_evalpt_T4_6<E>(in, o); break;
-        }
+    uint64_t c[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) c[j] = (uint64_t)evalc<B>(k, j);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int t = 0; t < E; ++t) {
+        uint64_t lin = acc;
+#pragma unroll
+        for (int j = 0; j < B; ++j) lin += c[j] * (uint64_t)in.load(j, t);
+        r[t] = (uint32_t)lin;
+        acc = (uint64_t)((int64_t)lin >> 32);
     }
 }
 
-// products y_k in smem: limb t of y_k at Y[(k*W2 + t)*G]
-template <int NP>
-struct SmemProducts {
-    const uint32_t* Y;
-    int w2;
+// interpolation row j: w_j = (sum_k A[j][k] y_k) / (o_j 2^s_j); y_k read from
+// smem Yl[(k*w2 + t)*32] (sign-extended past w2), w_j written to dst[t*32] for
+// t < Lw.  The shift is applied one limb late (s = 0 is a plain delay).
+template <int B>
+__device__ __forceinline__ void interp_row(int j, const uint32_t* __restrict__ Yl, int w2, uint32_t* __restrict__ dst,
+                                           int Lw) {
+    constexpr int NP = 2 * B - 1;
+    uint64_t A[NP];
     uint32_t fill[NP];
-    __device__ __forceinline__ uint32_t load(int k, int t) const {
-        return (t < w2) ? Y[(k * w2 + t) * 32] : fill[k];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        A[k] = (uint64_t)rowA<B>(j, k);
+        fill[k] = (Yl[(k * w2 + w2 - 1) * 32] >> 31) ? 0xFFFFFFFFu : 0u;
     }
-};
-
-struct SmemOut {
-    uint32_t* p;
-    __device__ __forceinline__ void store(int, int t, uint32_t x) const { p[t * 32] = x; }
-};
-
-template <int B, class In>
-__device__ __forceinline__ void interp_output(int j, const In& in, SmemOut& o, int Lw) {
-    if constexpr (B == 3) {
-        switch (j) {
-            case 0: tg_interpw_T3_0(in, o, Lw); break;
-            case 1: tg_interpw_T3_1(in, o, Lw); break;
-            case 2: tg_interpw_T3_2(in, o, Lw); break;
-            case 3: tg_interpw_T3_3(in, o, Lw); break;
-            default: tg_interpw_T3_4(in, o, Lw); break;
+    const uint32_t o = rowO<B>(j), oinv = rowInv<B>(j);
+    const int sh = rowS<B>(j);
+    uint64_t acc = 0;
+    uint32_t bor = 0, qp = 0;
+#pragma unroll 1
+    for (int t = 0; t <= Lw; ++t) {
+        uint64_t lin = acc;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            const uint32_t y = (t < w2) ? Yl[(k * w2 + t) * 32] : fill[k];
+            lin += A[k] * (uint64_t)y;
         }
-    } else {
-        switch (j) {
-            case 0: tg_interpw_T4_0(in, o, Lw); break;
-            case 1: tg_interpw_T4_1(in, o, Lw); break;
-            case 2: tg_interpw_T4_2(in, o, Lw); break;
-            case 3: tg_interpw_T4_3(in, o, Lw); break;
-            case 4: tg_interpw_T4_4(in, o, Lw); break;
-            case 5: tg_interpw_T4_5(in, o, Lw); break;
-            default: tg_interpw_T4_6(in, o, Lw); break;
-        }
+        acc = (uint64_t)((int64_t)lin >> 32);
+        const uint32_t q = tg_divexact_step((uint32_t)lin, bor, oinv, o);
+        if (t > 0) dst[(t - 1) * 32] = __funnelshift_r(qp, q, sh);
+        qp = q;
     }
 }
 
@@ -131,13 +130,6 @@ __device__ __forceinline__ void mul_signed_to_smem(uint32_t (&a)[E], uint32_t (&
     dst[(2 * E - 1) * 32] = (c0 ^ mask) + ncarry;
 }
 
-template <int B, int E>
-struct FusedCfg {
-    static constexpr int NP = 2 * B - 1;
-    static constexpr int G = 32;
-    static constexpr int THREADS = 32 * NP;
-};
-
 // shared memory bytes for a launch (Y | W | per-segment carries)
 __host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nseg) {
     const int NP = 2 * B - 1;
@@ -145,7 +137,7 @@ __host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nse
 }
 
 template <int B, int E, bool TOP>
-__global__ void __launch_bounds__(32 * (2 * B - 1)) k_fused_bottom(
+__global__ void __maxnreg__(E <= 18 ? 96 : 128) k_fused_bottom(
     const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV, uint32_t* __restrict__ out,
     size_t count, int n, int b, int Lw, int wout, int nseg) {
     constexpr int NP = 2 * B - 1;
@@ -180,30 +172,19 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_fused_bottom(
     __syncthreads();
 
     // ---- phase B: coefficient w_warp
-    if (valid) {
-        SmemProducts<NP> in;
-        in.Y = Y + lane;
-        in.w2 = 2 * E;
-#pragma unroll
-        for (int k = 0; k < NP; ++k) in.fill[k] = (Y[(k * 2 * E + 2 * E - 1) * G + lane] >> 31) ? 0xFFFFFFFFu : 0u;
-        SmemOut o{Wb + (warp * Lw) * G + lane};
-        interp_output<B>(warp, in, o, Lw);
-    }
+    if (valid) interp_row<B>(warp, Y + lane, 2 * E, Wb + (warp * Lw) * G + lane, Lw);
     __syncthreads();
 
     // ---- phase C1: segment sums with local carries (OUT aliases Y)
     uint32_t* OUT = Y;
     if (valid) {
-        uint32_t negfill[NP];
-#pragma unroll
-        for (int j = 0; j < NP; ++j) negfill[j] = Wb[(j * Lw + Lw - 1) * G + lane] >> 31;
         for (int s = warp; s < nseg; s += NP) {
-            uint32_t lowfills = 0;
-#pragma unroll
-            for (int j = 0; j < NP; ++j) if (j <= s - 3) lowfills += negfill[j];
-            uint32_t fillC = 0;
-#pragma unroll
-            for (int j = 0; j < NP; ++j) if (j == s - 2) fillC = negfill[j];
+            uint32_t lowfills = 0, fillC = 0;
+            for (int j = 0; j <= s - 2 && j < NP; ++j) {
+                const uint32_t f = Wb[(j * Lw + Lw - 1) * G + lane] >> 31;
+                if (j == s - 2) fillC = f;
+                else lowfills += f;
+            }
             const bool hasA = s < NP, hasB = s >= 1 && s - 1 < NP, hasC = s >= 2 && s - 2 < NP;
             const uint32_t* pA = Wb + ((hasA ? s : 0) * Lw) * G + lane;
             const uint32_t* pB = Wb + ((hasB ? s - 1 : 0) * Lw + b) * G + lane;

@@ -696,8 +696,9 @@ static toom_status check_device() {
 static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
                            const toom_plan_t& p, cudaStream_t st) {
     t_launches = 0;
-    if (!w || !u || !v || n == 0 || n > (1u << 30)) return TOOM_EINVAL;
+    if (n == 0 || n > (1u << 30)) return TOOM_EINVAL;
     if (batch == 0) return TOOM_OK;
+    if (!w || !u || !v) return TOOM_EINVAL;
     const size_t in_bytes = n * batch * 4, out_bytes = 2 * n * batch * 4;
     if (overlaps(w, out_bytes, u, in_bytes) || overlaps(w, out_bytes, v, in_bytes)) return TOOM_EINVAL;
     toom_status s = check_device();

@@ -695,6 +695,46 @@ def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None
     return "\n".join(L)
 
 
+def emit_row_tables(ps: PointSet) -> str:
+    """Constant tables for the fused kernel's table-driven streams:
+    evaluation coefficients c[k][j] = p_k^j q_k^(n-j) (homogeneous points) and
+    the interpolation rows w_j = (sum_k A[j][k] y_k) / (o_j 2^s_j), composed
+    from the even-odd + Newton-listing program (per_output_programs)."""
+    n = ps.n
+    NP = ps.npoints
+    rows = per_output_programs(build_interp(ps), f"interp_{ps.name}")
+    L = [f"// ---- table-driven rows for {ps.name} (fused bottom-level kernel)"]
+    L.append(f"TG_CONST long long tg_evalc_{ps.name}[{NP}][{ps.B}] = {{")
+    for (p, q) in ps.points:
+        L.append("  {" + ", ".join(str(p**j * q ** (n - j)) for j in range(ps.B)) + "},")
+    L.append("};")
+    A, O, INV, S = [], [], [], []
+    for j, pr in enumerate(rows):
+        coef = [0] * NP
+        if pr.ops:
+            op = pr.ops[0]
+            for t in op.terms:
+                assert t.s == 0
+                coef[pr.inputs.index(t.var)] = t.m
+            o, s = op.odiv, op.shr
+        else:
+            coef[pr.inputs.index(pr.outputs[0])] = 1
+            o, s = 1, 0
+        assert s < 32
+        A.append(coef)
+        O.append(o)
+        INV.append(_inv32(o))
+        S.append(s)
+    L.append(f"TG_CONST long long tg_rowA_{ps.name}[{NP}][{NP}] = {{")
+    for r in A:
+        L.append("  {" + ", ".join(str(x) for x in r) + "},")
+    L.append("};")
+    L.append(f"TG_CONST unsigned tg_rowO_{ps.name}[{NP}] = {{" + ", ".join(f"{x}u" for x in O) + "};")
+    L.append(f"TG_CONST unsigned tg_rowInv_{ps.name}[{NP}] = {{" + ", ".join(f"0x{x:08X}u" for x in INV) + "};")
+    L.append(f"TG_CONST int tg_rowS_{ps.name}[{NP}] = {{" + ", ".join(str(x) for x in S) + "};")
+    return "\n".join(L)
+
+
 def stats(prog: Program):
     nterms = sum(len(op.terms) for op in prog.ops)
     ndiv = sum(1 for op in prog.ops if op.odiv != 1)
@@ -714,6 +754,13 @@ HEADER = """// AUTO-GENERATED by paper_1602_02740_b200/gen/toomgen.py -- do not 
 #  else
 #    define TG_HD
 #    define TG_INLINE inline
+#  endif
+#endif
+#ifndef TG_CONST
+#  ifdef __CUDACC__
+#    define TG_CONST __constant__
+#  else
+#    define TG_CONST static const
 #  endif
 #endif
 #ifndef TG_HELPERS_DEFINED
@@ -800,11 +847,8 @@ def generate_all():
         parts.append(emit_stream_function(it, f"tg_interp_{ps.name}_even", [it.outputs[j] for j in ev_idx], ev_idx))
         parts.append(emit_stream_function(it, f"tg_interp_{ps.name}_odd", [it.outputs[j] for j in od_idx], od_idx))
         if ps.B <= 4:
-            # fused bottom-level kernel pieces: one point / one coefficient per thread
-            for k, pe in enumerate(build_eval_direct(ps)):
-                parts.append(emit_stream_function(pe, f"tg_evalpt_{ps.name}_{k}", unrolled=True))
-            for j, pj in enumerate(per_output_programs(build_interp(ps), f"interp_{ps.name}")):
-                parts.append(emit_stream_function(pj, f"tg_interpw_{ps.name}_{j}", prefetch=0))
+            # fused bottom-level kernel tables: one point / one coefficient row per warp
+            parts.append(emit_row_tables(ps))
         meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
     return "\n\n".join(parts) + "\n", meta
 
