@@ -35,6 +35,18 @@ struct FInTop {
     }
 };
 
+// parent operand staged in smem: block k limb t at P[(k*b + t)*33]
+struct SmemParent {
+    const uint32_t* P;
+    int b, lentop, B;
+    uint32_t fill;   // sign fill of the top block (0 at the top level)
+    __device__ __forceinline__ uint32_t load(int k, int t) const {
+        const int len = (k == B - 1) ? lentop : b;
+        if (t < len) return P[(k * b + t) * 33];
+        return (k == B - 1) ? fill : 0u;
+    }
+};
+
 template <int B>
 __device__ __forceinline__ long long evalc(int k, int j) {
     if constexpr (B == 3) return tg_evalc_T3[k][j];
@@ -131,13 +143,15 @@ __device__ __forceinline__ void mul_signed_to_smem(uint32_t (&a)[E], uint32_t (&
 }
 
 // shared memory bytes for a launch (Y | W | per-segment carries)
-__host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nseg) {
+__host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nseg, int n) {
     const int NP = 2 * B - 1;
-    return (size_t)4 * 32 * ((size_t)NP * 2 * E + (size_t)NP * Lw + 4 * (size_t)nseg);
+    size_t wreg = (size_t)NP * Lw * 32;
+    if ((size_t)2 * n * 33 > wreg) wreg = (size_t)2 * n * 33;   // parents staged in the W region
+    return (size_t)4 * ((size_t)NP * 2 * E * 32 + wreg + 4 * 32 * (size_t)nseg);
 }
 
 template <int B, int E, bool TOP>
-__global__ void __maxnreg__(E <= 18 ? 96 : 128) k_fused_bottom(
+__global__ void __maxnreg__(E <= 18 ? 88 : 128) k_fused_bottom(
     const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV, uint32_t* __restrict__ out,
     size_t count, int n, int b, int Lw, int wout, int nseg) {
     constexpr int NP = 2 * B - 1;
@@ -145,7 +159,8 @@ __global__ void __maxnreg__(E <= 18 ? 96 : 128) k_fused_bottom(
     extern __shared__ uint32_t sm[];
     uint32_t* Y = sm;                          // [NP][2E][G], later OUT [wout][G]
     uint32_t* Wb = Y + NP * 2 * E * G;         // [NP][Lw][G]
-    uint32_t* CO = Wb + NP * Lw * G;           // [nseg][G] segment carry-out
+    const int wreg = (NP * Lw * G > 2 * n * 33) ? NP * Lw * G : 2 * n * 33;
+    uint32_t* CO = Wb + wreg;                  // [nseg][G] segment carry-out
     uint32_t* L0 = CO + nseg * G;              // [nseg][G] limb 0 of the segment
     uint32_t* ON = L0 + nseg * G;              // [nseg][G] limbs 1.. all ones
     uint32_t* CI = ON + nseg * G;              // [nseg][G] resolved carry-in
@@ -155,18 +170,41 @@ __global__ void __maxnreg__(E <= 18 ? 96 : 128) k_fused_bottom(
     const bool valid = c < count;
     const int lentop = n - (B - 1) * b;
 
-    // ---- phase A: evaluate point `warp` of both operands, multiply
+    // ---- phase A0: stage the 32 parents' operands in smem (W region, unused
+    // until phase B): Pu/Pv [limb][PP], coalesced global loads by all warps
+    constexpr int PP = 33;                     // padded pitch (conflict-free transpose)
+    uint32_t* Pu = Wb;
+    uint32_t* Pv = Wb + n * PP;
+    {
+        const size_t c0 = (size_t)blockIdx.x * G;
+        const int nin = (int)min((size_t)G, count - c0);
+        if (TOP) {
+            // row-major rows of n limbs: thread idx -> (instance i, limb t)
+            for (int idx = threadIdx.x; idx < nin * n; idx += blockDim.x) {
+                const int i = idx / n, t = idx - i * n;
+                Pu[t * PP + i] = __ldg(srcU + (c0 + i) * (size_t)n + t);
+                Pv[t * PP + i] = __ldg(srcV + (c0 + i) * (size_t)n + t);
+            }
+        } else {
+            // interleaved [n][count]: rows of 32 consecutive instances
+            for (int t = warp; t < n; t += NP) {
+                if (lane < nin) {
+                    Pu[t * PP + lane] = __ldg(srcU + (size_t)t * count + c0 + lane);
+                    Pv[t * PP + lane] = __ldg(srcV + (size_t)t * count + c0 + lane);
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- phase A: evaluate point `warp` of both operands (from smem), multiply
     if (valid) {
         uint32_t a[E], bb[E];
-        if (TOP) {
-            eval_point<B, E>(warp, FInTop{srcU + c * (size_t)n, b, lentop, B}, a);
-            eval_point<B, E>(warp, FInTop{srcV + c * (size_t)n, b, lentop, B}, bb);
-        } else {
-            const uint32_t tu = __ldg(srcU + (size_t)(n - 1) * count + c);
-            const uint32_t tv = __ldg(srcV + (size_t)(n - 1) * count + c);
-            eval_point<B, E>(warp, InLevel{srcU + c, count, b, lentop, B, (tu >> 31) ? 0xFFFFFFFFu : 0u}, a);
-            eval_point<B, E>(warp, InLevel{srcV + c, count, b, lentop, B, (tv >> 31) ? 0xFFFFFFFFu : 0u}, bb);
-        }
+        const uint32_t fu = TOP ? 0u : ((Pu[(n - 1) * PP + lane] >> 31) ? 0xFFFFFFFFu : 0u);
+        const uint32_t fv = TOP ? 0u : ((Pv[(n - 1) * PP + lane] >> 31) ? 0xFFFFFFFFu : 0u);
+        eval_point<B, E>(warp, SmemParent{Pu + lane, b, lentop, B, fu}, a);
+        eval_point<B, E>(warp, SmemParent{Pv + lane, b, lentop, B, fv}, bb);
+        __syncwarp();
         mul_signed_to_smem<E>(a, bb, Y + (warp * 2 * E) * G + lane);
     }
     __syncthreads();

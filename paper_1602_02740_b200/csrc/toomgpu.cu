@@ -581,10 +581,11 @@ static toom_status launch_base(int E, const uint32_t* U, const uint32_t* V, uint
 template <int B, int E, bool TOP>
 static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out, cudaStream_t st) {
     const int nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
-    const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg);
+    const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg, Lv.n);
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
-        cudaFuncSetAttribute(k_fused_bottom<B, E, TOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_fused_bottom<B, E, TOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_fused_bottom<B, E, TOP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
     const unsigned grid = (unsigned)((Lv.count + 31) / 32);
