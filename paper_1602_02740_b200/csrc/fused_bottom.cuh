@@ -151,7 +151,7 @@ __host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nse
 }
 
 template <int B, int E, bool TOP>
-__global__ void __maxnreg__(E <= 18 ? 88 : 128) k_fused_bottom(
+__global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
     const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV, uint32_t* __restrict__ out,
     size_t count, int n, int b, int Lw, int wout, int nseg) {
     constexpr int NP = 2 * B - 1;
@@ -204,13 +204,33 @@ __global__ void __maxnreg__(E <= 18 ? 88 : 128) k_fused_bottom(
         const uint32_t fv = TOP ? 0u : ((Pv[(n - 1) * PP + lane] >> 31) ? 0xFFFFFFFFu : 0u);
         eval_point<B, E>(warp, SmemParent{Pu + lane, b, lentop, B, fu}, a);
         eval_point<B, E>(warp, SmemParent{Pv + lane, b, lentop, B, fv}, bb);
-        __syncwarp();
         mul_signed_to_smem<E>(a, bb, Y + (warp * 2 * E) * G + lane);
     }
     __syncthreads();
 
-    // ---- phase B: coefficient w_warp
-    if (valid) interp_row<B>(warp, Y + lane, 2 * E, Wb + (warp * Lw) * G + lane, Lw);
+    // ---- phase B: coefficient w_warp (w_0 = y_0 and w_2n = y_inf are copies)
+    if (valid) {
+        const uint32_t* Yl = Y + lane;
+        uint32_t* dst = Wb + (warp * Lw) * G + lane;
+        if (warp == 0 || warp == NP - 1) {
+            const uint32_t* src = Yl + (warp * 2 * E) * G;
+            for (int t = 0; t < Lw; ++t) dst[t * G] = src[t * G];
+        } else if constexpr (B == 3) {
+            switch (warp) {
+                case 1: tg_row_T3_1(Yl, 2 * E, dst, Lw); break;
+                case 2: tg_row_T3_2(Yl, 2 * E, dst, Lw); break;
+                default: tg_row_T3_3(Yl, 2 * E, dst, Lw); break;
+            }
+        } else {
+            switch (warp) {
+                case 1: tg_row_T4_1(Yl, 2 * E, dst, Lw); break;
+                case 2: tg_row_T4_2(Yl, 2 * E, dst, Lw); break;
+                case 3: tg_row_T4_3(Yl, 2 * E, dst, Lw); break;
+                case 4: tg_row_T4_4(Yl, 2 * E, dst, Lw); break;
+                default: tg_row_T4_5(Yl, 2 * E, dst, Lw); break;
+            }
+        }
+    }
     __syncthreads();
 
     // ---- phase C1: segment sums with local carries (OUT aliases Y)

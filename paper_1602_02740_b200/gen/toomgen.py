@@ -735,6 +735,48 @@ def emit_row_tables(ps: PointSet) -> str:
     return "\n".join(L)
 
 
+def emit_row_functions(ps: PointSet) -> str:
+    """Specialised per-coefficient streams for the fused kernel's phase B:
+    w_j = (sum_k A_jk y_k) / (o_j 2^s_j) with immediate multipliers and only
+    the nonzero terms; y_k in smem at Y[(k*w2 + t)*32], w_j to dst[t*32].
+    Requires w2 > Lw (child products are wider than the coefficients), so no
+    sign fill is ever needed.  Rows that are plain copies (w_0 = y_0,
+    w_2n = y_inf) are not emitted."""
+    rows = per_output_programs(build_interp(ps), f"interp_{ps.name}")
+    L = [f"// ---- specialised coefficient rows for {ps.name}"]
+    for j, pr in enumerate(rows):
+        if not pr.ops:
+            continue
+        op = pr.ops[0]
+        idx = [(pr.inputs.index(t.var), t.m) for t in op.terms]
+        assert all(t.s == 0 for t in op.terms) and op.shr < 32
+        L.append(f"// w_{j} = ({' '.join(f'{m:+d}*y{k}' for k, m in idx)}) / {op.odiv << op.shr}")
+        L.append(f"__device__ __forceinline__ void tg_row_{ps.name}_{j}(const uint32_t* __restrict__ Y, int w2, uint32_t* __restrict__ dst, int Lw) {{")
+        L.append("  uint64_t acc = 0; uint32_t bor = 0, qp = 0;")
+        for k, _ in idx:
+            L.append(f"  const uint32_t* __restrict__ y{k}p = Y + {k} * w2 * 32;")
+        L.append("  #pragma unroll 2")
+        L.append("  for (int t = 0; t <= Lw; ++t) {")
+        L.append("    uint64_t lin = acc;")
+        for k, m in idx:
+            L.append(f"    const uint32_t y{k} = y{k}p[t * 32];")
+        for k, m in idx:
+            if m > 0:
+                L.append(f"    lin = tg_madw({m}u, y{k}, lin);")
+            else:
+                L.append(f"    lin = tg_msubw({-m}u, y{k}, lin);")
+        L.append("    acc = (uint64_t)((int64_t)lin >> 32);")
+        if op.odiv != 1:
+            L.append(f"    const uint32_t q = tg_divexact_step((uint32_t)lin, bor, 0x{_inv32(op.odiv):08X}u, {op.odiv}u);")
+        else:
+            L.append("    const uint32_t q = (uint32_t)lin;")
+        L.append(f"    if (t > 0) dst[(t - 1) * 32] = tg_shr_limb_or_delay(qp, q, {op.shr});")
+        L.append("    qp = q;")
+        L.append("  }")
+        L.append("}")
+    return "\n".join(L)
+
+
 def stats(prog: Program):
     nterms = sum(len(op.terms) for op in prog.ops)
     ndiv = sum(1 for op in prog.ops if op.odiv != 1)
@@ -813,6 +855,14 @@ TG_HD TG_INLINE uint32_t tg_shr_limb(uint32_t lo, uint32_t hi, int r) {
   return (lo >> r) | (hi << (32 - r));
 #endif
 }
+// limb i of (x >> r) given lo = x[i], hi = x[i+1], 0 <= r < 32 (r = 0: lo)
+TG_HD TG_INLINE uint32_t tg_shr_limb_or_delay(uint32_t lo, uint32_t hi, int r) {
+#ifdef __CUDA_ARCH__
+  return __funnelshift_r(lo, hi, r);
+#else
+  return r ? ((lo >> r) | (hi << (32 - r))) : lo;
+#endif
+}
 // limb of (x << r) given lo = x[i-1], hi = x[i], 0 < r < 32
 TG_HD TG_INLINE uint32_t tg_shl_limb(uint32_t lo, uint32_t hi, int r) {
 #ifdef __CUDA_ARCH__
@@ -849,6 +899,9 @@ def generate_all():
         if ps.B <= 4:
             # fused bottom-level kernel tables: one point / one coefficient row per warp
             parts.append(emit_row_tables(ps))
+            parts.append("#ifdef __CUDACC__")
+            parts.append(emit_row_functions(ps))
+            parts.append("#endif")
         meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
     return "\n\n".join(parts) + "\n", meta
 
