@@ -112,6 +112,60 @@ __device__ __forceinline__ void interp_row(int j, const uint32_t* __restrict__ Y
     }
 }
 
+template <int B, int E>
+__device__ __forceinline__ void eval_point_rows(int k, const uint32_t* PU, const uint32_t* PV, uint32_t* dU, uint32_t* dV) {
+    if constexpr (B == 3) {
+        switch (k) {
+            case 0: tg_evalrow_T3_0<E>(PU, PV, dU, dV); break;
+            case 1: tg_evalrow_T3_1<E>(PU, PV, dU, dV); break;
+            case 2: tg_evalrow_T3_2<E>(PU, PV, dU, dV); break;
+            case 3: tg_evalrow_T3_3<E>(PU, PV, dU, dV); break;
+            default: tg_evalrow_T3_4<E>(PU, PV, dU, dV); break;
+        }
+    } else {
+        switch (k) {
+            case 0: tg_evalrow_T4_0<E>(PU, PV, dU, dV); break;
+            case 1: tg_evalrow_T4_1<E>(PU, PV, dU, dV); break;
+            case 2: tg_evalrow_T4_2<E>(PU, PV, dU, dV); break;
+            case 3: tg_evalrow_T4_3<E>(PU, PV, dU, dV); break;
+            case 4: tg_evalrow_T4_4<E>(PU, PV, dU, dV); break;
+            case 5: tg_evalrow_T4_5<E>(PU, PV, dU, dV); break;
+            default: tg_evalrow_T4_6<E>(PU, PV, dU, dV); break;
+        }
+    }
+}
+
+// two's-complement product of two E-limb two's-complement operands, 2E limbs
+// to dst[t*32]: the unsigned product A*B (Comba, IMAD.WIDE.U32 carry chains)
+// minus 2^(32E) * (sa*B + sb*A) (mod 2^(64E)), applied to the top E limbs.
+template <int E>
+__device__ __forceinline__ void mul_twos_to_smem(const uint32_t (&a)[E], const uint32_t (&b)[E], uint32_t* dst) {
+    const uint32_t ma = 0u - (a[E - 1] >> 31), mb = 0u - (b[E - 1] >> 31);
+    uint32_t c0 = 0, c1 = 0, c2 = 0;
+    // low half: plain columns
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+#pragma unroll
+        for (int i = 0; i <= k; ++i) TG_MADD(c0, c1, c2, a[i], b[k - i]);
+        dst[k * 32] = c0;
+        c0 = c1; c1 = c2; c2 = 0;
+    }
+    // high half: columns minus the correction, borrow chain in `br`
+    uint32_t br = 0;
+#pragma unroll
+    for (int k = E; k < 2 * E; ++k) {
+        if (k < 2 * E - 1) {
+#pragma unroll
+            for (int i = k - E + 1; i <= E - 1; ++i) TG_MADD(c0, c1, c2, a[i], b[k - i]);
+        }
+        const uint64_t sub = (uint64_t)(b[k - E] & ma) + (a[k - E] & mb) + br;
+        const uint64_t x = (uint64_t)c0 - (uint32_t)sub;
+        dst[k * 32] = (uint32_t)x;
+        br = (uint32_t)(sub >> 32) + (uint32_t)((x >> 32) & 1u);
+        c0 = c1; c1 = c2; c2 = 0;
+    }
+}
+
 // |a| * |b| with the product sign applied, 2E limbs streamed to dst[t*32]
 template <int E>
 __device__ __forceinline__ void mul_signed_to_smem(uint32_t (&a)[E], uint32_t (&b)[E], uint32_t* dst) {
@@ -146,7 +200,7 @@ __device__ __forceinline__ void mul_signed_to_smem(uint32_t (&a)[E], uint32_t (&
 __host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nseg, int n) {
     const int NP = 2 * B - 1;
     size_t wreg = (size_t)NP * Lw * 32;
-    if ((size_t)2 * n * 33 > wreg) wreg = (size_t)2 * n * 33;   // parents staged in the W region
+    if ((size_t)2 * B * E * 33 > wreg) wreg = (size_t)2 * B * E * 33;   // parents staged in the W region
     return (size_t)4 * ((size_t)NP * 2 * E * 32 + wreg + 4 * 32 * (size_t)nseg);
 }
 
@@ -159,7 +213,7 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
     extern __shared__ uint32_t sm[];
     uint32_t* Y = sm;                          // [NP][2E][G], later OUT [wout][G]
     uint32_t* Wb = Y + NP * 2 * E * G;         // [NP][Lw][G]
-    const int wreg = (NP * Lw * G > 2 * n * 33) ? NP * Lw * G : 2 * n * 33;
+    const int wreg = (NP * Lw * G > 2 * B * E * 33) ? NP * Lw * G : 2 * B * E * 33;
     uint32_t* CO = Wb + wreg;                  // [nseg][G] segment carry-out
     uint32_t* L0 = CO + nseg * G;              // [nseg][G] limb 0 of the segment
     uint32_t* ON = L0 + nseg * G;              // [nseg][G] limbs 1.. all ones
@@ -170,41 +224,51 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
     const bool valid = c < count;
     const int lentop = n - (B - 1) * b;
 
-    // ---- phase A0: stage the 32 parents' operands in smem (W region, unused
-    // until phase B): Pu/Pv [limb][PP], coalesced global loads by all warps
+    // ---- phase A0: stage the 32 parents' operand blocks in smem (W region,
+    // unused until phase B), padded to E limbs per block (zero fill, sign fill
+    // for the top block below the top level): P[op][j][t][33]
     constexpr int PP = 33;                     // padded pitch (conflict-free transpose)
     uint32_t* Pu = Wb;
-    uint32_t* Pv = Wb + n * PP;
+    uint32_t* Pv = Wb + B * E * PP;
     {
         const size_t c0 = (size_t)blockIdx.x * G;
         const int nin = (int)min((size_t)G, count - c0);
-        if (TOP) {
-            // row-major rows of n limbs: thread idx -> (instance i, limb t)
-            for (int idx = threadIdx.x; idx < nin * n; idx += blockDim.x) {
-                const int i = idx / n, t = idx - i * n;
-                Pu[t * PP + i] = __ldg(srcU + (c0 + i) * (size_t)n + t);
-                Pv[t * PP + i] = __ldg(srcV + (c0 + i) * (size_t)n + t);
-            }
-        } else {
-            // interleaved [n][count]: rows of 32 consecutive instances
-            for (int t = warp; t < n; t += NP) {
-                if (lane < nin) {
-                    Pu[t * PP + lane] = __ldg(srcU + (size_t)t * count + c0 + lane);
-                    Pv[t * PP + lane] = __ldg(srcV + (size_t)t * count + c0 + lane);
+        // rows t of block j: source limb j*b + t when t < len_j
+        for (int r = warp; r < B * E; r += NP) {
+            const int j = r / E, t = r - j * E;
+            const int len = (j == B - 1) ? lentop : b;
+            const int limb = j * b + t;
+            uint32_t xu = 0, xv = 0;
+            if (TOP) {
+                // row-major: lane i reads instance c0+i (uncoalesced, cached by L1/L2)
+                if (lane < nin && t < len) {
+                    xu = __ldg(srcU + (c0 + lane) * (size_t)n + limb);
+                    xv = __ldg(srcV + (c0 + lane) * (size_t)n + limb);
+                }
+            } else if (lane < nin) {
+                if (t < len) {
+                    xu = __ldg(srcU + (size_t)limb * count + c0 + lane);
+                    xv = __ldg(srcV + (size_t)limb * count + c0 + lane);
+                } else if (j == B - 1) {   // sign fill of the top block
+                    xu = (__ldg(srcU + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
+                    xv = (__ldg(srcV + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
                 }
             }
+            Pu[r * PP + lane] = xu;
+            Pv[r * PP + lane] = xv;
         }
     }
     __syncthreads();
 
-    // ---- phase A: evaluate point `warp` of both operands (from smem), multiply
+    // ---- phase A: evaluate point `warp` of both operands (from smem) into
+    // the warp's own Y[k] slot, load to registers, multiply into the same slot
     if (valid) {
+        uint32_t* slot = Y + (warp * 2 * E) * G + lane;
+        eval_point_rows<B, E>(warp, Pu + lane, Pv + lane, slot, slot + E * G);
         uint32_t a[E], bb[E];
-        const uint32_t fu = TOP ? 0u : ((Pu[(n - 1) * PP + lane] >> 31) ? 0xFFFFFFFFu : 0u);
-        const uint32_t fv = TOP ? 0u : ((Pv[(n - 1) * PP + lane] >> 31) ? 0xFFFFFFFFu : 0u);
-        eval_point<B, E>(warp, SmemParent{Pu + lane, b, lentop, B, fu}, a);
-        eval_point<B, E>(warp, SmemParent{Pv + lane, b, lentop, B, fv}, bb);
-        mul_signed_to_smem<E>(a, bb, Y + (warp * 2 * E) * G + lane);
+#pragma unroll
+        for (int t = 0; t < E; ++t) { a[t] = slot[t * G]; bb[t] = slot[(E + t) * G]; }
+        mul_twos_to_smem<E>(a, bb, slot);
     }
     __syncthreads();
 

@@ -777,6 +777,43 @@ def emit_row_functions(ps: PointSet) -> str:
     return "\n".join(L)
 
 
+def emit_evalrow_functions(ps: PointSet) -> str:
+    """Specialised per-point evaluation streams for the fused kernel's phase A:
+    U(p:q) = sum_j p^j q^(n-j) u_j for BOTH operands in one rolled loop, with
+    immediate multipliers.  Parent blocks are staged in smem padded to E limbs
+    (zero / sign filled), block j limb t at P[(j*E + t)*33]; the two E-limb
+    results go to dU[t*32], dV[t*32]."""
+    n = ps.n
+    L = [f"// ---- specialised point evaluations for {ps.name}"]
+    for k, (p, q) in enumerate(ps.points):
+        coef = [p**j * q ** (n - j) for j in range(ps.B)]
+        terms = [(j, c) for j, c in enumerate(coef) if c != 0]
+        L.append(f"// U({p}:{q}) = {' '.join(f'{c:+d}*u{j}' for j, c in terms)}")
+        L.append(f"template <int E> __device__ __forceinline__ void tg_evalrow_{ps.name}_{k}("
+                 "const uint32_t* __restrict__ PU, const uint32_t* __restrict__ PV, uint32_t* __restrict__ dU, uint32_t* __restrict__ dV) {")
+        if len(terms) == 1 and terms[0][1] == 1:
+            j = terms[0][0]
+            L.append("  #pragma unroll 2")
+            L.append(f"  for (int t = 0; t < E; ++t) {{ dU[t * 32] = PU[({j} * E + t) * 33]; dV[t * 32] = PV[({j} * E + t) * 33]; }}")
+            L.append("}")
+            continue
+        L.append("  uint64_t au = 0, av = 0;")
+        L.append("  #pragma unroll 2")
+        L.append("  for (int t = 0; t < E; ++t) {")
+        L.append("    uint64_t lu = au, lv = av;")
+        for j, c in terms:
+            L.append(f"    {{ const uint32_t x = PU[({j} * E + t) * 33], y = PV[({j} * E + t) * 33];")
+            if c > 0:
+                L.append(f"      lu = tg_madw({c}u, x, lu); lv = tg_madw({c}u, y, lv); }}")
+            else:
+                L.append(f"      lu = tg_msubw({-c}u, x, lu); lv = tg_msubw({-c}u, y, lv); }}")
+        L.append("    dU[t * 32] = (uint32_t)lu; dV[t * 32] = (uint32_t)lv;")
+        L.append("    au = (uint64_t)((int64_t)lu >> 32); av = (uint64_t)((int64_t)lv >> 32);")
+        L.append("  }")
+        L.append("}")
+    return "\n".join(L)
+
+
 def stats(prog: Program):
     nterms = sum(len(op.terms) for op in prog.ops)
     ndiv = sum(1 for op in prog.ops if op.odiv != 1)
@@ -901,6 +938,7 @@ def generate_all():
             parts.append(emit_row_tables(ps))
             parts.append("#ifdef __CUDACC__")
             parts.append(emit_row_functions(ps))
+            parts.append(emit_evalrow_functions(ps))
             parts.append("#endif")
         meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
     return "\n\n".join(parts) + "\n", meta
