@@ -233,29 +233,45 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
     {
         const size_t c0 = (size_t)blockIdx.x * G;
         const int nin = (int)min((size_t)G, count - c0);
-        // rows t of block j: source limb j*b + t when t < len_j
-        for (int r = warp; r < B * E; r += NP) {
+        // rows t of block j: source limb j*b + t when t < len_j; all loads of
+        // a warp are issued before its stores (compile-time trip count)
+        uint32_t fu = 0, fv = 0;
+        if (!TOP && lane < nin) {
+            fu = (__ldg(srcU + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
+            fv = (__ldg(srcV + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
+        }
+        constexpr int ROWS = B * E, ITER = (ROWS + NP - 1) / NP;
+        uint32_t xu[ITER], xv[ITER];
+#pragma unroll
+        for (int q = 0; q < ITER; ++q) {
+            const int r = warp + q * NP;
             const int j = r / E, t = r - j * E;
             const int len = (j == B - 1) ? lentop : b;
             const int limb = j * b + t;
-            uint32_t xu = 0, xv = 0;
-            if (TOP) {
-                // row-major: lane i reads instance c0+i (uncoalesced, cached by L1/L2)
-                if (lane < nin && t < len) {
-                    xu = __ldg(srcU + (c0 + lane) * (size_t)n + limb);
-                    xv = __ldg(srcV + (c0 + lane) * (size_t)n + limb);
-                }
-            } else if (lane < nin) {
+            xu[q] = 0;
+            xv[q] = 0;
+            if (r < ROWS && lane < nin) {
                 if (t < len) {
-                    xu = __ldg(srcU + (size_t)limb * count + c0 + lane);
-                    xv = __ldg(srcV + (size_t)limb * count + c0 + lane);
-                } else if (j == B - 1) {   // sign fill of the top block
-                    xu = (__ldg(srcU + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
-                    xv = (__ldg(srcV + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
+                    if (TOP) {
+                        xu[q] = __ldg(srcU + (c0 + lane) * (size_t)n + limb);
+                        xv[q] = __ldg(srcV + (c0 + lane) * (size_t)n + limb);
+                    } else {
+                        xu[q] = __ldg(srcU + (size_t)limb * count + c0 + lane);
+                        xv[q] = __ldg(srcV + (size_t)limb * count + c0 + lane);
+                    }
+                } else if (j == B - 1) {
+                    xu[q] = fu;
+                    xv[q] = fv;
                 }
             }
-            Pu[r * PP + lane] = xu;
-            Pv[r * PP + lane] = xv;
+        }
+#pragma unroll
+        for (int q = 0; q < ITER; ++q) {
+            const int r = warp + q * NP;
+            if (r < ROWS) {
+                Pu[r * PP + lane] = xu[q];
+                Pv[r * PP + lane] = xv[q];
+            }
         }
     }
     __syncthreads();

@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 
 }  // namespace tg
 #include "fused_bottom.cuh"
+#include "toplevel.cuh"
 namespace tg {
 
 // ------------------------------------------------------------------------
@@ -611,6 +612,48 @@ static toom_status launch_fused(const Level& Lv, bool top, const uint32_t* su, c
     return TOOM_EUNSUPPORTED;
 }
 
+static bool g_disable_toprows = false;
+
+static bool top_rows_ok(const Level& Lv) {
+    if (g_disable_toprows || (Lv.B != 3 && Lv.B != 4)) return false;
+    const int nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
+    return interp_top_rows_smem(Lv.B, Lv.Lw, nseg) <= 200 * 1024 && Lv.Lw == 2 * Lv.b + 1;
+}
+
+static toom_status launch_eval_top_rows(const Level& Lv, const uint32_t* u, const uint32_t* v, uint32_t* U1,
+                                        uint32_t* V1, cudaStream_t st) {
+    ProfScope ps(CAT_EVAL, st);
+    const unsigned grid = (unsigned)((Lv.count + 31) / 32);
+    if (Lv.B == 3) k_eval_top_rows<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
+    else k_eval_top_rows<4><<<grid, 32 * 7, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
+    ps.done(st);
+    ++t_launches;
+    return TOOM_OK;
+}
+
+template <int B>
+static void launch_interp_top_rows_t(const Level& Lv, const uint32_t* P1, uint32_t* w, cudaStream_t st) {
+    const int nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
+    const size_t smem = interp_top_rows_smem(B, Lv.Lw, nseg);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_interp_top_rows<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_interp_top_rows<B>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    const unsigned grid = (unsigned)((Lv.count + 31) / 32);
+    k_interp_top_rows<B><<<grid, 32 * (2 * B - 1), smem, st>>>(P1, w, Lv.count, 2 * Lv.e, Lv.Lw, Lv.b, 2 * Lv.n, nseg);
+}
+
+static toom_status launch_interp_top_rows(const Level& Lv, const uint32_t* P1, uint32_t* w, cudaStream_t st) {
+    ProfScope ps(CAT_INTERP, st);
+    if (Lv.B == 3) launch_interp_top_rows_t<3>(Lv, P1, w, st);
+    else launch_interp_top_rows_t<4>(Lv, P1, w, st);
+    ps.done(st);
+    ++t_launches;
+    return TOOM_OK;
+}
+
 // base level reached directly (no Toom level): schoolbook on row-major
 // operands via a transposing copy
 // row-major [count][n] -> interleaved [E][count], zero rows for n <= i < E
@@ -653,6 +696,11 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         const Level& Lv = plan.lv[l];
         const uint32_t* su = l == 0 ? u : (const uint32_t*)(ws + plan.lv[l - 1].offU);
         const uint32_t* sv = l == 0 ? v : (const uint32_t*)(ws + plan.lv[l - 1].offV);
+        if (l == 0 && top_rows_ok(Lv)) {
+            if ((s = launch_eval_top_rows(Lv, su, sv, (uint32_t*)(ws + Lv.offU), (uint32_t*)(ws + Lv.offV), st)))
+                return s;
+            continue;
+        }
         if ((s = launch_eval(Lv.B, l == 0, su, sv, (uint32_t*)(ws + Lv.offU), (uint32_t*)(ws + Lv.offV), Lv.count, Lv.n,
                              Lv.b, Lv.e, st)))
             return s;
@@ -675,6 +723,10 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
     for (size_t l = Lt; l-- > 0;) {
         const Level& Lv = plan.lv[l];
         uint32_t* out = l == 0 ? w : (uint32_t*)(ws + plan.lv[l - 1].offP);
+        if (l == 0 && top_rows_ok(Lv)) {
+            if ((s = launch_interp_top_rows(Lv, (const uint32_t*)(ws + Lv.offP), w, st))) return s;
+            continue;
+        }
         if ((s = launch_interp(Lv.B, l == 0, (const uint32_t*)(ws + Lv.offP), (uint32_t*)(ws + Lv.offW), out, Lv.count,
                                2 * Lv.e, Lv.Lw, Lv.b, 2 * Lv.n, st)))
             return s;
@@ -875,7 +927,12 @@ toom_status toom_base_interleaved(uint32_t* w, const uint32_t* u, const uint32_t
 
 int toom_npoints(int B) { return ps_desc(B).npts; }
 
-void toom_set_fused(int on) { g_disable_fused = (on == 0); }
+void toom_set_fused(int on) {
+    // 0: every level staged (k_eval / k_base / k_interp); 1: fused bottom level
+    // and warp-per-row top level (default)
+    g_disable_fused = (on == 0);
+    g_disable_toprows = (on == 0);
+}
 
 void toom_profile_enable(int on) {
     t_prof = on != 0;

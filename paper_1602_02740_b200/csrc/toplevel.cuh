@@ -1,0 +1,196 @@
+// Top-level evaluation (step a1+a2) and interpolation + recomposition
+// (steps a4+a5) for batched products whose top level is Toom-3/Toom-4, with
+// one warp per point / per coefficient row and one lane per product.
+//
+//   k_eval_top_rows<B>    CTA = 32 products x NP warps.  Row-major operand
+//                         limbs are staged through smem in chunks of CH limbs
+//                         with coalesced loads; warp k streams U(x_k), V(x_k)
+//                         (homogeneous coefficients p^j q^(n-j)) and writes the
+//                         child operands in the interleaved level layout.
+//   k_interp_top_rows<B>  CTA = 32 products x NP warps.  The child products y_k
+//                         are staged through smem in chunks; warp j streams the
+//                         coefficient row w_j = (sum_k A_jk y_k)/D_j (the
+//                         even-odd + Newton listing program composed per row,
+//                         PAPER.md:162) into smem; then the warps recompose
+//                         w = sum_j w_j 2^(32 b j) segment by segment with a
+//                         carry resolution between segments and write the
+//                         row-major result.
+#pragma once
+
+namespace tg {
+
+template <int B>
+__device__ __forceinline__ uint32_t rowstep(int j, const uint32_t (&y)[2 * B - 1], tg_rowstate& st) {
+    if constexpr (B == 3) return tg_rowstep_T3(j, y, st);
+    else return tg_rowstep_T4(j, y, st);
+}
+
+constexpr int TOP_CH = 16;   // limbs per staged chunk
+
+template <int B>
+__global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
+    const uint32_t* __restrict__ u, const uint32_t* __restrict__ v, uint32_t* __restrict__ U1,
+    uint32_t* __restrict__ V1, size_t count, int n, int b, int e) {
+    constexpr int NP = 2 * B - 1, G = 32, CH = TOP_CH, PP = 33;
+    __shared__ uint32_t S[2][B][CH][PP];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t c0 = (size_t)blockIdx.x * G;
+    const int nin = (int)min((size_t)G, count - c0);
+    const size_t c = c0 + lane;
+    const int lentop = n - (B - 1) * b;
+    uint64_t cf[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) cf[j] = (uint64_t)evalc<B>(warp, j);
+    const size_t stride_limb = (size_t)NP * count;
+    uint64_t au = 0, av = 0;
+    for (int t0 = 0; t0 < e; t0 += CH) {
+        // stage: (op, i, j, tt) with tt fastest -> coalesced row segments
+        for (int idx = threadIdx.x; idx < 2 * G * B * CH; idx += blockDim.x) {
+            const int tt = idx % CH;
+            const int j = (idx / CH) % B;
+            const int i = (idx / (CH * B)) % G;
+            const int op = idx / (CH * B * G);
+            const int t = t0 + tt;
+            const int len = (j == B - 1) ? lentop : b;
+            uint32_t x = 0;
+            if (i < nin && t < len) x = __ldg((op ? v : u) + (c0 + i) * (size_t)n + (size_t)j * b + t);
+            S[op][j][tt][i] = x;
+        }
+        __syncthreads();
+        if (lane < nin) {
+            const int tmax = min(CH, e - t0);
+            for (int tt = 0; tt < tmax; ++tt) {
+                uint64_t lu = au, lv = av;
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    lu += cf[j] * (uint64_t)S[0][j][tt][lane];
+                    lv += cf[j] * (uint64_t)S[1][j][tt][lane];
+                }
+                const size_t o = (size_t)(t0 + tt) * stride_limb + (size_t)warp * count + c;
+                U1[o] = (uint32_t)lu;
+                V1[o] = (uint32_t)lv;
+                au = (uint64_t)((int64_t)lu >> 32);
+                av = (uint64_t)((int64_t)lv >> 32);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__host__ __device__ inline size_t interp_top_rows_smem(int B, int Lw, int nseg) {
+    const int NP = 2 * B - 1;
+    return (size_t)4 * 32 * ((size_t)(NP - 2) * Lw + (size_t)NP * TOP_CH + 4 * (size_t)nseg);
+}
+
+template <int B>
+__global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_rows(
+    const uint32_t* __restrict__ P1, uint32_t* __restrict__ w, size_t count, int ywidth, int Lw, int b, int wout,
+    int nseg) {
+    constexpr int NP = 2 * B - 1, G = 32, CH = TOP_CH;
+    extern __shared__ uint32_t sm[];
+    uint32_t* W = sm;                              // rows 1..NP-2: [NP-2][Lw][32]
+    uint32_t* Ys = W + (NP - 2) * Lw * G;          // [NP][CH][32]
+    uint32_t* CO = Ys + NP * CH * G;               // [nseg][32]
+    uint32_t* L0 = CO + nseg * G;
+    uint32_t* ON = L0 + nseg * G;
+    uint32_t* CI = ON + nseg * G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t c0 = (size_t)blockIdx.x * G;
+    const int nin = (int)min((size_t)G, count - c0);
+    const size_t c = c0 + lane;
+    const bool valid = lane < nin;
+    const size_t S = (size_t)NP * count;           // limb stride of the child products
+
+    // ---- phase 1: coefficient rows 1..NP-2 (rows 0 and NP-1 are y_0, y_inf)
+    uint32_t fill = 0;
+    if (valid) fill = (__ldg(P1 + (size_t)(ywidth - 1) * S + (size_t)(warp) * count + c) >> 31) ? 0xFFFFFFFFu : 0u;
+    tg_rowstate st{0, 0, 0};
+    for (int t0 = 0; t0 <= Lw; t0 += CH) {
+        // warp k stages y_k limbs [t0, t0+CH) for the 32 products
+        {
+            uint32_t x[CH];
+#pragma unroll
+            for (int tt = 0; tt < CH; ++tt) {
+                const int t = t0 + tt;
+                x[tt] = 0;
+                if (valid) x[tt] = (t < ywidth) ? __ldg(P1 + (size_t)t * S + (size_t)warp * count + c) : fill;
+            }
+#pragma unroll
+            for (int tt = 0; tt < CH; ++tt) Ys[(warp * CH + tt) * G + lane] = x[tt];
+        }
+        __syncthreads();
+        if (valid && warp >= 1 && warp <= NP - 2) {
+            const int tmax = min(CH, Lw + 1 - t0);
+            for (int tt = 0; tt < tmax; ++tt) {
+                uint32_t y[NP];
+#pragma unroll
+                for (int k = 0; k < NP; ++k) y[k] = Ys[(k * CH + tt) * G + lane];
+                const uint32_t r = rowstep<B>(warp, y, st);
+                const int t = t0 + tt;
+                if (t >= 1) W[((warp - 1) * Lw + t - 1) * G + lane] = r;
+            }
+        }
+        __syncthreads();
+    }
+
+    // limb t of coefficient j (j = 0 and NP-1 straight from the products)
+    auto wl = [&](int j, int t) -> uint32_t {
+        if (j == 0 || j == NP - 1) return __ldg(P1 + (size_t)t * S + (size_t)j * count + c);
+        return W[((j - 1) * Lw + t) * G + lane];
+    };
+    // segment s limb r (without carry): w_s[r] + w_{s-1}[b+r] + (r==0) w_{s-2}[2b];
+    // every w_j >= 0 at the top level (sums of products of unsigned blocks)
+    auto seg_sum = [&](int s, int r) -> uint64_t {
+        uint64_t x = 0;
+        if (s < NP) x += wl(s, r);
+        if (s >= 1 && s - 1 < NP) x += wl(s - 1, b + r);
+        if (r == 0 && s >= 2 && s - 2 < NP) x += wl(s - 2, 2 * b);
+        return x;
+    };
+    // ---- phase 2: segment carry-outs
+    if (valid) {
+        for (int s = warp; s < nseg; s += NP) {
+            const int len = min(b, wout - s * b);
+            uint64_t carry = 0;
+            uint32_t ones = 0xFFFFFFFFu, l0 = 0;
+            for (int r = 0; r < len; ++r) {
+                const uint64_t x = carry + seg_sum(s, r);
+                const uint32_t lo = (uint32_t)x;
+                if (r == 0) l0 = lo; else ones &= lo;
+                carry = x >> 32;
+            }
+            CO[s * G + lane] = (uint32_t)carry;
+            L0[s * G + lane] = l0;
+            ON[s * G + lane] = ones == 0xFFFFFFFFu;
+        }
+    }
+    __syncthreads();
+    if (valid && warp == 0) {
+        uint32_t cin = 0;
+        for (int s = 0; s < nseg; ++s) {
+            CI[s * G + lane] = cin;
+            uint32_t cout = CO[s * G + lane];
+            if (cin) {
+                const uint32_t l0 = L0[s * G + lane];
+                if (l0 + cin < l0 && ON[s * G + lane]) cout += 1;
+            }
+            cin = cout;
+        }
+    }
+    __syncthreads();
+    // ---- phase 3: recompute each segment with its carry-in and write the row
+    if (valid) {
+        uint32_t* row = w + c * (size_t)wout;
+        for (int s = warp; s < nseg; s += NP) {
+            const int len = min(b, wout - s * b);
+            uint64_t carry = CI[s * G + lane];
+            for (int r = 0; r < len; ++r) {
+                const uint64_t x = carry + seg_sum(s, r);
+                row[s * b + r] = (uint32_t)x;
+                carry = x >> 32;
+            }
+        }
+    }
+}
+
+}  // namespace tg

@@ -752,7 +752,9 @@ def emit_row_functions(ps: PointSet) -> str:
         assert all(t.s == 0 for t in op.terms) and op.shr < 32
         L.append(f"// w_{j} = ({' '.join(f'{m:+d}*y{k}' for k, m in idx)}) / {op.odiv << op.shr}")
         L.append(f"__device__ __forceinline__ void tg_row_{ps.name}_{j}(const uint32_t* __restrict__ Y, int w2, uint32_t* __restrict__ dst, int Lw) {{")
-        L.append("  uint64_t acc = 0; uint32_t bor = 0, qp = 0;")
+        L.append("  uint64_t acc = 0; uint32_t qp = 0;")
+        if op.odiv != 1:
+            L.append("  uint32_t bor = 0;")
         for k, _ in idx:
             L.append(f"  const uint32_t* __restrict__ y{k}p = Y + {k} * w2 * 32;")
         L.append("  #pragma unroll 2")
@@ -774,6 +776,45 @@ def emit_row_functions(ps: PointSet) -> str:
         L.append("    qp = q;")
         L.append("  }")
         L.append("}")
+    return "\n".join(L)
+
+
+def emit_rowstep_functions(ps: PointSet) -> str:
+    """One LSB-first step of each nontrivial coefficient row: given limb t of
+    every y_k, update the row's carry / borrow state and return limb t-1 of
+    w_j (the exact shift lags one limb).  Callers choose where y and w live."""
+    rows = per_output_programs(build_interp(ps), f"interp_{ps.name}")
+    NP = ps.npoints
+    L = [f"// ---- coefficient row steps for {ps.name}"]
+    for j, pr in enumerate(rows):
+        if not pr.ops:
+            continue
+        op = pr.ops[0]
+        idx = [(pr.inputs.index(t.var), t.m) for t in op.terms]
+        L.append(f"__device__ __forceinline__ uint32_t tg_rowstep_{ps.name}_{j}(const uint32_t (&y)[{NP}], tg_rowstate& st) {{")
+        L.append("  uint64_t lin = st.acc;")
+        for k, m in idx:
+            L.append(f"  lin = {'tg_madw' if m > 0 else 'tg_msubw'}({abs(m)}u, y[{k}], lin);")
+        L.append("  st.acc = (uint64_t)((int64_t)lin >> 32);")
+        if op.odiv != 1:
+            L.append(f"  const uint32_t q = tg_divexact_step((uint32_t)lin, st.bor, 0x{_inv32(op.odiv):08X}u, {op.odiv}u);")
+        else:
+            L.append("  const uint32_t q = (uint32_t)lin;")
+        L.append(f"  const uint32_t r = tg_shr_limb_or_delay(st.qp, q, {op.shr});")
+        L.append("  st.qp = q;")
+        L.append("  return r;")
+        L.append("}")
+    L.append(f"__device__ __forceinline__ uint32_t tg_rowstep_{ps.name}(int j, const uint32_t (&y)[{NP}], tg_rowstate& st) {{")
+    L.append("  switch (j) {")
+    for j, pr in enumerate(rows):
+        if pr.ops:
+            L.append(f"    case {j}: return tg_rowstep_{ps.name}_{j}(y, st);")
+        else:
+            k = pr.inputs.index(pr.outputs[0])
+            L.append(f"    case {j}: {{ const uint32_t r = st.qp; st.qp = y[{k}]; return r; }}")
+    L.append("  }")
+    L.append("  return 0u;")
+    L.append("}")
     return "\n".join(L)
 
 
@@ -844,6 +885,7 @@ HEADER = """// AUTO-GENERATED by paper_1602_02740_b200/gen/toomgen.py -- do not 
 #endif
 #ifndef TG_HELPERS_DEFINED
 #define TG_HELPERS_DEFINED
+struct tg_rowstate { uint64_t acc; uint32_t bor, qp; };
 TG_HD TG_INLINE uint32_t tg_mulhi(uint32_t a, uint32_t b) {
 #ifdef __CUDA_ARCH__
   return __umulhi(a, b);
@@ -939,6 +981,7 @@ def generate_all():
             parts.append("#ifdef __CUDACC__")
             parts.append(emit_row_functions(ps))
             parts.append(emit_evalrow_functions(ps))
+            parts.append(emit_rowstep_functions(ps))
             parts.append("#endif")
         meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
     return "\n\n".join(parts) + "\n", meta
