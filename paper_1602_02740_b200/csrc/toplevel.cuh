@@ -77,20 +77,22 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
     }
 }
 
+constexpr int ITOP_CH = 12;  // limb steps per staged chunk of the child products
+
 __host__ __device__ inline size_t interp_top_rows_smem(int B, int Lw, int nseg) {
     const int NP = 2 * B - 1;
-    return (size_t)4 * 32 * ((size_t)(NP - 2) * Lw + (size_t)NP * TOP_CH + 4 * (size_t)nseg);
+    return (size_t)4 * 32 * ((size_t)(NP - 2) * Lw + 2 * (size_t)NP * ITOP_CH + 4 * (size_t)nseg);
 }
 
 template <int B>
 __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_rows(
     const uint32_t* __restrict__ P1, uint32_t* __restrict__ w, size_t count, int ywidth, int Lw, int b, int wout,
     int nseg) {
-    constexpr int NP = 2 * B - 1, G = 32, CH = TOP_CH;
+    constexpr int NP = 2 * B - 1, G = 32, CH = ITOP_CH;
     extern __shared__ uint32_t sm[];
     uint32_t* W = sm;                              // rows 1..NP-2: [NP-2][Lw][32]
-    uint32_t* Ys = W + (NP - 2) * Lw * G;          // [NP][CH][32]
-    uint32_t* CO = Ys + NP * CH * G;               // [nseg][32]
+    uint32_t* Ys = W + (NP - 2) * Lw * G;          // 2 buffers x [NP][CH][32]
+    uint32_t* CO = Ys + 2 * NP * CH * G;           // [nseg][32]
     uint32_t* L0 = CO + nseg * G;
     uint32_t* ON = L0 + nseg * G;
     uint32_t* CI = ON + nseg * G;
@@ -101,30 +103,43 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_rows(
     const bool valid = lane < nin;
     const size_t S = (size_t)NP * count;           // limb stride of the child products
 
-    // ---- phase 1: coefficient rows 1..NP-2 (rows 0 and NP-1 are y_0, y_inf)
-    uint32_t fill = 0;
-    if (valid) fill = (__ldg(P1 + (size_t)(ywidth - 1) * S + (size_t)(warp) * count + c) >> 31) ? 0xFFFFFFFFu : 0u;
-    tg_rowstate st{0, 0, 0};
-    for (int t0 = 0; t0 <= Lw; t0 += CH) {
-        // warp k stages y_k limbs [t0, t0+CH) for the 32 products
-        {
+    // stage limbs [t0, t0+CH) of y_k for k in [k0, k1) into buffer `buf`
+    auto stage = [&](int t0, int k0, int k1, int buf) {
+        uint32_t* dst = Ys + buf * NP * CH * G;
+        for (int k = k0; k < k1; ++k) {
+            uint32_t fill = 0;
+            if (valid) fill = (__ldg(P1 + (size_t)(ywidth - 1) * S + (size_t)k * count + c) >> 31) ? 0xFFFFFFFFu : 0u;
             uint32_t x[CH];
 #pragma unroll
             for (int tt = 0; tt < CH; ++tt) {
                 const int t = t0 + tt;
                 x[tt] = 0;
-                if (valid) x[tt] = (t < ywidth) ? __ldg(P1 + (size_t)t * S + (size_t)warp * count + c) : fill;
+                if (valid) x[tt] = (t < ywidth) ? __ldg(P1 + (size_t)t * S + (size_t)k * count + c) : fill;
             }
 #pragma unroll
-            for (int tt = 0; tt < CH; ++tt) Ys[(warp * CH + tt) * G + lane] = x[tt];
+            for (int tt = 0; tt < CH; ++tt) dst[(k * CH + tt) * G + lane] = x[tt];
         }
-        __syncthreads();
-        if (valid && warp >= 1 && warp <= NP - 2) {
+    };
+    // ---- phase 1: coefficient rows 1..NP-2 (rows 0 and NP-1 are y_0, y_inf).
+    // Warps 0 and NP-1 are the loaders (double-buffered chunks), warps
+    // 1..NP-2 compute their row from the current chunk.
+    stage(0, warp, warp + 1, 0);
+    __syncthreads();
+    tg_rowstate st{0, 0, 0};
+    const int nchunks = (Lw + 1 + CH - 1) / CH;
+    for (int ci = 0; ci < nchunks; ++ci) {
+        const int t0 = ci * CH;
+        if (warp == 0) {
+            if (ci + 1 < nchunks) stage(t0 + CH, 0, (NP + 1) / 2, (ci + 1) & 1);
+        } else if (warp == NP - 1) {
+            if (ci + 1 < nchunks) stage(t0 + CH, (NP + 1) / 2, NP, (ci + 1) & 1);
+        } else if (valid) {
+            const uint32_t* src = Ys + (ci & 1) * NP * CH * G;
             const int tmax = min(CH, Lw + 1 - t0);
             for (int tt = 0; tt < tmax; ++tt) {
                 uint32_t y[NP];
 #pragma unroll
-                for (int k = 0; k < NP; ++k) y[k] = Ys[(k * CH + tt) * G + lane];
+                for (int k = 0; k < NP; ++k) y[k] = src[(k * CH + tt) * G + lane];
                 const uint32_t r = rowstep<B>(warp, y, st);
                 const int t = t0 + tt;
                 if (t >= 1) W[((warp - 1) * Lw + t - 1) * G + lane] = r;
@@ -147,17 +162,26 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_rows(
         if (r == 0 && s >= 2 && s - 2 < NP) x += wl(s - 2, 2 * b);
         return x;
     };
+    constexpr int RU = 8;   // limbs per batch: loads issued before the carry chain
     // ---- phase 2: segment carry-outs
     if (valid) {
         for (int s = warp; s < nseg; s += NP) {
             const int len = min(b, wout - s * b);
             uint64_t carry = 0;
             uint32_t ones = 0xFFFFFFFFu, l0 = 0;
-            for (int r = 0; r < len; ++r) {
-                const uint64_t x = carry + seg_sum(s, r);
-                const uint32_t lo = (uint32_t)x;
-                if (r == 0) l0 = lo; else ones &= lo;
-                carry = x >> 32;
+            for (int r0 = 0; r0 < len; r0 += RU) {
+                uint64_t x[RU];
+#pragma unroll
+                for (int q = 0; q < RU; ++q) x[q] = (r0 + q < len) ? seg_sum(s, r0 + q) : 0;
+#pragma unroll
+                for (int q = 0; q < RU; ++q) {
+                    if (r0 + q < len) {
+                        const uint64_t y = carry + x[q];
+                        const uint32_t lo = (uint32_t)y;
+                        if (r0 + q == 0) l0 = lo; else ones &= lo;
+                        carry = y >> 32;
+                    }
+                }
             }
             CO[s * G + lane] = (uint32_t)carry;
             L0[s * G + lane] = l0;
@@ -184,10 +208,18 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_rows(
         for (int s = warp; s < nseg; s += NP) {
             const int len = min(b, wout - s * b);
             uint64_t carry = CI[s * G + lane];
-            for (int r = 0; r < len; ++r) {
-                const uint64_t x = carry + seg_sum(s, r);
-                row[s * b + r] = (uint32_t)x;
-                carry = x >> 32;
+            for (int r0 = 0; r0 < len; r0 += RU) {
+                uint64_t x[RU];
+#pragma unroll
+                for (int q = 0; q < RU; ++q) x[q] = (r0 + q < len) ? seg_sum(s, r0 + q) : 0;
+#pragma unroll
+                for (int q = 0; q < RU; ++q) {
+                    if (r0 + q < len) {
+                        const uint64_t y = carry + x[q];
+                        row[s * b + r0 + q] = (uint32_t)y;
+                        carry = y >> 32;
+                    }
+                }
             }
         }
     }
