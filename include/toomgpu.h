@@ -47,16 +47,23 @@ typedef enum {
 } toom_status;
 
 /* Recursion plan (SURVEY.md §8 "reference shape"; SPEC.md:315-320 ToomPlan).
- * top_B: B of the top level: 3 (points 0,1,-1,2,inf), 4 (0,+-1,+-2,1/2,inf)
- *        or 8 (the paper's points 0,+-1,+-2,...,+-64);
+ * top_B: B of the top level: 3 (points 0,1,-1,2,inf), 4 (0,+-1,+-2,1/2,inf),
+ *        8 (the paper's points 0,+-1,+-2,...,+-64) or
+ *        16 (31 points: 0, inf and the 29 smallest-height +-p/q, homogeneous;
+ *        BASELINE configs[4]);
  * lower levels: Toom-4 while the operand has more than t4 limbs, Toom-3
  *        while more than t3 limbs, schoolbook base case otherwise (<= 64 limbs);
- * chunk: products per scheduling chunk (0 = automatic).                     */
+ * chunk: products per scheduling chunk (0 = automatic);
+ * long_count: recursion levels with fewer than long_count instances (few,
+ *        long operands: the upper levels of one large product) run on the
+ *        limb-parallel long-vector kernels; deeper levels run one thread (or
+ *        lane) per instance.  0 = default (4096); 1 = never.               */
 typedef struct {
     int top_B;
     size_t t4;
     size_t t3;
     size_t chunk;
+    size_t long_count;
 } toom_plan_t;
 
 /* Default plan for a given top B: t4 = 256, t3 = 64, chunk automatic. */
@@ -64,7 +71,8 @@ toom_plan_t toom_default_plan(int B);
 
 /* w[i] = u[i] * v[i] for i < batch.
  * u, v: [batch][n] uint32 (row-major, device); w: [batch][2n] (device).
- * B: top-level B (see toom_plan_t).  n >= 1, batch >= 0 (batch 0: no-op).
+ * B: top-level B in {3, 4, 8, 16} (see toom_plan_t).  n >= 1, batch >= 0
+ * (batch 0: no-op).
  * Errors: TOOM_EINVAL (null/aliasing/B), TOOM_ENOMEM, TOOM_ECUDA.           */
 toom_status toom_mul_batched(uint32_t *w, const uint32_t *u, const uint32_t *v,
                              size_t n, size_t batch, int B, void *stream);

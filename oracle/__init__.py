@@ -56,6 +56,8 @@ def lib():
             L.oracle_schoolbook_batched.restype = None
             L.oracle_toom.argtypes = [P, sz, P, sz, P, ctypes.c_int, sz, sz]
             L.oracle_toom.restype = ctypes.c_int
+            L.oracle_toom_mt.argtypes = [P, sz, P, sz, P, ctypes.c_int, sz, sz, ctypes.c_int]
+            L.oracle_toom_mt.restype = ctypes.c_int
             L.oracle_toom_batched.argtypes = [P, P, P, sz, sz, ctypes.c_int, sz, sz]
             L.oracle_toom_batched.restype = ctypes.c_int
             L.oracle_reset_counters.argtypes = []
@@ -103,10 +105,15 @@ def schoolbook_batched(u, v) -> np.ndarray:
     return w
 
 
-def toom(u, v, top_B: int = 0, t4: int = T4_DEFAULT, t3: int = T3_DEFAULT) -> np.ndarray:
+def toom(u, v, top_B: int = 0, t4: int = T4_DEFAULT, t3: int = T3_DEFAULT, threads: int = 1) -> np.ndarray:
+    """O2 on one product; threads > 1 puts the 2B-1 top-level products on
+    that many host threads (Eq. 2.5)."""
     u, v = _u32(u), _u32(v)
     w = np.zeros(u.size + v.size, dtype=np.uint32)
-    st = lib().oracle_toom(_p(u), u.size, _p(v), v.size, _p(w), top_B, t4, t3)
+    if threads > 1:
+        st = lib().oracle_toom_mt(_p(u), u.size, _p(v), v.size, _p(w), top_B, t4, t3, threads)
+    else:
+        st = lib().oracle_toom(_p(u), u.size, _p(v), v.size, _p(w), top_B, t4, t3)
     if st:
         raise InexactDivision(f"oracle_toom status {st}")
     return w

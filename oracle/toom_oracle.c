@@ -36,6 +36,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <pthread.h>
 
 typedef uint32_t limb_t;
 
@@ -52,6 +53,7 @@ static _Thread_local int g_inexact = 0;      /* sticky: a "exact" division left 
 static _Thread_local int g_skip_division = -1; /* fault injection: skip the k-th listing-1 division */
 static _Thread_local long g_division_counter = 0;
 static _Thread_local long g_products[64];    /* products computed per recursion depth (Eq. 2.1) */
+static _Thread_local int g_top_threads = 1;  /* P processors on the top-level products (Eq. 2.5) */
 
 static void *xmalloc(size_t bytes) {
     void *p = malloc(bytes ? bytes : 1);
@@ -322,6 +324,62 @@ static bigint signed_product(const bigint *a, const bigint *b, const oracle_plan
     return y;
 }
 
+/* one pointwise product y = a*b of the Toom level (Eq. 2.1) */
+typedef struct {
+    bigint a, b, y;
+    const oracle_plan *plan;
+    int depth;
+    int inexact;
+    long products[64];
+} prod_task;
+
+typedef struct {
+    prod_task *tasks;
+    int ntask, tid, nthr;
+} prod_worker;
+
+static void *prod_worker_main(void *arg) {
+    prod_worker *w = (prod_worker *)arg;
+    for (int t = w->tid; t < w->ntask; t += w->nthr) {
+        prod_task *k = &w->tasks[t];
+        g_inexact = 0;
+        memset(g_products, 0, sizeof g_products);
+        k->y = signed_product(&k->a, &k->b, k->plan, k->depth);
+        k->inexact = g_inexact;
+        memcpy(k->products, g_products, sizeof g_products);
+        bi_free(&k->a);
+        bi_free(&k->b);
+    }
+    return NULL;
+}
+
+/* the products of one level, on `nthr` threads (independent: Eq. 2.5); the
+ * workers' sticky inexact flags and per-depth counters are merged back */
+static void run_products(prod_task *tasks, int ntask, int nthr) {
+    if (nthr > ntask) nthr = ntask;
+    if (nthr <= 1) {
+        for (int t = 0; t < ntask; t++) {
+            tasks[t].y = signed_product(&tasks[t].a, &tasks[t].b, tasks[t].plan, tasks[t].depth);
+            bi_free(&tasks[t].a);
+            bi_free(&tasks[t].b);
+        }
+        return;
+    }
+    pthread_t *th = (pthread_t *)xmalloc(sizeof(pthread_t) * nthr);
+    prod_worker *ws = (prod_worker *)xmalloc(sizeof(prod_worker) * nthr);
+    for (int i = 0; i < nthr; i++) {
+        ws[i].tasks = tasks; ws[i].ntask = ntask; ws[i].tid = i; ws[i].nthr = nthr;
+        pthread_create(&th[i], NULL, prod_worker_main, &ws[i]);
+    }
+    for (int i = 0; i < nthr; i++) pthread_join(th[i], NULL);
+    for (int t = 0; t < ntask; t++) {
+        g_inexact |= tasks[t].inexact;
+        for (int d = 0; d < 64; d++) g_products[d] += tasks[t].products[d];
+    }
+    free(th);
+    free(ws);
+}
+
 /* Split |a| into B blocks of b limbs (Eq. 1.1: u = U(2^b)); blocks past the
  * end are zero (the shorter operand is zero-padded). */
 static void split_blocks(const bigint *a, int B, size_t b, bigint *blk) {
@@ -368,8 +426,19 @@ static bigint toom_rec(const bigint *u, const bigint *v, const oracle_plan *plan
     split_blocks(u, B, b, ub);
     split_blocks(v, B, b, vb);
 
-    /* points: x_0 = 0 and +-2^j, j = 0..n-1 (PAPER.md:200 + §4): 2n+1 = 2B-1 products */
-    bigint W0 = signed_product(&ub[0], &vb[0], plan, depth + 1);   /* W(0) = U(0)V(0) */
+    /* points: x_0 = 0 and +-2^j, j = 0..n-1 (PAPER.md:200 + §4): 2n+1 = 2B-1 products.
+     * Evaluate every point first (Eq. 4.1, 4.3-4.4), then form the products
+     * (Eq. 2.1) -- at depth 0 on P threads (Eq. 2.5). */
+    prod_task *tasks = (prod_task *)xmalloc(sizeof(prod_task) * (2 * n + 1));
+    tasks[0].a = bi_copy(&ub[0]);                 /* U(0) = u_0 */
+    tasks[0].b = bi_copy(&vb[0]);
+    for (int j = 0; j < n; j++) {
+        eval_pair(ub, B, (unsigned)j, &tasks[1 + 2 * j].a, &tasks[2 + 2 * j].a);
+        eval_pair(vb, B, (unsigned)j, &tasks[1 + 2 * j].b, &tasks[2 + 2 * j].b);
+    }
+    for (int t = 0; t < 2 * n + 1; t++) { tasks[t].plan = plan; tasks[t].depth = depth + 1; }
+    run_products(tasks, 2 * n + 1, depth == 0 ? g_top_threads : 1);
+    bigint W0 = tasks[0].y;                       /* W(0) = U(0)V(0) */
     bigint *We = (bigint *)xmalloc(sizeof(bigint) * (n + 1));
     bigint *Wo = (bigint *)xmalloc(sizeof(bigint) * (n + 1));
     int64_t *z = (int64_t *)xmalloc(sizeof(int64_t) * (n + 1));
@@ -377,11 +446,8 @@ static bigint toom_rec(const bigint *u, const bigint *v, const oracle_plan *plan
     We[0] = bi_copy(&W0);          /* even problem: first point (0, W(0)) */
     Wo[0] = bi_new(1);             /* odd problem: first point (0, 0) */
     for (int j = 0; j < n; j++) {
-        bigint up, um, vp, vm;
-        eval_pair(ub, B, (unsigned)j, &up, &um);
-        eval_pair(vb, B, (unsigned)j, &vp, &vm);
-        bigint yp = signed_product(&up, &vp, plan, depth + 1);    /* W(x)  */
-        bigint ym = signed_product(&um, &vm, plan, depth + 1);    /* W(-x) */
+        bigint yp = tasks[1 + 2 * j].y;    /* W(x)  */
+        bigint ym = tasks[2 + 2 * j].y;    /* W(-x) */
         /* Eq. 4.5: W_e(x^2) = (W(x) + W(-x)) / 2 */
         bigint s = bi_add(&yp, &ym);
         We[j + 1] = bi_divexact_word(&s, 2);
@@ -391,9 +457,9 @@ static bigint toom_rec(const bigint *u, const bigint *v, const oracle_plan *plan
         Wo[j + 1] = bi_divexact_word(&dx, 2);
         z[j + 1] = (int64_t)1 << (2 * j);   /* z = x^2 = 4^j <= 2^28 for B = 16 */
         bi_free(&s); bi_free(&d); bi_free(&dx);
-        bi_free(&up); bi_free(&um); bi_free(&vp); bi_free(&vm);
         bi_free(&yp); bi_free(&ym);
     }
+    free(tasks);
 
     /* the two degree-n interpolations (independent) */
     listing_divided_differences(n, z, We);
@@ -433,11 +499,30 @@ static bigint toom_rec(const bigint *u, const bigint *v, const oracle_plan *plan
  * code 3). */
 int oracle_toom(const limb_t *u, size_t nu, const limb_t *v, size_t nv, limb_t *w,
                 int top_B, size_t t4, size_t t3) {
+    g_top_threads = 1;
     oracle_plan plan = {top_B, t4, t3};
     int saved = g_inexact;
     g_inexact = 0;
     bigint a = bi_from_limbs(u, nu), b = bi_from_limbs(v, nv);
     bigint r = toom_rec(&a, &b, &plan, 0);
+    for (size_t i = 0; i < nu + nv; i++) w[i] = i < r.n ? r.d[i] : 0;
+    int bad = g_inexact || r.n > nu + nv;
+    bi_free(&a); bi_free(&b); bi_free(&r);
+    g_inexact = saved || bad;
+    return bad ? 3 : 0;
+}
+
+/* as oracle_toom with the top-level products on `threads` host threads
+ * (Eq. 2.5: P processors on the 2B-1 top-level products) */
+int oracle_toom_mt(const limb_t *u, size_t nu, const limb_t *v, size_t nv, limb_t *w,
+                   int top_B, size_t t4, size_t t3, int threads) {
+    oracle_plan plan = {top_B, t4, t3};
+    int saved = g_inexact;
+    g_inexact = 0;
+    g_top_threads = threads > 1 ? threads : 1;
+    bigint a = bi_from_limbs(u, nu), b = bi_from_limbs(v, nv);
+    bigint r = toom_rec(&a, &b, &plan, 0);
+    g_top_threads = 1;
     for (size_t i = 0; i < nu + nv; i++) w[i] = i < r.n ? r.d[i] : 0;
     int bad = g_inexact || r.n > nu + nv;
     bi_free(&a); bi_free(&b); bi_free(&r);

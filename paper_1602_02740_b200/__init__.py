@@ -29,12 +29,13 @@ class ToomError(RuntimeError):
 
 
 class ToomPlan(ctypes.Structure):
-    """toom_plan_t: top_B, t4, t3, chunk (see include/toomgpu.h)."""
-    _fields_ = [("top_B", ctypes.c_int), ("t4", ctypes.c_size_t), ("t3", ctypes.c_size_t), ("chunk", ctypes.c_size_t)]
+    """toom_plan_t: top_B, t4, t3, chunk, long_count (see include/toomgpu.h)."""
+    _fields_ = [("top_B", ctypes.c_int), ("t4", ctypes.c_size_t), ("t3", ctypes.c_size_t), ("chunk", ctypes.c_size_t),
+                ("long_count", ctypes.c_size_t)]
 
 
-def plan(B: int, t4: int = 256, t3: int = 64, chunk: int = 0) -> ToomPlan:
-    return ToomPlan(B, t4, t3, chunk)
+def plan(B: int, t4: int = 256, t3: int = 64, chunk: int = 0, long_count: int = 0) -> ToomPlan:
+    return ToomPlan(B, t4, t3, chunk, long_count)
 
 
 # exported symbols and their ctypes signatures (tests check every symbol of
@@ -99,14 +100,14 @@ def _stream(stream=None) -> int:
 
 
 def toom_mul_batched(u: torch.Tensor, v: torch.Tensor, B: int = 4, t4: int = 256, t3: int = 64, chunk: int = 0,
-                     out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                     out: torch.Tensor | None = None, stream=None, long_count: int = 0) -> torch.Tensor:
     """w[i] = u[i] * v[i]; u, v: [batch][n] uint32 CUDA tensors; returns [batch][2n]."""
     if u.shape != v.shape or u.dim() != 2:
         raise ValueError("u and v must both be [batch][n]")
     batch, n = u.shape
     if out is None:
         out = torch.empty((batch, 2 * n), dtype=u.dtype, device=u.device)
-    p = plan(B, t4, t3, chunk)
+    p = plan(B, t4, t3, chunk, long_count)
     st = lib().toom_mul_batched_plan(_dev(out, "out"), _dev(u, "u"), _dev(v, "v"), n, batch, ctypes.byref(p),
                                      _stream(stream))
     _check(st, "toom_mul_batched")
@@ -174,9 +175,10 @@ def last_launch_count() -> int:
     return lib().toom_last_launch_count()
 
 
-def plan_describe(n: int, batch: int, B: int = 4, t4: int = 256, t3: int = 64, chunk: int = 0) -> dict:
+def plan_describe(n: int, batch: int, B: int = 4, t4: int = 256, t3: int = 64, chunk: int = 0,
+                  long_count: int = 0) -> dict:
     import json
-    p = plan(B, t4, t3, chunk)
+    p = plan(B, t4, t3, chunk, long_count)
     need = lib().toom_plan_describe(n, batch, ctypes.byref(p), None, 0)
     if not need:
         raise ValueError("invalid plan")

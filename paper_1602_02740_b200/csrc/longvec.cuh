@@ -1,0 +1,397 @@
+// Long-vector (limb-parallel) executor for the upper recursion levels of a
+// single large product (BASELINE configs C4, C5): few instances, long
+// operands.  SURVEY.md §7 H1/H2, DESIGN.md §6.
+//
+// Every evaluation (step a2), interpolation (step a4) and recomposition
+// (step a5) step of such a level is a sequence of OPS
+//
+//     dst = ((sum_i m_i * (S_i << s_i)) / o) >> shr        (o odd, all exact)
+//
+// over whole vectors, computed modulo 2^(32 W) (W = output limbs).  S_i is a
+// slice of a source vector (limbs [start, start+len), zero- or sign-extended
+// past len), which covers the block split of Eq. 1.1 (start = j b), the
+// recomposition w = sum_j w_j 2^(32 b j) of Eq. 1.3 (s_i = 32 b j) and the
+// generated evaluation / interpolation programs (gen/toomgen.py,
+// emit_long_tables: the paper's even-odd + listing programs, PAPER.md:114-120,
+// 154-158, 164-186, or their per-coefficient matrix form).
+//
+// One launch per op, one pass over the data: a tile of NT threads x CH limbs
+// forms the linear combination limb by limb (64- or 128-bit accumulators),
+// normalises it locally, and resolves the carries and the exact-division
+// borrows across the whole vector with a single-pass decoupled look-back scan.
+// The scan state between limb positions is (c, beta): c the signed carry of
+// the linear combination, beta the 2-adic division borrow; a chunk maps it by
+//     c'    = cout[p]                         p = piece(c) in {0,1,2}
+//     beta' = beta*m - c*m + g[p]  (mod o)
+// (p selects whether the chunk's low limbs absorb the incoming carry with a
+// borrow/carry out of the chunk; the borrow follows from the closed form
+// beta_t = -(x mod 2^(32t)) 2^(-32t) mod o).  These maps compose, so tiles
+// publish their aggregate before their predecessors finish.
+#pragma once
+
+namespace tg {
+
+constexpr int LV_MAXT = 40;     // terms per op
+constexpr int LV_NT = 256;      // threads per tile
+constexpr int LV_CH = 4;        // limbs per thread
+constexpr int LV_TL = LV_NT * LV_CH;
+constexpr int LV_MAXHALO = 8;   // look-ahead limbs of the final right shift (shr < 32*7)
+
+struct LTermDev {
+    const uint32_t* base;       // limb `start` of instance 0
+    long long inst_stride;      // limbs between instances
+    long long limb_stride;      // limbs between consecutive limbs of one value
+    int len;                    // slice length; limbs >= len are the fill
+    int sign;                   // 1: sign-extend past len, 0: zero-extend
+    int a, r;                   // left shift by 32 a + r bits (0 <= r < 32)
+    long long m;                // multiplier
+};
+
+struct LOpDev {
+    uint32_t* dst;
+    long long dst_inst_stride, dst_limb_stride;
+    int W;                      // output limbs
+    int nt;
+    uint32_t o, oinv;           // exact division by odd o (o = 1: none)
+    uint32_t p32, Mch, mi;      // 2^32 mod o, 2^(32 CH) mod o, (2^(32 CH))^-1 mod o
+    int sa, sr;                 // final right shift shr = 32 sa + sr
+    int tiles_per_inst;
+    int count;
+    int wide;                   // 128-bit accumulators
+    LTermDev t[LV_MAXT];
+};
+
+struct LAgg {
+    long long lo, hi;           // piece thresholds: p = 0 if c < lo, 2 if c >= hi, else 1
+    long long cout[3];
+    uint32_t m, g[3];
+};
+
+struct LStatus {
+    unsigned flag;              // epoch*4 + {1 aggregate, 2 inclusive}
+    unsigned beta;
+    long long c;
+    LAgg agg;
+};
+
+__device__ __forceinline__ uint32_t lv_mulmod(uint32_t a, uint32_t b, uint32_t o) {
+    return (uint32_t)(((unsigned long long)a * b) % o);
+}
+__device__ __forceinline__ uint32_t lv_negmod(long long c, uint32_t o) {
+    long long r = c % (long long)o;          // in (-o, o)
+    if (r < 0) r += o;
+    return r ? o - (uint32_t)r : 0u;         // (-c) mod o
+}
+__device__ __forceinline__ int lv_piece(const LAgg& A, long long c) { return c < A.lo ? 0 : (c >= A.hi ? 2 : 1); }
+
+// A then B
+__device__ __forceinline__ LAgg lv_compose(const LAgg& A, const LAgg& B, uint32_t o) {
+    LAgg C;
+    C.lo = A.lo;
+    C.hi = A.hi;
+    C.m = (o > 1) ? lv_mulmod(A.m, B.m, o) : 0u;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        const long long c1 = A.cout[p];
+        const int q = lv_piece(B, c1);
+        C.cout[p] = B.cout[q];
+        if (o > 1) {
+            const unsigned long long x = (unsigned long long)A.g[p] * B.m + (unsigned long long)lv_negmod(c1, o) * B.m + B.g[q];
+            C.g[p] = (uint32_t)(x % o);
+        } else {
+            C.g[p] = 0;
+        }
+    }
+    return C;
+}
+
+__device__ __forceinline__ void lv_apply(const LAgg& A, long long& c, uint32_t& beta, uint32_t o) {
+    const int p = lv_piece(A, c);
+    if (o > 1) {
+        const unsigned long long x = (unsigned long long)beta * A.m + (unsigned long long)lv_negmod(c, o) * A.m + A.g[p];
+        beta = (uint32_t)(x % o);
+    }
+    c = A.cout[p];
+}
+
+__device__ __forceinline__ LAgg lv_shfl_up(const LAgg& a, int d) {
+    LAgg r;
+    r.lo = __shfl_up_sync(0xffffffffu, a.lo, d);
+    r.hi = __shfl_up_sync(0xffffffffu, a.hi, d);
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        r.cout[p] = __shfl_up_sync(0xffffffffu, a.cout[p], d);
+        r.g[p] = __shfl_up_sync(0xffffffffu, a.g[p], d);
+    }
+    r.m = __shfl_up_sync(0xffffffffu, a.m, d);
+    return r;
+}
+
+// limb i of slice S of term T for instance `inst` (i may be < 0 or >= len)
+__device__ __forceinline__ uint32_t lv_slice(const LTermDev& T, const uint32_t* src, int i, uint32_t fill) {
+    if (i < 0) return 0u;
+    if (i >= T.len) return fill;
+    return __ldg(src + (long long)i * T.limb_stride);
+}
+
+// accumulate sum_i m_i * limb_p(S_i << s_i) for positions p0 .. p0+N-1
+template <typename Acc, int N>
+__device__ __forceinline__ void lv_lincomb(const LOpDev& op, int nt, long long inst, int p0, Acc (&lin)[N]) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) lin[q] = 0;
+    for (int k = 0; k < nt; ++k) {
+        const LTermDev& T = op.t[k];
+        const uint32_t* src = T.base + inst * T.inst_stride;
+        uint32_t fill = 0;
+        if (T.sign && T.len > 0) fill = (__ldg(src + (long long)(T.len - 1) * T.limb_stride) >> 31) ? 0xFFFFFFFFu : 0u;
+        const int i0 = p0 - T.a;
+        uint32_t v[N + 1];
+#pragma unroll
+        for (int q = 0; q <= N; ++q) v[q] = lv_slice(T, src, i0 - 1 + q, fill);
+        const long long m = T.m;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            const uint32_t x = T.r ? __funnelshift_l(v[q], v[q + 1], T.r) : v[q + 1];
+            lin[q] += (Acc)m * (Acc)x;
+        }
+    }
+}
+
+template <bool WIDE>
+__global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ opp, LStatus* __restrict__ status,
+                                                   unsigned epoch, unsigned* __restrict__ tile_ctr) {
+    using Acc = typename std::conditional<WIDE, __int128, long long>::type;
+    const LOpDev& op = *opp;
+    __shared__ unsigned s_tile;
+    __shared__ LAgg s_wagg[LV_NT / 32];
+    __shared__ long long s_c;
+    __shared__ unsigned s_beta;
+    __shared__ uint32_t Q[LV_TL + LV_MAXHALO + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const long long inst = tile / op.tiles_per_inst;
+    const int k = (int)(tile - inst * op.tiles_per_inst);
+    const int tstart = k * LV_TL;
+    const int p0 = tstart + tid * LV_CH;
+    const uint32_t o = op.o;
+    const int nt = op.nt;
+
+    Acc lin[LV_CH];
+    lv_lincomb<Acc, LV_CH>(op, nt, inst, p0, lin);
+
+    // local normalisation (carry-in 0) -> thread aggregate
+    uint32_t x[LV_CH];
+    long long c = 0;
+#pragma unroll
+    for (int q = 0; q < LV_CH; ++q) {
+        const Acc v = lin[q] + (Acc)c;
+        x[q] = (uint32_t)v;
+        c = (long long)(v >> 32);
+    }
+    LAgg A;
+    {
+        const unsigned long long L64 = (unsigned long long)x[0] | ((unsigned long long)x[1] << 32);
+        bool tz = true, to = true;
+#pragma unroll
+        for (int q = 2; q < LV_CH; ++q) { tz &= (x[q] == 0u); to &= (x[q] == 0xFFFFFFFFu); }
+        A.lo = (tz && L64 <= 0x8000000000000000ull) ? (long long)(0ull - L64) : LLONG_MIN;
+        const unsigned long long comp = 0ull - L64;   // 2^64 - L64
+        A.hi = (to && L64 != 0 && comp <= (unsigned long long)LLONG_MAX) ? (long long)comp : LLONG_MAX;
+        A.cout[0] = c - 1;
+        A.cout[1] = c;
+        A.cout[2] = c + 1;
+        if (o > 1) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int q = LV_CH - 1; q >= 0; --q) r = (uint32_t)(((unsigned long long)r * op.p32 + x[q]) % o);
+            A.m = op.mi;
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+                // g[p] = (-Lmod + (p-1) M) * mi mod o
+                unsigned long long t = (unsigned long long)(o - r) + (p == 2 ? op.Mch : 0u) + (p == 0 ? (o - op.Mch) : 0u);
+                A.g[p] = lv_mulmod((uint32_t)(t % o), op.mi, o);
+            }
+        } else {
+            A.m = 0;
+            A.g[0] = A.g[1] = A.g[2] = 0;
+        }
+    }
+    // warp inclusive scan
+    LAgg inc = A;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const LAgg prev = lv_shfl_up(inc, d);
+        if (lane >= d) inc = lv_compose(prev, inc, o);
+    }
+    const LAgg excl = lv_shfl_up(inc, 1);   // valid for lane > 0
+    if (lane == 31) s_wagg[warp] = inc;
+    __syncthreads();
+    // tile aggregate, published before the look-back
+    const bool first = (k == 0);
+    LStatus* st = status + tile;
+    if (tid == 0) {
+        LAgg T = s_wagg[0];
+        for (int w = 1; w < LV_NT / 32; ++w) T = lv_compose(T, s_wagg[w], o);
+        long long cin = 0;
+        uint32_t bin = 0;
+        if (!first) {
+            st->agg = T;
+            __threadfence();
+            atomicExch(&st->flag, epoch * 4u + 1u);
+            // decoupled look-back over the tiles of this instance
+            bool have = false;
+            LAgg acc;
+            long long j = (long long)tile - 1;
+            for (;;) {
+                LStatus* ps = status + j;
+                unsigned f;
+                do { f = *(volatile unsigned*)&ps->flag; } while (f != epoch * 4u + 1u && f != epoch * 4u + 2u);
+                __threadfence();
+                if (f == epoch * 4u + 2u) {
+                    cin = *(volatile long long*)&ps->c;
+                    bin = *(volatile unsigned*)&ps->beta;
+                    if (have) lv_apply(acc, cin, bin, o);
+                    break;
+                }
+                LAgg a;
+                volatile LAgg* va = (volatile LAgg*)&ps->agg;
+                a.lo = va->lo; a.hi = va->hi;
+                a.cout[0] = va->cout[0]; a.cout[1] = va->cout[1]; a.cout[2] = va->cout[2];
+                a.m = va->m; a.g[0] = va->g[0]; a.g[1] = va->g[1]; a.g[2] = va->g[2];
+                acc = have ? lv_compose(a, acc, o) : a;
+                have = true;
+                --j;
+            }
+        }
+        // inclusive state of this tile
+        long long cout = cin;
+        uint32_t bout = bin;
+        lv_apply(T, cout, bout, o);
+        st->c = cout;
+        st->beta = bout;
+        __threadfence();
+        atomicExch(&st->flag, epoch * 4u + 2u);
+        s_c = cin;
+        s_beta = bin;
+    }
+    __syncthreads();
+    // this thread's carry-in / borrow-in
+    long long cin = s_c;
+    uint32_t bin = s_beta;
+    for (int w = 0; w < warp; ++w) lv_apply(s_wagg[w], cin, bin, o);
+    if (lane > 0) lv_apply(excl, cin, bin, o);
+    // exact limbs, exact division, quotients to smem
+    c = cin;
+    uint32_t beta = bin;
+#pragma unroll
+    for (int q = 0; q < LV_CH; ++q) {
+        const Acc v = lin[q] + (Acc)c;
+        uint32_t xq = (uint32_t)v;
+        c = (long long)(v >> 32);
+        if (o > 1) xq = tg_divexact_step(xq, beta, op.oinv, o);
+        Q[tid * LV_CH + q] = xq;
+    }
+    const int halo = op.sa + (op.sr ? 1 : 0);
+    if (tid == LV_NT - 1 && halo > 0) {
+        // quotient limbs just past the tile (the next tile's first limbs),
+        // continuing this tile's carry / borrow chain
+        Acc hl[LV_MAXHALO];
+        lv_lincomb<Acc, LV_MAXHALO>(op, nt, inst, tstart + LV_TL, hl);
+        for (int h = 0; h < halo; ++h) {
+            const Acc v = hl[h] + (Acc)c;
+            uint32_t xq = (uint32_t)v;
+            c = (long long)(v >> 32);
+            if (o > 1) xq = tg_divexact_step(xq, beta, op.oinv, o);
+            Q[LV_TL + h] = xq;
+        }
+    }
+    __syncthreads();
+    // right shift, coalesced stores
+    uint32_t* dst = op.dst + inst * op.dst_inst_stride;
+    for (int i = tid; i < LV_TL; i += LV_NT) {
+        const int t = tstart + i;
+        if (t >= op.W) break;
+        const uint32_t lo = Q[i + op.sa];
+        const uint32_t y = op.sr ? __funnelshift_r(lo, Q[i + op.sa + 1], op.sr) : lo;
+        dst[(long long)t * op.dst_limb_stride] = y;
+    }
+}
+
+// ------------------------------------------------------------------------
+// host side: op builder
+// ------------------------------------------------------------------------
+struct LVec {                  // a vector family: value of instance c, limb i at base[c*is + i*ls]
+    const uint32_t* base;
+    long long is, ls;
+    int len;                   // exact length (limbs beyond: fill)
+    int sign;
+};
+
+static uint32_t host_inv32(uint32_t o) {
+    uint32_t x = o;            // Newton: x = x (2 - o x), 5 steps from 3 bits
+    for (int i = 0; i < 5; ++i) x *= 2u - o * x;
+    return x;
+}
+static uint32_t host_powmod(unsigned long long b, unsigned long long e, uint32_t o) {
+    unsigned long long r = 1 % o;
+    b %= o;
+    while (e) {
+        if (e & 1) r = r * b % o;
+        b = b * b % o;
+        e >>= 1;
+    }
+    return (uint32_t)r;
+}
+static uint32_t host_invmod(uint32_t a, uint32_t o) {   // o odd, gcd(a, o) = 1
+    long long t = 0, nt = 1, r = o, nr = a % o;
+    while (nr) {
+        long long q = r / nr;
+        long long x = t - q * nt; t = nt; nt = x;
+        x = r - q * nr; r = nr; nr = x;
+    }
+    if (t < 0) t += o;
+    return (uint32_t)t;
+}
+
+struct LOpBuilder {
+    LOpDev op;
+    LOpBuilder(uint32_t* dst, long long is, long long ls, int W, int count, uint32_t o = 1, int shr = 0) {
+        memset(&op, 0, sizeof op);
+        op.dst = dst;
+        op.dst_inst_stride = is;
+        op.dst_limb_stride = ls;
+        op.W = W;
+        op.count = count;
+        op.o = o;
+        op.oinv = host_inv32(o);
+        if (o > 1) {
+            op.p32 = host_powmod(2, 32, o);
+            op.Mch = host_powmod(2, 32ull * LV_CH, o);
+            op.mi = host_invmod(op.Mch, o);
+        }
+        op.sa = shr / 32;
+        op.sr = shr % 32;
+        op.tiles_per_inst = (W + LV_TL - 1) / LV_TL;
+    }
+    // term m * (slice << s), slice = limbs [start, start+len) of v (len clipped to v.len)
+    bool add(const LVec& v, long long m, long long s, int start = 0, int len = -1, int sign = -1) {
+        if (op.nt >= LV_MAXT || m == 0) return m == 0;
+        LTermDev& T = op.t[op.nt++];
+        T.base = v.base + (long long)start * v.ls;
+        T.inst_stride = v.is;
+        T.limb_stride = v.ls;
+        const int avail = v.len - start;
+        T.len = len < 0 ? avail : (len < avail ? len : avail);
+        if (T.len < 0) T.len = 0;
+        // a slice that stops inside the exact value is zero-extended unless asked
+        T.sign = sign < 0 ? ((T.len == avail) ? v.sign : 0) : sign;
+        T.a = (int)(s / 32);
+        T.r = (int)(s % 32);
+        T.m = m;
+        return true;
+    }
+};
+
+}  // namespace tg

@@ -18,6 +18,9 @@
 #include <vector>
 #include <mutex>
 #include <string>
+#include <climits>
+#include <algorithm>
+#include <type_traits>
 
 #include "../../include/toomgpu.h"
 #include "generated/toom_programs.cuh"
@@ -43,6 +46,7 @@ static PSDesc ps_desc(int B) {
             for (int k = 0; k < 8; ++k) { s += p; p *= 64; }
             return {8, 15, s};
         }
+        case 16: return {16, 31, tg_growthS_T16};   // 31-point set (configs[4])
         default: return {0, 0, 0};
     }
 }
@@ -365,6 +369,7 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 }  // namespace tg
 #include "fused_bottom.cuh"
 #include "toplevel.cuh"
+#include "longvec.cuh"
 namespace tg {
 
 // ------------------------------------------------------------------------
@@ -378,6 +383,7 @@ struct Level {
     int e = 0;          // child operand width
     int Lw = 0;         // interpolation output width per coefficient
     int npts = 0;
+    bool lng = false;   // long-vector (limb-parallel) level
     size_t offU = 0, offV = 0, offP = 0, offW = 0;   // child operands/products, this level's scratch
 };
 
@@ -385,7 +391,38 @@ struct Plan {
     std::vector<Level> lv;   // lv[0..L-1] Toom levels, lv[L] = base level
     size_t bytes = 0;
     bool fused = false;      // bottom Toom level runs as k_fused_bottom
+    bool signed_in = false;  // user operands are two's complement (stage export)
+    // long-vector levels: slot pool, scan status, tile counters, op descriptors
+    size_t offSlots = 0, offStatus = 0, offCtr = 0, offDesc = 0;
+    size_t nStatus = 0, nCtr = 0, nDesc = 0;
 };
+
+// generated long-vector tables of a point set
+struct LongTables {
+    const tg_lterm* et; const tg_lop* eo; int neo;
+    const tg_lterm* it; const tg_lop* io; const int* iout; int nio; int nslots; int lag;
+};
+static bool long_tables(int B, LongTables& T) {
+#define TG_LT(NM)                                                                                      \
+    T = {tg_lt_##NM##_eval, tg_lo_##NM##_eval, tg_lnops_##NM##_eval, tg_lt_##NM##_interp,              \
+         tg_lo_##NM##_interp, tg_lout_##NM##_interp, tg_lnops_##NM##_interp, tg_lnslots_##NM##_interp,  \
+         tg_llag_##NM##_interp};                                                                       \
+    return true;
+    switch (B) {
+        case 3: TG_LT(T3)
+        case 4: TG_LT(T4)
+        case 8: TG_LT(P8)
+        case 16: TG_LT(T16)
+        default: return false;
+    }
+#undef TG_LT
+}
+static int long_Wt(const Level& L) {
+    LongTables T;
+    long_tables(L.B, T);
+    return L.Lw + T.lag;
+}
+static size_t long_tiles(size_t count, int W) { return count * (size_t)((W + LV_TL - 1) / LV_TL); }
 
 // base widths with a fused bottom-level instantiation (C1 33, C2 18, C3/C4/C5 23, ...)
 static bool fused_E_supported(int E) {
@@ -437,9 +474,21 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         width = L.e;
         if (depth > 40) return TOOM_EUNSUPPORTED;
     }
+    // long-vector levels: a prefix of the Toom levels with few instances
+    {
+        const size_t lc = p.long_count ? p.long_count : 4096;
+        LongTables T;
+        for (size_t l = 0; l + 1 < plan.lv.size(); ++l) {
+            Level& L = plan.lv[l];
+            if (L.count < lc && long_tables(L.B, T)) L.lng = true;
+            else break;
+        }
+        for (size_t l = 0; l + 1 < plan.lv.size(); ++l)
+            if (plan.lv[l].B == 16 && !plan.lv[l].lng) return TOOM_EUNSUPPORTED;   // T16 runs long only
+    }
     // fused bottom level?
     plan.fused = false;
-    if (plan.lv.size() >= 2 && !g_disable_fused) {
+    if (plan.lv.size() >= 2 && !g_disable_fused && !plan.lv[plan.lv.size() - 2].lng) {
         const Level& Bt = plan.lv[plan.lv.size() - 2];
         if ((Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
             2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e)
@@ -455,7 +504,27 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         L.offU = take((size_t)L.e * cc);
         L.offV = take((size_t)L.e * cc);
         L.offP = take((size_t)2 * L.e * cc);
-        L.offW = take((size_t)L.npts * L.Lw * L.count);
+        L.offW = L.lng ? 0 : take((size_t)L.npts * L.Lw * L.count);
+    }
+    size_t slot_limbs = 0, tiles = 0, nops = 0;
+    for (size_t l = 0; l < nstaged; ++l) {
+        const Level& L = plan.lv[l];
+        if (!L.lng) continue;
+        LongTables T;
+        long_tables(L.B, T);
+        const int Wt = long_Wt(L);
+        slot_limbs = std::max(slot_limbs, (size_t)T.nslots * L.count * Wt);
+        tiles = std::max(tiles, long_tiles(L.count, std::max(std::max(Wt, L.e), 2 * L.n)));
+        nops += 2 * (size_t)T.neo + T.nio + 1;
+    }
+    if (nops) {
+        plan.offSlots = take(slot_limbs);
+        plan.nStatus = tiles;
+        plan.offStatus = take((tiles * sizeof(LStatus) + 3) / 4);
+        plan.nCtr = nops;
+        plan.offCtr = take(nops);
+        plan.nDesc = nops;
+        plan.offDesc = take((nops * sizeof(LOpDev) + 3) / 4);
     }
     plan.bytes = off;
     return TOOM_OK;
@@ -657,12 +726,15 @@ static toom_status launch_interp_top_rows(const Level& Lv, const uint32_t* P1, u
 // base level reached directly (no Toom level): schoolbook on row-major
 // operands via a transposing copy
 // row-major [count][n] -> interleaved [E][count], zero rows for n <= i < E
-__global__ void k_transpose_in(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t count, int n, int E) {
+__global__ void k_transpose_in(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t count, int n, int E,
+                               int sgn) {
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= count * (size_t)E) return;
     const size_t c = gid / E;
     const int i = (int)(gid % E);
-    dst[(size_t)i * count + c] = i < n ? src[c * (size_t)n + i] : 0u;
+    uint32_t fill = 0;
+    if (sgn && i >= n) fill = (src[c * (size_t)n + n - 1] >> 31) ? 0xFFFFFFFFu : 0u;
+    dst[(size_t)i * count + c] = i < n ? src[c * (size_t)n + i] : fill;
 }
 __global__ void k_transpose_out(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t count, int n2) {
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -672,10 +744,170 @@ __global__ void k_transpose_out(const uint32_t* __restrict__ src, uint32_t* __re
     dst[gid] = src[(size_t)i * count + c];
 }
 
+// ------------------------------------------------------------------------
+// long-vector levels: op descriptors for one call (down: evaluation of both
+// operands at every point; up: the interpolation program, then the
+// recomposition op), built on the host and uploaded once per call
+// ------------------------------------------------------------------------
+struct LongCall {
+    std::vector<LOpDev> down, up;
+};
+
+// layout of level l's child operand / product families
+static LVec child_vec(const Plan& plan, size_t l, const uint8_t* ws, size_t off, int width, int k) {
+    const Level& L = plan.lv[l];
+    const bool next_long = (l + 1 < plan.lv.size() - 1) && plan.lv[l + 1].lng &&
+                           !(plan.fused && l + 1 == plan.lv.size() - 2);
+    const uint32_t* base = (const uint32_t*)(ws + off);
+    if (next_long)   // row-major [npts*count][width], child k*count + c
+        return LVec{base + (size_t)k * L.count * width, width, 1, width, 1};
+    // interleaved [width][npts*count]
+    return LVec{base + (size_t)k * L.count, 1, (long long)L.npts * (long long)L.count, width, 1};
+}
+
+// evaluation ops of one long level: U(x_k) for every point k of one operand
+// family `par` (Eq. 1.1 split as slices, homogeneous point values)
+template <class ChildF>
+static void long_eval_ops(const Level& L, const LVec& par, ChildF child, std::vector<LOpDev>& out) {
+    LongTables T;
+    long_tables(L.B, T);
+    for (int k = 0; k < T.neo; ++k) {
+        const tg_lop& o = T.eo[k];
+        LVec dv = child(o.dst);
+        LOpBuilder b((uint32_t*)dv.base, dv.is, dv.ls, L.e, (int)L.count);
+        for (int t = 0; t < o.nt; ++t) {
+            const tg_lterm& tm = T.et[o.t0 + t];
+            const int j = -tm.src - 1;
+            const int len = (j == L.B - 1) ? L.lentop : L.b;
+            b.add(par, tm.m, tm.s, j * L.b, len, (j == L.B - 1) ? -1 : 0);
+        }
+        b.op.wide = o.wide;
+        out.push_back(b.op);
+    }
+}
+
+// interpolation program (steps a4) over the slot pool, then the
+// recomposition w = sum_j w_j 2^(32 b j) (Eq. 1.3, step a5) into dst
+// (row-major [count][2n], two's complement)
+template <class YF>
+static void long_interp_ops(const Level& L, YF yv, uint32_t* slots, uint32_t* dst, std::vector<LOpDev>& out) {
+    LongTables T;
+    long_tables(L.B, T);
+    const int cnt = (int)L.count;
+    const int Wt = long_Wt(L);
+    auto slot_vec = [&](int sl) { return LVec{slots + (size_t)sl * cnt * Wt, Wt, 1, Wt, 0}; };
+    for (int i = 0; i < T.nio; ++i) {
+        const tg_lop& o = T.io[i];
+        LVec dv = slot_vec(o.dst);
+        LOpBuilder b((uint32_t*)dv.base, dv.is, dv.ls, Wt, cnt, o.odiv, o.shr);
+        for (int t = 0; t < o.nt; ++t) {
+            const tg_lterm& tm = T.it[o.t0 + t];
+            b.add(tm.src < 0 ? yv(-tm.src - 1) : slot_vec(tm.src), tm.m, tm.s);
+        }
+        b.op.wide = o.wide;
+        out.push_back(b.op);
+    }
+    LOpBuilder b(dst, 2 * L.n, 1, 2 * L.n, cnt);
+    for (int j = 0; j < L.npts; ++j) {
+        const int src = T.iout[j];
+        if (src < 0) b.add(yv(-src - 1), 1, 32ll * L.b * j);
+        else b.add(slot_vec(src), 1, 32ll * L.b * j, 0, L.Lw, 1);
+    }
+    b.op.wide = 0;
+    out.push_back(b.op);
+}
+
+static void build_long_level(const Plan& plan, size_t l, uint32_t* w, const uint32_t* u, const uint32_t* v, uint8_t* ws,
+                             LongCall& lc) {
+    const Level& L = plan.lv[l];
+    for (int opd = 0; opd < 2; ++opd) {
+        LVec par;
+        if (l == 0) par = LVec{opd ? v : u, L.n, 1, L.n, plan.signed_in ? 1 : 0};   // user operands, row-major
+        else par = LVec{(const uint32_t*)(ws + (opd ? plan.lv[l - 1].offV : plan.lv[l - 1].offU)), L.n, 1, L.n, 1};
+        const size_t off = opd ? L.offV : L.offU;
+        long_eval_ops(L, par, [&](int k) { return child_vec(plan, l, ws, off, L.e, k); }, lc.down);
+    }
+    uint32_t* dst = (l == 0) ? w : (uint32_t*)(ws + plan.lv[l - 1].offP);
+    long_interp_ops(L, [&](int k) { return child_vec(plan, l, ws, L.offP, 2 * L.e, k); }, (uint32_t*)(ws + plan.offSlots),
+                    dst, lc.up);
+}
+
+static std::mutex g_desc_mu;
+static LOpDev* g_desc_host = nullptr;   // pinned staging for the descriptor upload
+static size_t g_desc_cap = 0;
+static cudaEvent_t g_desc_ev = nullptr;
+
+// upload the call's op descriptors (pinned staging, one copy) and reset the
+// scan status / tile counters, all stream-ordered
+static toom_status long_prepare(const std::vector<LOpDev>& a, const std::vector<LOpDev>& b, LOpDev* ddesc,
+                                LStatus* status, size_t nStatus, unsigned* ctr, size_t nCtr, cudaStream_t st) {
+    const size_t nd = a.size() + b.size();
+    std::lock_guard<std::mutex> g(g_desc_mu);
+    if (g_desc_ev) cudaEventSynchronize(g_desc_ev);   // previous upload finished reading the staging
+    if (nd > g_desc_cap) {
+        if (g_desc_host) cudaFreeHost(g_desc_host);
+        if (cudaMallocHost((void**)&g_desc_host, nd * sizeof(LOpDev)) != cudaSuccess) {
+            cudaGetLastError();
+            g_desc_host = nullptr;
+            g_desc_cap = 0;
+            return TOOM_ENOMEM;
+        }
+        g_desc_cap = nd;
+    }
+    if (!a.empty()) memcpy(g_desc_host, a.data(), a.size() * sizeof(LOpDev));
+    if (!b.empty()) memcpy(g_desc_host + a.size(), b.data(), b.size() * sizeof(LOpDev));
+    if (cudaMemcpyAsync(ddesc, g_desc_host, nd * sizeof(LOpDev), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return TOOM_ECUDA;
+    if (!g_desc_ev) cudaEventCreateWithFlags(&g_desc_ev, cudaEventDisableTiming);
+    cudaEventRecord(g_desc_ev, st);
+    cudaMemsetAsync(status, 0, nStatus * sizeof(LStatus), st);
+    cudaMemsetAsync(ctr, 0, nCtr * sizeof(unsigned), st);
+    return TOOM_OK;
+}
+
+static toom_status launch_long_ops(const std::vector<LOpDev>& ops, size_t first, const LOpDev* ddesc, LStatus* status,
+                                   unsigned* ctr, unsigned& epoch, int cat, cudaStream_t st) {
+    for (size_t i = 0; i < ops.size(); ++i) {
+        const LOpDev& o = ops[i];
+        const unsigned grid = (unsigned)((size_t)o.count * o.tiles_per_inst);
+        if (grid == 0) continue;
+        ProfScope ps(cat, st);
+        if (o.wide) k_long_op<true><<<grid, LV_NT, 0, st>>>(ddesc + first + i, status, epoch, ctr + first + i);
+        else k_long_op<false><<<grid, LV_NT, 0, st>>>(ddesc + first + i, status, epoch, ctr + first + i);
+        ps.done(st);
+        ++epoch;
+        ++t_launches;
+    }
+    return TOOM_OK;
+}
+
 static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, const uint32_t* v, int n, size_t batch,
                             uint8_t* ws, cudaStream_t st) {
     const size_t L = plan.lv.size() - 1;   // number of Toom levels
     toom_status s;
+    // long-vector prefix of the recursion
+    size_t Tl = 0;
+    while (Tl < L && plan.lv[Tl].lng) ++Tl;
+    LongCall lc;
+    std::vector<size_t> up_first(Tl + 1, 0);
+    LOpDev* ddesc = (LOpDev*)(ws + plan.offDesc);
+    LStatus* status = (LStatus*)(ws + plan.offStatus);
+    unsigned* ctr = (unsigned*)(ws + plan.offCtr);
+    unsigned epoch = 1;
+    if (Tl) {
+        std::vector<std::vector<LOpDev>> ups(Tl);
+        for (size_t l = 0; l < Tl; ++l) {
+            LongCall one;
+            build_long_level(plan, l, w, u, v, ws, one);
+            lc.down.insert(lc.down.end(), one.down.begin(), one.down.end());
+            ups[l] = one.up;
+        }
+        // up order: deepest long level first
+        for (size_t l = Tl; l-- > 0;) lc.up.insert(lc.up.end(), ups[l].begin(), ups[l].end());
+        if (lc.down.size() + lc.up.size() > plan.nDesc) return TOOM_EINVAL;
+        if ((s = long_prepare(lc.down, lc.up, ddesc, status, plan.nStatus, ctr, plan.nCtr, st))) return s;
+        if ((s = launch_long_ops(lc.down, 0, ddesc, status, ctr, epoch, CAT_EVAL, st))) return s;
+    }
     if (L == 0) {
         // schoolbook only (n <= 64): the base kernel multiplies signed
         // operands, so the unsigned inputs get one zero limb on top
@@ -683,8 +915,8 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         uint32_t* tu = (uint32_t*)ws;
         uint32_t* tv = tu + ((batch * E + 63) & ~(size_t)63);
         uint32_t* tp = tv + ((batch * E + 63) & ~(size_t)63);
-        k_transpose_in<<<nblk(batch * E, 256), 256, 0, st>>>(u, tu, batch, n, E);
-        k_transpose_in<<<nblk(batch * E, 256), 256, 0, st>>>(v, tv, batch, n, E);
+        k_transpose_in<<<nblk(batch * E, 256), 256, 0, st>>>(u, tu, batch, n, E, plan.signed_in);
+        k_transpose_in<<<nblk(batch * E, 256), 256, 0, st>>>(v, tv, batch, n, E, plan.signed_in);
         if ((s = launch_base(E, tu, tv, tp, batch, st))) return s;
         k_transpose_out<<<nblk(batch * 2 * n, 256), 256, 0, st>>>(tp, w, batch, 2 * n);
         t_launches += 3;
@@ -692,7 +924,7 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
     }
     const size_t Lt = plan.fused ? L - 1 : L;   // levels run as staged eval/interp launches
     // down: evaluation
-    for (size_t l = 0; l < Lt; ++l) {
+    for (size_t l = Tl; l < Lt; ++l) {
         const Level& Lv = plan.lv[l];
         const uint32_t* su = l == 0 ? u : (const uint32_t*)(ws + plan.lv[l - 1].offU);
         const uint32_t* sv = l == 0 ? v : (const uint32_t*)(ws + plan.lv[l - 1].offV);
@@ -720,7 +952,7 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             return s;
     }
     // up: interpolation + recomposition
-    for (size_t l = Lt; l-- > 0;) {
+    for (size_t l = Lt; l-- > Tl;) {
         const Level& Lv = plan.lv[l];
         uint32_t* out = l == 0 ? w : (uint32_t*)(ws + plan.lv[l - 1].offP);
         if (l == 0 && top_rows_ok(Lv)) {
@@ -730,6 +962,9 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         if ((s = launch_interp(Lv.B, l == 0, (const uint32_t*)(ws + Lv.offP), (uint32_t*)(ws + Lv.offW), out, Lv.count,
                                2 * Lv.e, Lv.Lw, Lv.b, 2 * Lv.n, st)))
             return s;
+    }
+    if (Tl) {
+        if ((s = launch_long_ops(lc.up, lc.down.size(), ddesc, status, ctr, epoch, CAT_INTERP, st))) return s;
     }
     return TOOM_OK;
 }
@@ -747,7 +982,7 @@ static toom_status check_device() {
 }
 
 static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
-                           const toom_plan_t& p, cudaStream_t st) {
+                           const toom_plan_t& p, cudaStream_t st, bool sgn = false) {
     t_launches = 0;
     if (n == 0 || n > (1u << 30)) return TOOM_EINVAL;
     if (batch == 0) return TOOM_OK;
@@ -760,6 +995,8 @@ static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, si
     if (chunk > batch) chunk = batch;
     Plan plan;
     if ((s = make_plan((int)n, chunk, p, plan))) return s;
+    plan.signed_in = sgn;
+    if (sgn && plan.lv.size() > 1 && !plan.lv[0].lng) return TOOM_EUNSUPPORTED;   // signed top level: long path only
     size_t need = plan.bytes;
     if (plan.lv.size() == 1) need = (2 * ((chunk * (n + 1) + 63) & ~(size_t)63) + 2 * chunk * (n + 1)) * 4;
     void* ws = nullptr;
@@ -769,6 +1006,8 @@ static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, si
         if (cnt != chunk) {
             Plan p2;
             if ((s = make_plan((int)n, cnt, p, p2))) return s;
+            p2.signed_in = sgn;
+            if (sgn && p2.lv.size() > 1 && !p2.lv[0].lng) return TOOM_EUNSUPPORTED;
             if ((s = run_plan(p2, w + c0 * 2 * n, u + c0 * n, v + c0 * n, (int)n, cnt, (uint8_t*)ws, st))) return s;
         } else {
             if ((s = run_plan(plan, w + c0 * 2 * n, u + c0 * n, v + c0 * n, (int)n, cnt, (uint8_t*)ws, st))) return s;
@@ -796,6 +1035,7 @@ toom_plan_t toom_default_plan(int B) {
     p.t4 = 256;
     p.t3 = 64;
     p.chunk = 0;
+    p.long_count = 0;
     return p;
 }
 
@@ -807,7 +1047,7 @@ toom_status toom_mul_batched_plan(uint32_t* w, const uint32_t* u, const uint32_t
 
 toom_status toom_mul_batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch, int B,
                              void* stream) {
-    if (B != 3 && B != 4 && B != 8) return fail(TOOM_EINVAL);
+    if (B != 3 && B != 4 && B != 8 && B != 16) return fail(TOOM_EINVAL);
     toom_plan_t p = toom_default_plan(B);
     return fail(batched(w, u, v, n, batch, p, (cudaStream_t)stream));
 }
@@ -816,7 +1056,7 @@ toom_status toom_mul(uint32_t* w, const uint32_t* u, size_t nu, const uint32_t* 
     cudaStream_t st = (cudaStream_t)stream;
     t_launches = 0;
     if (!w || (nu && !u) || (nv && !v)) return fail(TOOM_EINVAL);
-    if (B != 3 && B != 4 && B != 8) return fail(TOOM_EINVAL);
+    if (B != 3 && B != 4 && B != 8 && B != 16) return fail(TOOM_EINVAL);
     if ((nu && overlaps(w, (nu + nv) * 4, u, nu * 4)) || (nv && overlaps(w, (nu + nv) * 4, v, nv * 4)))
         return fail(TOOM_EINVAL);
     toom_status s = check_device();
@@ -962,8 +1202,8 @@ size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t* plan, char*
         const Level& L = pl.lv[l];
         char tmp[512];
         snprintf(tmp, sizeof tmp,
-                 "%s{\"B\": %d, \"count\": %zu, \"n\": %d, \"b\": %d, \"lentop\": %d, \"e\": %d, \"Lw\": %d, \"npts\": %d}",
-                 l ? ", " : "", L.B, L.count, L.n, L.b, L.lentop, L.e, L.Lw, L.npts);
+                 "%s{\"B\": %d, \"count\": %zu, \"n\": %d, \"b\": %d, \"lentop\": %d, \"e\": %d, \"Lw\": %d, \"npts\": %d, \"long\": %s}",
+                 l ? ", " : "", L.B, L.count, L.n, L.b, L.lentop, L.e, L.Lw, L.npts, L.lng ? "true" : "false");
         js += tmp;
     }
     char tail[128];

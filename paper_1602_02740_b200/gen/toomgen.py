@@ -954,6 +954,179 @@ TG_HD TG_INLINE uint32_t tg_shl_limb(uint32_t lo, uint32_t hi, int r) {
 """
 
 
+# ------------------------------------------------- long-vector op tables
+#
+# The long-vector executor (csrc/longvec.cuh) runs a program as a sequence of
+# limb-parallel launches, one per op  dst = ((sum_i m_i * (src_i << s_i)) / o) >> shr,
+# each op computed modulo 2^(32 W) over whole vectors (W = slot width).  The
+# tables below give, per point set: the evaluation ops (one per point,
+# U(p:q) = sum_k p^k q^(n-k) u_k; PAPER.md:16-24 with homogeneous points) and
+# the interpolation ops (temps assigned to a minimal set of vector slots by
+# liveness), with the per-op look-ahead ("lag") the right shifts need.
+
+LONG_DIGIT = 40          # big multipliers are split into signed 40-bit digits
+
+
+def _split_mult(m, s):
+    """m * 2^s as a list of (digit, shift) with |digit| < 2^(LONG_DIGIT-1)+1."""
+    if abs(m) < (1 << 62) // 64:
+        return [(m, s)]
+    out = []
+    sh = s
+    while m != 0:
+        d = m & ((1 << LONG_DIGIT) - 1)
+        if d >= 1 << (LONG_DIGIT - 1):
+            d -= 1 << LONG_DIGIT
+        out.append((d, sh))
+        m = (m - d) >> LONG_DIGIT
+        sh += LONG_DIGIT
+    return [(d, x) for d, x in out if d != 0]
+
+
+def long_program(prog: Program, outputs_are_slots=True):
+    """Assign slots; returns dict(ops=[(dst, [(src, m, s)], odiv, shr)], outputs, nslots, lag).
+    src >= 0: slot, src < 0: input -(k+1).  dst >= 0 slot."""
+    inputs = {v: -(k + 1) for k, v in enumerate(prog.inputs)}
+    ops = _live_ops(prog, prog.outputs)
+    last = {}
+    for i, op in enumerate(ops):
+        for t in op.terms:
+            last[t.var] = i
+    for v in prog.outputs:
+        last[v] = len(ops)
+    where = dict(inputs)
+    free, nslots = [], 0
+    out_ops = []
+    for i, op in enumerate(ops):
+        if free:
+            free.sort()
+            d = free.pop(0)
+        else:
+            d = nslots
+            nslots += 1
+        terms = []
+        for t in op.terms:
+            if t.var == "ZERO":
+                continue
+            for m, s in _split_mult(t.m, t.s):
+                terms.append((where[t.var], m, s))
+        out_ops.append((d, terms, op.odiv, op.shr))
+        where[op.dst] = d
+        for t in op.terms:
+            if t.var != "ZERO" and last.get(t.var) == i and where[t.var] >= 0 and t.var not in prog.outputs:
+                if where[t.var] not in free:
+                    free.append(where[t.var])
+    # deficits (limbs of look-ahead consumed below the slot width)
+    deficit = {}
+    slot_def = {}
+    for d, terms, o, shr in out_ops:
+        a, r = divmod(shr, 32)
+        lag = a + (1 if r else 0)
+        dd = 0
+        for src, m, s in terms:
+            if src >= 0:
+                dd = max(dd, slot_def[src] - s // 32)
+        slot_def[d] = max(0, dd) + lag
+    lag = max([slot_def[where[v]] for v in prog.outputs if where[v] >= 0] + [0])
+    outs = [where[v] for v in prog.outputs]
+    # sanity: exact execution on random ints through the slot machine
+    return dict(ops=out_ops, outputs=outs, nslots=nslots, lag=lag)
+
+
+def run_long(lp, inputs):
+    slots = {}
+    def val(src):
+        return inputs[-src - 1] if src < 0 else slots[src]
+    assert all(d >= 0 for d, _, _, _ in lp["ops"])
+    for d, terms, o, shr in lp["ops"]:
+        x = sum(m * (val(src) << s) for src, m, s in terms)
+        assert x % (o << shr) == 0
+        slots[d] = x // (o << shr)
+    return [val(s) for s in lp["outputs"]]
+
+
+def long_eval_program(ps: PointSet):
+    """One op per point (direct homogeneous evaluation)."""
+    n = ps.n
+    ops = []
+    for k, (p, q) in enumerate(ps.points):
+        terms = []
+        for j in range(ps.B):
+            c = p**j * q ** (n - j)
+            if c:
+                sh = (abs(c) & -abs(c)).bit_length() - 1     # powers of two become shifts
+                terms += [(-(j + 1), m, s) for m, s in _split_mult(c >> sh, sh)]
+        ops.append((k, terms, 1, 0))
+    return dict(ops=ops, outputs=list(range(len(ps.points))), nslots=len(ps.points), lag=0)
+
+
+def long_interp_program(ps: PointSet):
+    if ps.B <= 4:
+        # PAPER.md:162 matrix form: one op per coefficient, composed from the
+        # even-odd + listing program (per_output_programs)
+        it = build_interp(ps)
+        progs = per_output_programs(it, f"li_{ps.name}")
+        ops, outs, ns = [], [], 0
+        for j, p in enumerate(progs):
+            if not p.ops:
+                outs.append(-(it.inputs.index(p.outputs[0]) + 1))
+                continue
+            op = p.ops[0]
+            ops.append((ns, [(-(it.inputs.index(t.var) + 1), t.m, t.s) for t in op.terms], op.odiv, op.shr))
+            outs.append(ns)
+            ns += 1
+        lag = max([((op[3] // 32) + (1 if op[3] % 32 else 0)) for op in ops] + [0])
+        return dict(ops=ops, outputs=outs, nslots=ns, lag=lag)
+    return long_program(fuse_single_use(build_interp(ps)))
+
+
+def _growth_S(ps: PointSet):
+    return max(sum(abs(p**k * q ** (ps.n - k)) for k in range(ps.B)) for p, q in ps.points)
+
+
+def emit_long_tables(ps: PointSet) -> str:
+    rng = random.Random(7)
+    ev = long_eval_program(ps)
+    it = long_interp_program(ps)
+    # round trip on exact integers through the slot machines
+    for _ in range(3):
+        U = [rng.randrange(-(1 << 200), 1 << 200) for _ in range(ps.B)]
+        V = [rng.randrange(-(1 << 200), 1 << 200) for _ in range(ps.B)]
+        EU, EV = run_long(ev, U), run_long(ev, V)
+        W = run_long(it, [a * b for a, b in zip(EU, EV)])
+        conv = [sum(U[i] * V[k - i] for i in range(ps.B) if 0 <= k - i < ps.B) for k in range(2 * ps.B - 1)]
+        assert W == conv, ps.name
+    lines = [f"// long-vector tables for {ps.name} (csrc/longvec.cuh)"]
+    nm = ps.name
+    lines.append(f"constexpr unsigned long long tg_growthS_{nm} = {_growth_S(ps)}ull;")
+    for tag, lp in (("eval", ev), ("interp", it)):
+        terms, ops = [], []
+        for d, ts, o, shr in lp["ops"]:
+            t0 = len(terms)
+            for src, m, s in ts:
+                terms.append(f"{{{src}, {s}, {m}ll}}")
+            sm = sum(abs(m) for _, m, _ in ts)
+            wide = 1 if sm >= (1 << 30) else 0
+            assert sm < (1 << 61), (nm, tag, sm)
+            inv = pow(o, -1, 1 << 32) if o > 1 else 1
+            ops.append(f"{{{d}, {t0}, {len(ts)}, {o}u, 0x{inv:08X}u, {shr}, {wide}}}")
+        lines.append(f"static const tg_lterm tg_lt_{nm}_{tag}[] = {{" + ", ".join(terms) + "};")
+        lines.append(f"static const tg_lop tg_lo_{nm}_{tag}[] = {{" + ", ".join(ops) + "};")
+        lines.append(f"static const int tg_lout_{nm}_{tag}[] = {{" + ", ".join(str(x) for x in lp["outputs"]) + "};")
+        lines.append(f"constexpr int tg_lnops_{nm}_{tag} = {len(ops)};")
+        lines.append(f"constexpr int tg_lnslots_{nm}_{tag} = {lp['nslots']};")
+        lines.append(f"constexpr int tg_llag_{nm}_{tag} = {lp['lag']};")
+    return "\n".join(lines)
+
+
+LONG_HEADER = """
+// one term m * (src << s) of a long-vector op; src >= 0 slot, src < 0 input -(k+1)
+struct tg_lterm { int src; int s; long long m; };
+// dst = ((sum of terms) / odiv) >> shr   (odiv odd, oinv = odiv^-1 mod 2^32)
+struct tg_lop { int dst; int t0; int nt; unsigned odiv; unsigned oinv; int shr; int wide; };
+"""
+
+
 def generate_all():
     # T16 (31 points, C5's top level) runs through the long-vector path, not
     # the streaming emitter (its multipliers exceed one word).
@@ -984,6 +1157,9 @@ def generate_all():
             parts.append(emit_rowstep_functions(ps))
             parts.append("#endif")
         meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
+    parts.append(LONG_HEADER)
+    for ps in [pointset_T3(), pointset_T4(), pointset_paper(8), pointset_T16_31()]:
+        parts.append(emit_long_tables(ps))
     return "\n\n".join(parts) + "\n", meta
 
 

@@ -268,3 +268,76 @@ def test_fused_bottom_equals_staged_and_oracle(B, n, t4, t3):
 def test_c2_plan_uses_fused_bottom():
     info = tg.plan_describe(256, 65536, B=4, t4=32, t3=32)
     assert info["fused_bottom"] and info["levels"][-1]["n"] == 18
+
+
+# ------------------------------------------------------------ long-vector levels (C4/C5 upper levels)
+
+
+@pytest.mark.parametrize("B", [3, 4, 8, 16])
+@pytest.mark.parametrize("n", [40, 257, 1500, 5000, 20011])
+def test_long_path_single_product(B, n):
+    """toom_mul on one product: the upper levels run on the limb-parallel
+    long-vector kernels (several tiles per vector at n >= 2048, ragged tail)."""
+    if n < 2 * B:
+        pytest.skip("below the smallest split")
+    rng = np.random.default_rng(n + B)
+    a = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    info = tg.plan_describe(n, 1, B=B)
+    assert info["levels"][0]["long"] or info["levels"][0]["B"] != B
+    w = host(tg.toom_mul(dev(a), dev(b), B=B))
+    assert np.array_equal(w, oracle.schoolbook(a, b)), info
+
+
+@pytest.mark.parametrize("B", [3, 4, 8, 16])
+def test_long_path_adversarial_carries(B):
+    """all-ones, alternating, single-bit and zero-top operands: long carry and
+    borrow chains across tiles (every limb 0xFFFFFFFF propagates)."""
+    n = 9000
+    ones = np.full(n, 0xFFFFFFFF, np.uint32)
+    alt = np.zeros(n, np.uint32)
+    alt[1::2] = 0xFFFFFFFF
+    bit = np.zeros(n, np.uint32)
+    bit[n // 3] = 1 << 7
+    low = np.zeros(n, np.uint32)
+    low[: n // 2] = 0xFFFFFFFF
+    cases = [(ones, ones), (alt, alt), (bit, ones), (low, ones), (ones, low)]
+    for a, b in cases:
+        w = host(tg.toom_mul(dev(a), dev(b), B=B))
+        assert I(w) == I(a) * I(b)
+
+
+@pytest.mark.parametrize("B,n", [(3, 300), (4, 1000), (8, 2048), (4, 4100)])
+def test_long_vs_short_levels_batched(B, n):
+    """The same batch with the upper levels forced long (long_count large) and
+    forced instance-parallel (long_count=1): identical to the oracle."""
+    rng = np.random.default_rng(n * 3 + B)
+    batch = 9
+    u = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    v = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    u[0] = 0xFFFFFFFF
+    v[0] = 0xFFFFFFFF
+    want = oracle.schoolbook_batched(u, v)
+    for lc in (1, 1 << 30):
+        w = host(tg.toom_mul_batched(dev(u), dev(v), B=B, long_count=lc))
+        assert np.array_equal(w, want), lc
+
+
+def test_c5_shape_reduced():
+    """C5's top level (31-point Toom-16, homogeneous points) at 2^16 limbs,
+    recursing with Toom-4/3: bit-exact against the oracle's own recursive Toom
+    (paper points) and residues."""
+    seed = synth.seed_for(5)
+    n = 1 << 16
+    u = synth.uniform_limbs(seed, 7, 1, 0, n)[0]
+    v = synth.uniform_limbs(seed, 7, 1, 1, n)[0]
+    w = host(tg.toom_mul(dev(u), dev(v), B=16))
+    check_residues(u, v, w)
+    assert np.array_equal(w, oracle.toom(u, v, top_B=16))
+
+
+@pytest.mark.slow
+def test_c5_full():
+    u, v = synth.config_inputs(5)
+    w = host(tg.toom_mul(dev(u), dev(v), B=16))
+    check_residues(u, v, w)
