@@ -159,6 +159,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -224,8 +225,8 @@ def main():
     ms_per_step = ms / args.steps
     value = world * batch / (ms_per_step * 1e-3)
 
-    # per-kernel-category durations (separate instrumented pass, CUDA events
-    # on the launching stream) for the roofline of the dominant kernel
+    # per-kernel durations (separate instrumented pass, CUDA events recorded on
+    # the launching stream around every launch) for the roofline of each kernel
     tg.profile_enable(True)
     for _ in range(args.steps):
         step()
@@ -233,48 +234,52 @@ def main():
     tg.profile_enable(False)
     plan = tg.plan_describe(n, batch, B=B, t4=C2["t4"], t3=C2["t3"])
     lv = plan["levels"]
-    base = lv[-1]
-    E = base["n"]
-    lp_per_launch = base["count"] * E * E                     # algorithmic limb-products of the base case
-    base_ms = prof["base"]["ms"] / max(1, prof["base"]["launches"])
-    lp_rate, _ = tg.probe_limb_products()
-    achieved = lp_per_launch / (base_ms * 1e-3)
-
-    # algorithmic bytes of the streaming stages (each value read once, written once)
-    def stage_bytes():
-        evb = 0
-        itb = 0
-        for i, L in enumerate(lv[:-1]):
-            cc = L["count"] * L["npts"]
-            evb += 2 * (L["count"] * L["n"] + cc * L["e"]) * 4
-            itb += (cc * 2 * L["e"] + L["count"] * 2 * L["n"]) * 4
-        return evb, itb
-    ev_bytes, it_bytes = stage_bytes()
-    ev_ms = prof["eval"]["ms"] / args.steps
-    it_ms = prof["interp"]["ms"] / args.steps
     pk, pk_kind = peaks()
-    shares = {k: prof[k]["ms"] / args.steps for k in ("eval", "base", "interp")}
+    hbm_peak = pk.get("hbm_gbs")
+    lp_rate, _ = tg.probe_limb_products()
+    L0, L1 = lv[0], lv[1]
+    E = lv[-1]["n"]
+    # per-launch algorithmic work of the three kernels of a C2 step:
+    #   eval   (k_eval_top_rows<4>)   : read u, v; write the 7 evaluated pairs
+    #   fused  (k_fused_bottom<4,18>) : 7 * E^2 limb-products per level-1 parent
+    #   interp (k_interp_top_stream<4>): read the 7 products; write w
+    kern = {
+        "eval": dict(name="k_eval_top_rows<4>", bound="hbm",
+                     units=2 * (L0["count"] * L0["n"] + L0["count"] * L0["npts"] * L0["e"]) * 4),
+        "base": dict(name="k_fused_bottom<4,18>", bound="alu", units=L1["count"] * L1["npts"] * E * E,
+                     bytes=(2 * L1["count"] * L1["n"] + L1["count"] * 2 * L1["n"]) * 4),
+        "interp": dict(name="k_interp_top_stream<4>", bound="hbm",
+                       units=(L0["count"] * L0["npts"] * 2 * L0["e"] + L0["count"] * 2 * L0["n"]) * 4),
+    }
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f)
+    except OSError:
+        pass
+    shares = {k: prof[k]["ms"] / max(1, prof[k]["launches"]) for k in kern}
+    kernels = {}
+    for k, d in kern.items():
+        ms_l = shares[k]
+        if d["bound"] == "hbm":
+            ach = d["units"] / (ms_l * 1e-3) / 1e9
+            kernels[k] = {"kernel": d["name"], "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": ach / hbm_peak, "traffic": traffic.get(d["name"]), "ms_per_launch": ms_l,
+                          "algorithmic_bytes_per_launch": d["units"]}
+        else:
+            ach = d["units"] / (ms_l * 1e-3)
+            kernels[k] = {"kernel": d["name"], "bound": "alu", "achieved": ach / 1e12, "peak": lp_rate / 1e12,
+                          "unit": "T limb-products/s", "frac": ach / lp_rate, "traffic": traffic.get(d["name"]),
+                          "ms_per_launch": ms_l, "limb_products_per_launch": d["units"],
+                          "hbm_GBps": d["bytes"] / (ms_l * 1e-3) / 1e9,
+                          "peak_kind": "measured live by toom_probe_limb_products (mad.lo.cc/madc.hi.cc/addc chains, "
+                                       "148 SMs x 8 CTAs)"}
     dominant = max(shares, key=shares.get)
-
-    roofline = {
-        "kernel": "k_base (schoolbook base case, step a3)",
-        "bound": "alu",
-        "achieved": achieved / 1e12,
-        "peak": lp_rate / 1e12,
-        "unit": "T limb-products/s",
-        "frac": achieved / lp_rate,
-        "traffic": None,
-        "peak_kind": "measured on this GPU by toom_probe_limb_products (same mad.lo.cc/madc.hi.cc/addc sequence)",
-        "units_per_launch": lp_per_launch,
-    }
-    stages = {
-        "ms_per_step": {k: round(v, 5) for k, v in shares.items()},
-        "dominant": dominant,
-        "eval_GBps": ev_bytes / (ev_ms * 1e-3) / 1e9 if ev_ms else None,
-        "interp_GBps": it_bytes / (it_ms * 1e-3) / 1e9 if it_ms else None,
-        "hbm_peak_GBps": pk.get("hbm_gbs"), "hbm_peak_kind": pk_kind,
-        "eval_bytes": ev_bytes, "interp_bytes": it_bytes,
-    }
+    roofline = dict(kernels[dominant])
+    roofline["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roofline["bound"] == "hbm" else "live probe") \
+        if pk_kind == "measured" else "fallback"
+    stages = {"ms_per_step": {k: round(prof[k]["ms"] / args.steps, 5) for k in kern}, "dominant": dominant,
+              "kernels": kernels}
 
     # end-to-end through the public C ABI with HOST buffers (pinned)
     e2e = None
@@ -297,6 +302,29 @@ def main():
         e2e = {"value": world * batch * args.steps / dt, "unit": "products/s",
                "h2d_bytes_per_step": 2 * batch * n * 4, "d2h_bytes_per_step": batch * 2 * n * 4,
                "ms_per_step": 1e3 * dt / args.steps}
+
+    # secondary metric of BASELINE.json: ms per 32-Mbit product (configs[3], C4:
+    # one product of two 2^20-limb operands, recursive Toom-4 -> Toom-3)
+    c4 = None
+    if rank == 0 and not args.no_c4:
+        a4, b4 = synth.config_inputs(4)
+        a4, b4 = torch.from_numpy(a4).cuda(), torch.from_numpy(b4).cuda()
+        w4 = torch.empty(2 * a4.numel(), dtype=a4.dtype, device="cuda")
+        for _ in range(2):
+            tg.toom_mul(a4, b4, B=4, out=w4)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        reps = 5
+        e0.record(stream)
+        for _ in range(reps):
+            tg.toom_mul(a4, b4, B=4, out=w4)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        c4 = {"workload": "C4: one product of two 2^20-limb (32-Mbit) uniform operands, Toom-4 -> Toom-3 -> "
+                          "schoolbook (BASELINE.json configs[3])", "ms_per_product": e0.elapsed_time(e1) / reps,
+              "reps": reps, "launches_per_product": tg.last_launch_count()}
+        del a4, b4, w4
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -322,6 +350,7 @@ def main():
             "stages": stages,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "ms_per_32mbit_product": c4,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "us_per_product": 1e3 * ms_per_step / batch,

@@ -54,10 +54,12 @@ typedef enum {
  * lower levels: Toom-4 while the operand has more than t4 limbs, Toom-3
  *        while more than t3 limbs, schoolbook base case otherwise (<= 64 limbs);
  * chunk: products per scheduling chunk (0 = automatic);
- * long_count: recursion levels with fewer than long_count instances (few,
- *        long operands: the upper levels of one large product) run on the
- *        limb-parallel long-vector kernels; deeper levels run one thread (or
- *        lane) per instance.  0 = default (4096); 1 = never.               */
+ * long_count: which recursion levels run on the limb-parallel long-vector
+ *        kernels (the upper levels of one large product: few, long
+ *        operands); the levels below run one thread (or lane) per instance.
+ *        0 = default: levels whose operands exceed 2048 limbs; 1 = never;
+ *        k >= 2: levels with fewer than k instances.  Always a prefix of
+ *        the recursion.                                                    */
 typedef struct {
     int top_B;
     size_t t4;
@@ -142,6 +144,13 @@ double toom_probe_limb_products(double *ms, void *stream);
  * staged launches through HBM; results are identical (tests compare both). */
 void toom_set_fused(int on);
 
+/* Top-level interpolation of batched Toom-3/Toom-4 products: 2 (default) =
+ * products of a group of instances staged in shared memory, rows in place,
+ * then recomposition (k_interp_top_smem); 1 = one streaming pass per product
+ * over the common-denominator matrix form (k_interp_top_stream); 0 = the
+ * per-row kernel (k_interp_top_rows).  All are exact; tests compare them. */
+void toom_set_top_stream(int on);
+
 /* ---- stage exports (tests, bench) ------------------------------------- */
 
 /* Base case alone (step a3): batched schoolbook of signed two's-complement
@@ -157,6 +166,38 @@ toom_status toom_base_interleaved(uint32_t *w, const uint32_t *u, const uint32_t
 toom_status toom_eval_top(uint32_t *out, const uint32_t *a, size_t n, size_t batch, int B, void *stream);
 size_t toom_eval_width(size_t n, int B);
 int toom_npoints(int B);
+
+/* ---- long-path stage exports (sharded top level, C5; SURVEY.md §8(b),(e)) --
+ * These run one top Toom level of `batch` instances on the limb-parallel
+ * long-vector kernels, so that the 2B-1 top-level products can be computed
+ * on other GPUs (Eq. 2.5).  B in {3, 4, 8, 16};
+ * e = toom_eval_width(n, B); all values two's complement little-endian.     */
+
+/* Step a1+a2: out[k][i][0..e) = A_i(x_k) for every point k of B's point set
+ * (homogeneous evaluation sum_j a_ij p^j q^(B-1-j), Eq. 1.1-1.2), where
+ * a[i][0..n) is split into B blocks of ceil(n/B) limbs.  a is unsigned
+ * (is_signed = 0) or two's complement (is_signed = 1).  out: device,
+ * [2B-1][batch][e], must not overlap a.                                     */
+toom_status toom_eval_points(uint32_t *out, const uint32_t *a, size_t n, size_t batch, int B,
+                             int is_signed, void *stream);
+
+/* Steps a4+a5: from the 2B-1 pointwise products y[k][i][0..2e) (Eq. 2.1,
+ * two's complement), interpolate the coefficients w_0..w_{2B-2} (even-odd
+ * method, Eqs. 4.5-4.6, with the listings PAPER.md:114-120, 154-158 or their
+ * matrix form PAPER.md:162; exact divisions) and recompose
+ * w[i][0..2n) = sum_j w_j 2^(32 b j) (Eq. 1.3).  w must not overlap y.      */
+toom_status toom_interp_recompose(uint32_t *w, const uint32_t *y, size_t n, size_t batch, int B,
+                                  void *stream);
+
+/* As toom_mul_batched_plan for two's-complement operands u[i], v[i] of n
+ * limbs; w[i] gets the 2n-limb two's-complement product.  The top level must
+ * be a long-vector level (batch < plan->long_count or its default), else
+ * TOOM_EUNSUPPORTED.  Used for the sharded top-level products of C5.       */
+toom_status toom_mul_signed_batched(uint32_t *w, const uint32_t *u, const uint32_t *v, size_t n,
+                                    size_t batch, const toom_plan_t *plan, void *stream);
+
+/* 2e: limbs of one pointwise product of toom_eval_points' outputs. */
+size_t toom_product_width_point(size_t n, int B);
 
 #ifdef __cplusplus
 }

@@ -60,9 +60,14 @@ SIGNATURES = {
     "toom_npoints": (_I, [_I]),
     "toom_profile_enable": (None, [_I]),
     "toom_set_fused": (None, [_I]),
+    "toom_set_top_stream": (None, [_I]),
     "toom_profile_collect": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_size_t), _I]),
     "toom_plan_describe": (_SZ, [_SZ, _SZ, ctypes.POINTER(ToomPlan), ctypes.c_char_p, _SZ]),
     "toom_probe_limb_products": (ctypes.c_double, [ctypes.POINTER(ctypes.c_double), _P]),
+    "toom_eval_points": (_I, [_P, _P, _SZ, _SZ, _I, _I, _P]),
+    "toom_interp_recompose": (_I, [_P, _P, _SZ, _SZ, _I, _P]),
+    "toom_mul_signed_batched": (_I, [_P, _P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
+    "toom_product_width_point": (_SZ, [_SZ, _I]),
 }
 
 
@@ -166,6 +171,40 @@ def eval_top(a: torch.Tensor, B: int, stream=None) -> torch.Tensor:
     return out
 
 
+def eval_points(a: torch.Tensor, B: int, signed: bool = False, stream=None) -> torch.Tensor:
+    """Long-path stage a1+a2: a [batch][n] -> [2B-1][batch][e] values at the
+    point set of B (two's complement)."""
+    batch, n = a.shape
+    e = lib().toom_eval_width(n, B)
+    npts = lib().toom_npoints(B)
+    out = torch.empty((npts, batch, e), dtype=a.dtype, device=a.device)
+    _check(lib().toom_eval_points(_dev(out, "out"), _dev(a, "a"), n, batch, B, 1 if signed else 0, _stream(stream)),
+           "toom_eval_points")
+    return out
+
+
+def interp_recompose(y: torch.Tensor, n: int, B: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Long-path stages a4+a5: y [2B-1][batch][2e] products -> w [batch][2n]."""
+    npts, batch, w2 = y.shape
+    if out is None:
+        out = torch.empty((batch, 2 * n), dtype=y.dtype, device=y.device)
+    _check(lib().toom_interp_recompose(_dev(out, "out"), _dev(y, "y"), n, batch, B, _stream(stream)),
+           "toom_interp_recompose")
+    return out
+
+
+def mul_signed_batched(u: torch.Tensor, v: torch.Tensor, B: int = 4, t4: int = 256, t3: int = 64,
+                       long_count: int = 0, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Two's-complement products w[i] = u[i]*v[i] ([batch][n] -> [batch][2n])."""
+    batch, n = u.shape
+    if out is None:
+        out = torch.empty((batch, 2 * n), dtype=u.dtype, device=u.device)
+    p = plan(B, t4, t3, 0, long_count)
+    _check(lib().toom_mul_signed_batched(_dev(out, "out"), _dev(u, "u"), _dev(v, "v"), n, batch, ctypes.byref(p),
+                                         _stream(stream)), "toom_mul_signed_batched")
+    return out
+
+
 def workspace_bytes(n: int, batch: int, B: int = 4, t4: int = 256, t3: int = 64, chunk: int = 0) -> int:
     p = plan(B, t4, t3, chunk)
     return lib().toom_workspace_bytes(n, batch, ctypes.byref(p))
@@ -193,6 +232,12 @@ CATEGORIES = ("eval", "base", "interp", "other")
 def set_fused(on: bool = True):
     """Use (default) or bypass the fused bottom-level kernel."""
     lib().toom_set_fused(1 if on else 0)
+
+
+def set_top_stream(mode: int = 2):
+    """Top-level interpolation kernel: 2 smem-staged (default), 1 one-pass
+    stream, 0 per-row (all exact)."""
+    lib().toom_set_top_stream(int(mode))
 
 
 def profile_enable(on: bool = True):

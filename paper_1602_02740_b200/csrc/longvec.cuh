@@ -33,7 +33,7 @@ namespace tg {
 
 constexpr int LV_MAXT = 40;     // terms per op
 constexpr int LV_NT = 256;      // threads per tile
-constexpr int LV_CH = 4;        // limbs per thread
+constexpr int LV_CH = 16;       // limbs per thread
 constexpr int LV_TL = LV_NT * LV_CH;
 constexpr int LV_MAXHALO = 8;   // look-ahead limbs of the final right shift (shr < 32*7)
 
@@ -54,8 +54,10 @@ struct LOpDev {
     int nt;
     uint32_t o, oinv;           // exact division by odd o (o = 1: none)
     uint32_t p32, Mch, mi;      // 2^32 mod o, 2^(32 CH) mod o, (2^(32 CH))^-1 mod o
+    unsigned long long orcp;    // floor(2^64 / o) (Barrett reduction)
     int sa, sr;                 // final right shift shr = 32 sa + sr
     int tiles_per_inst;
+    int nthreads;               // threads per tile (multiple of 32, <= LV_NT)
     int count;
     int wide;                   // 128-bit accumulators
     LTermDev t[LV_MAXT];
@@ -74,30 +76,45 @@ struct LStatus {
     LAgg agg;
 };
 
-__device__ __forceinline__ uint32_t lv_mulmod(uint32_t a, uint32_t b, uint32_t o) {
-    return (uint32_t)(((unsigned long long)a * b) % o);
+// modulus o (odd, < 2^32) with its Barrett reciprocal floor(2^64 / o)
+struct LMod {
+    uint32_t o;
+    unsigned long long rcp;
+};
+__device__ __forceinline__ uint32_t lv_mod(unsigned long long x, const LMod& M) {
+    const unsigned long long q = __umul64hi(x, M.rcp);
+    unsigned long long r = x - q * M.o;
+    while (r >= M.o) r -= M.o;
+    return (uint32_t)r;
 }
-__device__ __forceinline__ uint32_t lv_negmod(long long c, uint32_t o) {
-    long long r = c % (long long)o;          // in (-o, o)
-    if (r < 0) r += o;
-    return r ? o - (uint32_t)r : 0u;         // (-c) mod o
+__device__ __forceinline__ uint32_t lv_mulmod(uint32_t a, uint32_t b, const LMod& M) {
+    return lv_mod((unsigned long long)a * b, M);
+}
+// (-c) mod o for a signed 64-bit c
+__device__ __forceinline__ uint32_t lv_negmod(long long c, const LMod& M) {
+    const uint32_t r = lv_mod((unsigned long long)(c < 0 ? -c : c), M);   // |c| mod o (|c| < 2^63)
+    return c < 0 ? r : (r ? M.o - r : 0u);
 }
 __device__ __forceinline__ int lv_piece(const LAgg& A, long long c) { return c < A.lo ? 0 : (c >= A.hi ? 2 : 1); }
+// element p of a 3-array without dynamic indexing (keeps it in registers)
+template <typename T>
+__device__ __forceinline__ T lv_sel(const T (&a)[3], int p) { return p == 0 ? a[0] : (p == 1 ? a[1] : a[2]); }
 
 // A then B
-__device__ __forceinline__ LAgg lv_compose(const LAgg& A, const LAgg& B, uint32_t o) {
+__device__ __forceinline__ LAgg lv_compose(const LAgg& A, const LAgg& B, const LMod& M) {
+    const uint32_t o = M.o;
     LAgg C;
     C.lo = A.lo;
     C.hi = A.hi;
-    C.m = (o > 1) ? lv_mulmod(A.m, B.m, o) : 0u;
+    C.m = (o > 1) ? lv_mulmod(A.m, B.m, M) : 0u;
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
         const long long c1 = A.cout[p];
         const int q = lv_piece(B, c1);
-        C.cout[p] = B.cout[q];
+        C.cout[p] = lv_sel(B.cout, q);
         if (o > 1) {
-            const unsigned long long x = (unsigned long long)A.g[p] * B.m + (unsigned long long)lv_negmod(c1, o) * B.m + B.g[q];
-            C.g[p] = (uint32_t)(x % o);
+            const unsigned long long x = (unsigned long long)A.g[p] * B.m + (unsigned long long)lv_negmod(c1, M) * B.m + lv_sel(B.g, q);
+            C.g[p] = lv_mod(x, M);
         } else {
             C.g[p] = 0;
         }
@@ -105,13 +122,13 @@ __device__ __forceinline__ LAgg lv_compose(const LAgg& A, const LAgg& B, uint32_
     return C;
 }
 
-__device__ __forceinline__ void lv_apply(const LAgg& A, long long& c, uint32_t& beta, uint32_t o) {
+__device__ __forceinline__ void lv_apply(const LAgg& A, long long& c, uint32_t& beta, const LMod& M) {
     const int p = lv_piece(A, c);
-    if (o > 1) {
-        const unsigned long long x = (unsigned long long)beta * A.m + (unsigned long long)lv_negmod(c, o) * A.m + A.g[p];
-        beta = (uint32_t)(x % o);
+    if (M.o > 1) {
+        const unsigned long long x = (unsigned long long)beta * A.m + (unsigned long long)lv_negmod(c, M) * A.m + lv_sel(A.g, p);
+        beta = lv_mod(x, M);
     }
-    c = A.cout[p];
+    c = lv_sel(A.cout, p);
 }
 
 __device__ __forceinline__ LAgg lv_shfl_up(const LAgg& a, int d) {
@@ -168,14 +185,16 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
     __shared__ unsigned s_beta;
     __shared__ uint32_t Q[LV_TL + LV_MAXHALO + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int NT = blockDim.x, NW = NT >> 5, TL = NT * LV_CH;   // NT: a multiple of 32, <= LV_NT
     if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
     const long long inst = tile / op.tiles_per_inst;
     const int k = (int)(tile - inst * op.tiles_per_inst);
-    const int tstart = k * LV_TL;
+    const int tstart = k * TL;
     const int p0 = tstart + tid * LV_CH;
     const uint32_t o = op.o;
+    const LMod M{op.o, op.orcp};
     const int nt = op.nt;
 
     Acc lin[LV_CH];
@@ -205,13 +224,13 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
         if (o > 1) {
             uint32_t r = 0;
 #pragma unroll
-            for (int q = LV_CH - 1; q >= 0; --q) r = (uint32_t)(((unsigned long long)r * op.p32 + x[q]) % o);
+            for (int q = LV_CH - 1; q >= 0; --q) r = lv_mod((unsigned long long)r * op.p32 + x[q], M);
             A.m = op.mi;
 #pragma unroll
             for (int p = 0; p < 3; ++p) {
                 // g[p] = (-Lmod + (p-1) M) * mi mod o
                 unsigned long long t = (unsigned long long)(o - r) + (p == 2 ? op.Mch : 0u) + (p == 0 ? (o - op.Mch) : 0u);
-                A.g[p] = lv_mulmod((uint32_t)(t % o), op.mi, o);
+                A.g[p] = lv_mulmod(lv_mod(t, M), op.mi, M);
             }
         } else {
             A.m = 0;
@@ -223,7 +242,7 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         const LAgg prev = lv_shfl_up(inc, d);
-        if (lane >= d) inc = lv_compose(prev, inc, o);
+        if (lane >= d) inc = lv_compose(prev, inc, M);
     }
     const LAgg excl = lv_shfl_up(inc, 1);   // valid for lane > 0
     if (lane == 31) s_wagg[warp] = inc;
@@ -231,57 +250,100 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
     // tile aggregate, published before the look-back
     const bool first = (k == 0);
     LStatus* st = status + tile;
-    if (tid == 0) {
+    if (warp == 0) {
         LAgg T = s_wagg[0];
-        for (int w = 1; w < LV_NT / 32; ++w) T = lv_compose(T, s_wagg[w], o);
+        for (int w = 1; w < NW; ++w) T = lv_compose(T, s_wagg[w], M);
         long long cin = 0;
         uint32_t bin = 0;
         if (!first) {
-            st->agg = T;
-            __threadfence();
-            atomicExch(&st->flag, epoch * 4u + 1u);
-            // decoupled look-back over the tiles of this instance
-            bool have = false;
-            LAgg acc;
-            long long j = (long long)tile - 1;
-            for (;;) {
-                LStatus* ps = status + j;
-                unsigned f;
-                do { f = *(volatile unsigned*)&ps->flag; } while (f != epoch * 4u + 1u && f != epoch * 4u + 2u);
+            if (lane == 0) {
+                st->agg = T;
                 __threadfence();
-                if (f == epoch * 4u + 2u) {
-                    cin = *(volatile long long*)&ps->c;
-                    bin = *(volatile unsigned*)&ps->beta;
-                    if (have) lv_apply(acc, cin, bin, o);
+                atomicExch(&st->flag, epoch * 4u + 1u);
+            }
+            // decoupled look-back over the tiles of this instance, a window
+            // of 32 predecessors per step (lane L looks at tile jhi - L)
+            const long long base = (long long)tile - k;   // first tile of the instance (always inclusive)
+            bool have = false;
+            LAgg acc;                                       // composition of the later windows
+            long long jhi = (long long)tile - 1;
+            for (;;) {
+                const long long j = jhi - lane;
+                unsigned f = 0;
+                LAgg a;
+                a.lo = LLONG_MIN; a.hi = LLONG_MAX;
+                a.cout[0] = a.cout[1] = a.cout[2] = 0; a.m = 1; a.g[0] = a.g[1] = a.g[2] = 0;
+                long long ic = 0;
+                unsigned ib = 0;
+                if (j >= base) {
+                    LStatus* ps = status + j;
+                    do { f = *(volatile unsigned*)&ps->flag; } while (f != epoch * 4u + 1u && f != epoch * 4u + 2u);
+                    __threadfence();
+                    if (f == epoch * 4u + 2u) {
+                        ic = *(volatile long long*)&ps->c;
+                        ib = *(volatile unsigned*)&ps->beta;
+                    } else {
+                        volatile LAgg* va = (volatile LAgg*)&ps->agg;
+                        a.lo = va->lo; a.hi = va->hi;
+                        a.cout[0] = va->cout[0]; a.cout[1] = va->cout[1]; a.cout[2] = va->cout[2];
+                        a.m = va->m; a.g[0] = va->g[0]; a.g[1] = va->g[1]; a.g[2] = va->g[2];
+                    }
+                }
+                const unsigned incm = __ballot_sync(0xffffffffu, f == epoch * 4u + 2u);
+                const int lim = incm ? (__ffs(incm) - 1) : 32;   // lanes [0, lim) carry aggregates
+                // ordered reduction of the aggregates of lanes [0, lim) into lane 0
+                // (a higher lane is an earlier tile: combined = compose(x[L+d], x[L]))
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    LAgg other;
+                    other.lo = __shfl_down_sync(0xffffffffu, a.lo, d);
+                    other.hi = __shfl_down_sync(0xffffffffu, a.hi, d);
+#pragma unroll
+                    for (int p = 0; p < 3; ++p) {
+                        other.cout[p] = __shfl_down_sync(0xffffffffu, a.cout[p], d);
+                        other.g[p] = __shfl_down_sync(0xffffffffu, a.g[p], d);
+                    }
+                    other.m = __shfl_down_sync(0xffffffffu, a.m, d);
+                    if ((lane & (2 * d - 1)) == 0 && lane + d < lim) a = lv_compose(other, a, M);
+                }
+                if (incm) {
+                    ic = __shfl_sync(0xffffffffu, ic, lim);
+                    ib = __shfl_sync(0xffffffffu, ib, lim);
+                    if (lane == 0) {
+                        cin = ic;
+                        bin = ib;
+                        if (lim > 0) lv_apply(a, cin, bin, M);
+                        if (have) lv_apply(acc, cin, bin, M);
+                    }
                     break;
                 }
-                LAgg a;
-                volatile LAgg* va = (volatile LAgg*)&ps->agg;
-                a.lo = va->lo; a.hi = va->hi;
-                a.cout[0] = va->cout[0]; a.cout[1] = va->cout[1]; a.cout[2] = va->cout[2];
-                a.m = va->m; a.g[0] = va->g[0]; a.g[1] = va->g[1]; a.g[2] = va->g[2];
-                acc = have ? lv_compose(a, acc, o) : a;
-                have = true;
-                --j;
+                if (lane == 0) {
+                    acc = have ? lv_compose(a, acc, M) : a;
+                    have = true;
+                }
+                have = __shfl_sync(0xffffffffu, have, 0);
+                jhi -= 32;
             }
         }
-        // inclusive state of this tile
-        long long cout = cin;
-        uint32_t bout = bin;
-        lv_apply(T, cout, bout, o);
-        st->c = cout;
-        st->beta = bout;
-        __threadfence();
-        atomicExch(&st->flag, epoch * 4u + 2u);
-        s_c = cin;
-        s_beta = bin;
+        if (lane == 0) {
+            // inclusive state of this tile
+            long long cout = cin;
+            uint32_t bout = bin;
+            lv_apply(T, cout, bout, M);
+            st->c = cout;
+            st->beta = bout;
+            __threadfence();
+            atomicExch(&st->flag, epoch * 4u + 2u);
+            s_c = cin;
+            s_beta = bin;
+        }
     }
     __syncthreads();
     // this thread's carry-in / borrow-in
     long long cin = s_c;
     uint32_t bin = s_beta;
-    for (int w = 0; w < warp; ++w) lv_apply(s_wagg[w], cin, bin, o);
-    if (lane > 0) lv_apply(excl, cin, bin, o);
+    for (int w = 0; w < warp; ++w) lv_apply(s_wagg[w], cin, bin, M);
+    if (lane > 0) lv_apply(excl, cin, bin, M);
     // exact limbs, exact division, quotients to smem
     c = cin;
     uint32_t beta = bin;
@@ -294,23 +356,25 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
         Q[tid * LV_CH + q] = xq;
     }
     const int halo = op.sa + (op.sr ? 1 : 0);
-    if (tid == LV_NT - 1 && halo > 0) {
+    if (tid == NT - 1 && halo > 0) {
         // quotient limbs just past the tile (the next tile's first limbs),
         // continuing this tile's carry / borrow chain
         Acc hl[LV_MAXHALO];
-        lv_lincomb<Acc, LV_MAXHALO>(op, nt, inst, tstart + LV_TL, hl);
-        for (int h = 0; h < halo; ++h) {
+        lv_lincomb<Acc, LV_MAXHALO>(op, nt, inst, tstart + TL, hl);
+#pragma unroll
+        for (int h = 0; h < LV_MAXHALO; ++h) {
+            if (h >= halo) break;
             const Acc v = hl[h] + (Acc)c;
             uint32_t xq = (uint32_t)v;
             c = (long long)(v >> 32);
             if (o > 1) xq = tg_divexact_step(xq, beta, op.oinv, o);
-            Q[LV_TL + h] = xq;
+            Q[TL + h] = xq;
         }
     }
     __syncthreads();
     // right shift, coalesced stores
     uint32_t* dst = op.dst + inst * op.dst_inst_stride;
-    for (int i = tid; i < LV_TL; i += LV_NT) {
+    for (int i = tid; i < TL; i += NT) {
         const int t = tstart + i;
         if (t >= op.W) break;
         const uint32_t lo = Q[i + op.sa];
@@ -367,13 +431,23 @@ struct LOpBuilder {
         op.o = o;
         op.oinv = host_inv32(o);
         if (o > 1) {
+            op.orcp = ~0ull / o;   // floor((2^64 - 1) / o) == floor(2^64 / o) for odd o > 1
             op.p32 = host_powmod(2, 32, o);
             op.Mch = host_powmod(2, 32ull * LV_CH, o);
             op.mi = host_invmod(op.Mch, o);
         }
         op.sa = shr / 32;
         op.sr = shr % 32;
-        op.tiles_per_inst = (W + LV_TL - 1) / LV_TL;
+        // tile size: the fewest padded limbs, then the largest tile
+        int best = LV_NT;
+        long long bestw = -1;
+        for (int nt = LV_NT; nt >= 64; nt -= 32) {
+            const long long tl = (long long)nt * LV_CH, tiles = (W + tl - 1) / tl;
+            const long long pad = tiles * tl;
+            if (bestw < 0 || pad < bestw) { bestw = pad; best = nt; }
+        }
+        op.nthreads = best;
+        op.tiles_per_inst = (W + best * LV_CH - 1) / (best * LV_CH);
     }
     // term m * (slice << s), slice = limbs [start, start+len) of v (len clipped to v.len)
     bool add(const LVec& v, long long m, long long s, int start = 0, int len = -1, int sign = -1) {

@@ -422,7 +422,7 @@ static int long_Wt(const Level& L) {
     long_tables(L.B, T);
     return L.Lw + T.lag;
 }
-static size_t long_tiles(size_t count, int W) { return count * (size_t)((W + LV_TL - 1) / LV_TL); }
+static size_t long_tiles(size_t count, int W) { return count * (size_t)((W + 64 * LV_CH - 1) / (64 * LV_CH)); }
 
 // base widths with a fused bottom-level instantiation (C1 33, C2 18, C3/C4/C5 23, ...)
 static bool fused_E_supported(int E) {
@@ -448,7 +448,7 @@ static int choose_B(const toom_plan_t& p, int depth, int n) {
     return B;
 }
 
-static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& plan) {
+static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& plan, bool top_long = false) {
     plan.lv.clear();
     size_t count = batch;
     int width = n;
@@ -476,11 +476,15 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
     }
     // long-vector levels: a prefix of the Toom levels with few instances
     {
-        const size_t lc = p.long_count ? p.long_count : 4096;
+        // default (long_count = 0): operands longer than 2048 limbs (few,
+        // long vectors: one thread per instance would stream too long);
+        // long_count = 1: never; otherwise: levels with < long_count instances
         LongTables T;
         for (size_t l = 0; l + 1 < plan.lv.size(); ++l) {
             Level& L = plan.lv[l];
-            if (L.count < lc && long_tables(L.B, T)) L.lng = true;
+            const bool want = L.B == 16 || (top_long && l == 0) ||   // T16: no instance-parallel program
+                              (p.long_count == 0 ? (L.n > 2048) : (p.long_count > 1 && L.count < p.long_count));
+            if (want && long_tables(L.B, T)) L.lng = true;
             else break;
         }
         for (size_t l = 0; l + 1 < plan.lv.size(); ++l)
@@ -714,8 +718,47 @@ static void launch_interp_top_rows_t(const Level& Lv, const uint32_t* P1, uint32
     k_interp_top_rows<B><<<grid, 32 * (2 * B - 1), smem, st>>>(P1, w, Lv.count, 2 * Lv.e, Lv.Lw, Lv.b, 2 * Lv.n, nseg);
 }
 
+static int g_top_stream = 2;   // 2: smem kernel, 1: one-pass stream, 0: per-row kernel
+
+template <int B>
+static bool launch_interp_top_smem_t(const Level& Lv, const uint32_t* P1, uint32_t* w, cudaStream_t st) {
+    const int ywidth = 2 * Lv.e, nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
+    constexpr int NP = 2 * B - 1;
+    // instances per CTA: up to 32, two CTAs per SM if possible
+    int G = 32;
+    while (G > 8 && interp_top_smem_bytes(B, ywidth, G, nseg) > 113 * 1024) G -= 4;
+    if (interp_top_smem_bytes(B, ywidth, G, nseg) > 220 * 1024 || Lv.Lw >= ywidth || Lv.Lw != 2 * Lv.b + 1) return false;
+    const size_t smem = interp_top_smem_bytes(B, ywidth, G, nseg);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_interp_top_smem<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_interp_top_smem<B>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    const unsigned grid = (unsigned)((Lv.count + G - 1) / G);
+    k_interp_top_smem<B><<<grid, 32 * NP, smem, st>>>(P1, w, Lv.count, ywidth, Lv.Lw, Lv.b, 2 * Lv.n, G, nseg);
+    return true;
+}
+
 static toom_status launch_interp_top_rows(const Level& Lv, const uint32_t* P1, uint32_t* w, cudaStream_t st) {
     ProfScope ps(CAT_INTERP, st);
+    if (g_top_stream == 2) {
+        const bool ok = Lv.B == 3 ? launch_interp_top_smem_t<3>(Lv, P1, w, st) : launch_interp_top_smem_t<4>(Lv, P1, w, st);
+        if (ok) {
+            ps.done(st);
+            ++t_launches;
+            return TOOM_OK;
+        }
+    }
+    const int X = 2 * Lv.e - 2 * Lv.b;
+    if (g_top_stream >= 1 && X >= 0 && X <= Lv.b) {
+        const unsigned grid = (unsigned)((Lv.count + 32 * ITS_WARPS - 1) / (32 * ITS_WARPS));
+        if (Lv.B == 3) k_interp_top_stream<3><<<grid, 32 * ITS_WARPS, 0, st>>>(P1, w, Lv.count, 2 * Lv.e, Lv.b, 2 * Lv.n);
+        else k_interp_top_stream<4><<<grid, 32 * ITS_WARPS, 0, st>>>(P1, w, Lv.count, 2 * Lv.e, Lv.b, 2 * Lv.n);
+        ps.done(st);
+        ++t_launches;
+        return TOOM_OK;
+    }
     if (Lv.B == 3) launch_interp_top_rows_t<3>(Lv, P1, w, st);
     else launch_interp_top_rows_t<4>(Lv, P1, w, st);
     ps.done(st);
@@ -872,8 +915,8 @@ static toom_status launch_long_ops(const std::vector<LOpDev>& ops, size_t first,
         const unsigned grid = (unsigned)((size_t)o.count * o.tiles_per_inst);
         if (grid == 0) continue;
         ProfScope ps(cat, st);
-        if (o.wide) k_long_op<true><<<grid, LV_NT, 0, st>>>(ddesc + first + i, status, epoch, ctr + first + i);
-        else k_long_op<false><<<grid, LV_NT, 0, st>>>(ddesc + first + i, status, epoch, ctr + first + i);
+        if (o.wide) k_long_op<true><<<grid, o.nthreads, 0, st>>>(ddesc + first + i, status, epoch, ctr + first + i);
+        else k_long_op<false><<<grid, o.nthreads, 0, st>>>(ddesc + first + i, status, epoch, ctr + first + i);
         ps.done(st);
         ++epoch;
         ++t_launches;
@@ -994,7 +1037,7 @@ static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, si
     size_t chunk = p.chunk ? p.chunk : batch;
     if (chunk > batch) chunk = batch;
     Plan plan;
-    if ((s = make_plan((int)n, chunk, p, plan))) return s;
+    if ((s = make_plan((int)n, chunk, p, plan, sgn))) return s;
     plan.signed_in = sgn;
     if (sgn && plan.lv.size() > 1 && !plan.lv[0].lng) return TOOM_EUNSUPPORTED;   // signed top level: long path only
     size_t need = plan.bytes;
@@ -1005,7 +1048,7 @@ static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, si
         const size_t cnt = (batch - c0 < chunk) ? batch - c0 : chunk;
         if (cnt != chunk) {
             Plan p2;
-            if ((s = make_plan((int)n, cnt, p, p2))) return s;
+            if ((s = make_plan((int)n, cnt, p, p2, sgn))) return s;
             p2.signed_in = sgn;
             if (sgn && p2.lv.size() > 1 && !p2.lv[0].lng) return TOOM_EUNSUPPORTED;
             if ((s = run_plan(p2, w + c0 * 2 * n, u + c0 * n, v + c0 * n, (int)n, cnt, (uint8_t*)ws, st))) return s;
@@ -1023,11 +1066,99 @@ __global__ void k_pad_copy(const uint32_t* __restrict__ src, size_t nsrc, uint32
     if (i < ndst) dst[i] = i < nsrc ? src[i] : 0u;
 }
 
+// one top Toom level (count instances of n limbs) run on the long path
+static bool long_top_level(size_t n, size_t count, int B, Level& L) {
+    LongTables T;
+    const PSDesc d = ps_desc(B);
+    if (!d.B || !long_tables(B, T) || n > (1u << 30) || !split_ok((int)n, B)) return false;
+    L.B = B;
+    L.count = count;
+    L.n = (int)n;
+    L.npts = d.npts;
+    L.b = (L.n + B - 1) / B;
+    L.lentop = L.n - (B - 1) * L.b;
+    L.e = L.b + (bitlen(d.S) + 1 + 31) / 32;
+    L.Lw = 2 * L.b + 1;
+    L.lng = true;
+    return true;
+}
+
+// run long ops with a scratch workspace [slots | status | ctr | desc]; `build`
+// appends the ops given the slot pool pointer
+template <class BuildF>
+static toom_status run_long_standalone(size_t slot_limbs, size_t tiles, size_t nops, BuildF build, cudaStream_t st) {
+    auto rnd = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t bS = rnd(slot_limbs * 4), bT = rnd(tiles * sizeof(LStatus)), bC = rnd(nops * 4),
+                 bD = rnd(nops * sizeof(LOpDev));
+    void* ws = nullptr;
+    toom_status s;
+    if ((s = get_ws(bS + bT + bC + bD, &ws))) return s;
+    uint8_t* base = (uint8_t*)ws;
+    LStatus* status = (LStatus*)(base + bS);
+    unsigned* ctr = (unsigned*)(base + bS + bT);
+    LOpDev* ddesc = (LOpDev*)(base + bS + bT + bC);
+    std::vector<LOpDev> ops, none;
+    build((uint32_t*)base, ops);
+    if (ops.size() > nops) return TOOM_EINVAL;
+    if ((s = long_prepare(ops, none, ddesc, status, tiles, ctr, nops, st))) return s;
+    unsigned epoch = 1;
+    return launch_long_ops(ops, 0, ddesc, status, ctr, epoch, CAT_OTHER, st);
+}
+
 }  // namespace tg
 
 using namespace tg;
 
 extern "C" {
+
+toom_status toom_mul_signed_batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
+                                    const toom_plan_t* plan, void* stream) {
+    if (!plan) return fail(TOOM_EINVAL);
+    return fail(batched(w, u, v, n, batch, *plan, (cudaStream_t)stream, true));
+}
+
+toom_status toom_eval_points(uint32_t* out, const uint32_t* a, size_t n, size_t batch, int B, int is_signed,
+                             void* stream) {
+    t_launches = 0;
+    Level L;
+    if (!out || !a || !long_top_level(n, batch, B, L)) return fail(TOOM_EINVAL);
+    if (batch == 0) return TOOM_OK;
+    if (overlaps(out, (size_t)L.npts * batch * L.e * 4, a, n * batch * 4)) return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    LongTables T;
+    long_tables(B, T);
+    const LVec par{a, (long long)n, 1, (int)n, is_signed ? 1 : 0};
+    s = run_long_standalone(0, long_tiles(batch, L.e), (size_t)T.neo,
+                            [&](uint32_t*, std::vector<LOpDev>& ops) {
+                                long_eval_ops(L, par, [&](int k) { return LVec{out + (size_t)k * batch * L.e, L.e, 1, L.e, 1}; }, ops);
+                            },
+                            (cudaStream_t)stream);
+    if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+    return fail(s);
+}
+
+toom_status toom_interp_recompose(uint32_t* w, const uint32_t* y, size_t n, size_t batch, int B, void* stream) {
+    t_launches = 0;
+    Level L;
+    if (!w || !y || !long_top_level(n, batch, B, L)) return fail(TOOM_EINVAL);
+    if (batch == 0) return TOOM_OK;
+    if (overlaps(w, 2 * n * batch * 4, y, (size_t)L.npts * batch * 2 * L.e * 4)) return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    LongTables T;
+    long_tables(B, T);
+    const int Wt = long_Wt(L);
+    const size_t slot_limbs = (size_t)T.nslots * batch * Wt;
+    s = run_long_standalone(slot_limbs, long_tiles(batch, std::max(Wt, 2 * L.n)), (size_t)T.nio + 1,
+                            [&](uint32_t* slots, std::vector<LOpDev>& ops) {
+                                long_interp_ops(L, [&](int k) { return LVec{y + (size_t)k * batch * 2 * L.e, 2 * L.e, 1, 2 * L.e, 1}; },
+                                                slots, w, ops);
+                            },
+                            (cudaStream_t)stream);
+    if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+    return fail(s);
+}
 
 toom_plan_t toom_default_plan(int B) {
     toom_plan_t p;
@@ -1167,6 +1298,8 @@ toom_status toom_base_interleaved(uint32_t* w, const uint32_t* u, const uint32_t
 
 int toom_npoints(int B) { return ps_desc(B).npts; }
 
+void toom_set_top_stream(int on) { g_top_stream = on; }
+
 void toom_set_fused(int on) {
     // 0: every level staged (k_eval / k_base / k_interp); 1: fused bottom level
     // and warp-per-row top level (default)
@@ -1217,6 +1350,8 @@ size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t* plan, char*
     }
     return js.size() + 1;
 }
+
+size_t toom_product_width_point(size_t n, int B) { return 2 * toom_eval_width(n, B); }
 
 size_t toom_eval_width(size_t n, int B) {
     const PSDesc d = ps_desc(B);

@@ -226,3 +226,258 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_rows(
 }
 
 }  // namespace tg
+
+namespace tg {
+
+// ------------------------------------------------------------------------
+// Top-level interpolation + recomposition in ONE streaming pass per product
+// (steps a4 + a5; C1, C2).  The per-coefficient matrix form of the even-odd +
+// listing program over the common denominator Dc = lcm D_j:
+//     Dc * w = sum_j 2^(32 b j) N_j,   N_j = sum_k A'_jk y_k  (= Dc w_j >= 0)
+// One thread per product streams w LSB-first: at output limb t = s b + r the
+// rows j = s, s-1, s-2 contribute N_j limbs r, b + r, 2b + r, each row with
+// its own signed carry chain (a chain ends after 2e limbs: N_j < 2^(32*2e));
+// the three limb streams plus an unsigned carry give Dc*w, which is divided
+// exactly by the odd part of Dc (2-adic inverse) and shifted by its power of
+// two.  Products are read interleaved (coalesced across the warp); output
+// limbs are staged per warp in shared memory and written row-major.
+// ------------------------------------------------------------------------
+template <int B> struct Comb;
+template <> struct Comb<3> {
+    static constexpr unsigned o = tg_combO_T3, inv = tg_combInv_T3;
+    static constexpr int s = tg_combS_T3;
+    __device__ static int A(int j, int k) { return (int)tg_combA_T3[j][k]; }
+};
+template <> struct Comb<4> {
+    static constexpr unsigned o = tg_combO_T4, inv = tg_combInv_T4;
+    static constexpr int s = tg_combS_T4;
+    __device__ static int A(int j, int k) { return (int)tg_combA_T4[j][k]; }
+};
+
+constexpr int ITS_WARPS = 4;
+
+template <int B>
+__global__ void __launch_bounds__(32 * ITS_WARPS) k_interp_top_stream(const uint32_t* __restrict__ P1,
+                                                                      uint32_t* __restrict__ w, size_t count,
+                                                                      int ywidth, int b, int wout) {
+    constexpr int NP = 2 * B - 1;
+    __shared__ uint32_t stage[ITS_WARPS][32][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t c0w = (size_t)blockIdx.x * blockDim.x + (size_t)warp * 32;
+    const size_t c = c0w + lane;
+    const bool valid = c < count;
+    const size_t S = (size_t)NP * count;
+    const uint32_t* yb = P1 + (valid ? c : 0);
+    const int X = ywidth - 2 * b;                 // limbs of y_k beyond 2b
+    long long ca = 0, cb = 0, cc = 0;             // row carries (j = s, s-1, s-2)
+    unsigned long long T = 0;                     // carry of the sum
+    uint32_t bor = 0, qp = 0;
+    uint32_t(*buf)[33] = stage[warp];
+    const int nseg = wout / b + 1;                // covers limbs 0 .. wout (one extra for the shift)
+    for (int s = 0; s <= nseg; ++s) {
+        const bool hA = s < NP, hB = s >= 1 && s - 1 < NP, hC = s >= 2 && s - 2 < NP;
+        int Aa[NP], Ab[NP], Ac[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            Aa[k] = hA ? Comb<B>::A(s, k) : 0;
+            Ab[k] = hB ? Comb<B>::A(s - 1, k) : 0;
+            Ac[k] = hC ? Comb<B>::A(s - 2, k) : 0;
+        }
+        cc = cb;
+        cb = ca;
+        ca = 0;
+        const int t0 = s * b;
+        const int rmax = min(b, wout + 1 - t0);
+        for (int r = 0; r < rmax; ++r) {
+            long long la = ca, lb = cb, lc = cc;
+            if (valid) {
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    const uint32_t* yk = yb + (size_t)k * count;
+                    if (hA) la += (long long)Aa[k] * (long long)__ldg(yk + (size_t)r * S);
+                    if (hB) lb += (long long)Ab[k] * (long long)__ldg(yk + (size_t)(b + r) * S);
+                    if (hC && r < X) lc += (long long)Ac[k] * (long long)__ldg(yk + (size_t)(2 * b + r) * S);
+                }
+            }
+            ca = la >> 32;
+            cb = lb >> 32;
+            unsigned long long x = T + (uint32_t)la + (uint32_t)lb;
+            if (r < X) {
+                cc = lc >> 32;
+                x += (uint32_t)lc;
+            }
+            T = x >> 32;
+            const uint32_t q = tg_divexact_step((uint32_t)x, bor, Comb<B>::inv, Comb<B>::o);
+            const int t = t0 + r;
+            if (t > 0) {
+                const int e = t - 1;
+                buf[e & 31][lane] = Comb<B>::s ? __funnelshift_r(qp, q, Comb<B>::s) : qp;
+                if ((e & 31) == 31 || e == wout - 1) {
+                    __syncwarp();
+                    const int eb = e & ~31;
+                    const int ncol = e - eb + 1;
+                    for (int i = 0; i < 32; ++i) {
+                        if (c0w + i < count && lane < ncol) w[(c0w + i) * (size_t)wout + eb + lane] = buf[lane][i];
+                    }
+                    __syncwarp();
+                }
+            }
+            qp = q;
+        }
+    }
+}
+
+}  // namespace tg
+
+namespace tg {
+
+// ------------------------------------------------------------------------
+// Top-level interpolation + recomposition with the products of a group of G
+// instances resident in shared memory (steps a4 + a5; C1, C2):
+//   phase 0  all threads: cp.async the 2B-1 products of the G instances,
+//            [NP][2e][G] (each (limb, point) row is G contiguous words)
+//   phase 1  warp j (1 <= j <= NP-2): stream the coefficient row
+//            w_j = (sum_k A_jk y_k) / D_j (even-odd + listing program composed
+//            per row) LSB-first, in lock-stepped chunks, and
+//            write w_j in place over y_j (w_0 = y_0, w_2n = y_inf)
+//   phase 2  recompose w = sum_j w_j 2^(32 b j) (Eq. 1.3) segment by segment:
+//            local carries, one lane per instance resolves the carries between
+//            segments, then the final limbs go to the row-major output.
+// ------------------------------------------------------------------------
+__host__ __device__ inline size_t interp_top_smem_bytes(int B, int ywidth, int G, int nseg) {
+    return (size_t)4 * ((size_t)(2 * B - 1) * ywidth * G + 4 * (size_t)nseg * G);
+}
+
+__device__ __forceinline__ void cp_async4(uint32_t* dst_smem, const uint32_t* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
+}
+
+template <int B>
+__global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint32_t* __restrict__ P1,
+                                                                       uint32_t* __restrict__ w, size_t count,
+                                                                       int ywidth, int Lw, int b, int wout, int G,
+                                                                       int nseg) {
+    constexpr int NP = 2 * B - 1, CK = 16;
+    extern __shared__ uint32_t sm[];
+    uint32_t* Y = sm;                                   // [NP][ywidth][G]
+    uint32_t* CO = Y + (size_t)NP * ywidth * G;         // [nseg][G]
+    uint32_t* L0 = CO + nseg * G;
+    uint32_t* ON = L0 + nseg * G;
+    uint32_t* CI = ON + nseg * G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t c0 = (size_t)blockIdx.x * G;
+    const int nin = (int)min((size_t)G, count - c0);
+    const size_t S = (size_t)NP * count;
+    // ---- phase 0
+    {
+        const int total = NP * ywidth * G;
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int g = idx % G;
+            const int row = idx / G;                    // k * ywidth + t
+            const int k = row / ywidth, t = row - k * ywidth;
+            if (g < nin) cp_async4(Y + idx, P1 + (size_t)t * S + (size_t)k * count + c0 + g);
+            else Y[idx] = 0u;
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const bool act = lane < G;
+    // ---- phase 1: rows 1..NP-2, in place
+    {
+        const int j = warp;
+        const bool rw = act && j >= 1 && j <= NP - 2;
+        tg_rowstate st{0, 0, 0};
+        for (int t0 = 0; t0 <= Lw; t0 += CK) {
+            uint32_t ob[CK];
+            if (rw) {
+#pragma unroll
+                for (int tt = 0; tt < CK; ++tt) {
+                    const int t = t0 + tt;
+                    ob[tt] = 0;
+                    if (t <= Lw) {
+                        uint32_t y[NP];
+#pragma unroll
+                        for (int k = 0; k < NP; ++k) y[k] = Y[(k * ywidth + t) * G + lane];
+                        ob[tt] = rowstep<B>(j, y, st);
+                    }
+                }
+            }
+            __syncthreads();
+            if (rw) {
+#pragma unroll
+                for (int tt = 0; tt < CK; ++tt) {
+                    const int t = t0 + tt;
+                    if (t >= 1 && t <= Lw) Y[(j * ywidth + t - 1) * G + lane] = ob[tt];
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // ---- phase 2: recomposition (every w_j >= 0 at the top level)
+    auto wl = [&](int j, int t) -> uint32_t { return Y[(j * ywidth + t) * G + lane]; };
+    auto seg_sum = [&](int s, int r) -> uint64_t {
+        uint64_t x = 0;
+        if (s < NP) x += wl(s, r);
+        if (s >= 1 && s - 1 < NP) x += wl(s - 1, b + r);
+        if (r == 0 && s >= 2 && s - 2 < NP) x += wl(s - 2, 2 * b);
+        return x;
+    };
+    if (act) {
+        for (int s = warp; s < nseg; s += NP) {
+            const int len = min(b, wout - s * b);
+            uint64_t carry = 0;
+            uint32_t ones = 0xFFFFFFFFu, l0 = 0;
+            for (int r = 0; r < len; ++r) {
+                const uint64_t y = carry + seg_sum(s, r);
+                const uint32_t lo = (uint32_t)y;
+                if (r == 0) l0 = lo; else ones &= lo;
+                carry = y >> 32;
+            }
+            CO[s * G + lane] = (uint32_t)carry;
+            L0[s * G + lane] = l0;
+            ON[s * G + lane] = ones == 0xFFFFFFFFu;
+        }
+    }
+    __syncthreads();
+    if (act && warp == 0) {
+        uint32_t cin = 0;
+        for (int s = 0; s < nseg; ++s) {
+            CI[s * G + lane] = cin;
+            uint32_t cout = CO[s * G + lane];
+            if (cin) {
+                const uint32_t l0 = L0[s * G + lane];
+                if (l0 + cin < l0 && ON[s * G + lane]) cout += 1;
+            }
+            cin = cout;
+        }
+    }
+    __syncthreads();
+    if (act && lane < nin) {
+        uint32_t* row = w + (c0 + lane) * (size_t)wout;
+        for (int s = warp; s < nseg; s += NP) {
+            const int len = min(b, wout - s * b);
+            uint64_t carry = CI[s * G + lane];
+            int r = 0;
+            if (((s * b) & 3) == 0 && (wout & 3) == 0) {
+                for (; r + 4 <= len; r += 4) {
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t y = carry + seg_sum(s, r + q);
+                        o[q] = (uint32_t)y;
+                        carry = y >> 32;
+                    }
+                    *reinterpret_cast<uint4*>(row + s * b + r) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
+            }
+            for (; r < len; ++r) {
+                const uint64_t y = carry + seg_sum(s, r);
+                row[s * b + r] = (uint32_t)y;
+                carry = y >> 32;
+            }
+        }
+    }
+}
+
+}  // namespace tg

@@ -732,6 +732,20 @@ def emit_row_tables(ps: PointSet) -> str:
     L.append(f"TG_CONST unsigned tg_rowO_{ps.name}[{NP}] = {{" + ", ".join(f"{x}u" for x in O) + "};")
     L.append(f"TG_CONST unsigned tg_rowInv_{ps.name}[{NP}] = {{" + ", ".join(f"0x{x:08X}u" for x in INV) + "};")
     L.append(f"TG_CONST int tg_rowS_{ps.name}[{NP}] = {{" + ", ".join(str(x) for x in S) + "};")
+    # combined form over a common denominator Dc = lcm_j D_j (PAPER.md:162
+    # matrix form + Eq. 1.3): Dc w = sum_j 2^(32 b j) sum_k (Dc/D_j) A[j][k] y_k
+    Ds = [O[j] << S[j] for j in range(NP)]
+    Dc = reduce(_lcm, Ds, 1)
+    sc = (Dc & -Dc).bit_length() - 1
+    oc = Dc >> sc
+    assert oc < (1 << 32) and sc < 32
+    L.append(f"TG_CONST long long tg_combA_{ps.name}[{NP}][{NP}] = {{")
+    for j in range(NP):
+        L.append("  {" + ", ".join(str(A[j][k] * (Dc // Ds[j])) for k in range(NP)) + "},")
+    L.append("};")
+    L.append(f"constexpr unsigned tg_combO_{ps.name} = {oc}u;")
+    L.append(f"constexpr unsigned tg_combInv_{ps.name} = 0x{_inv32(oc):08X}u;")
+    L.append(f"constexpr int tg_combS_{ps.name} = {sc};")
     return "\n".join(L)
 
 
