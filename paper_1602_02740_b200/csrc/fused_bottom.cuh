@@ -204,7 +204,12 @@ __host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nse
     return (size_t)4 * ((size_t)NP * 2 * E * 32 + wreg + 4 * 32 * (size_t)nseg);
 }
 
-template <int B, int E, bool TOP>
+// MODE: 0 = parents interleaved [n][count], signed (a lower level of a batch);
+//       1 = parents row-major [count][n], unsigned (the top level);
+//       2 = parents row-major [count][n], signed (below a long-vector level).
+// Output products: interleaved [2n][count] for MODE 0, row-major [count][2n]
+// otherwise.
+template <int B, int E, int MODE>
 __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
     const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV, uint32_t* __restrict__ out,
     size_t count, int n, int b, int Lw, int wout, int nseg) {
@@ -236,9 +241,13 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
         // rows t of block j: source limb j*b + t when t < len_j; all loads of
         // a warp are issued before its stores (compile-time trip count)
         uint32_t fu = 0, fv = 0;
-        if (!TOP && lane < nin) {
+        if (MODE == 0 && lane < nin) {
             fu = (__ldg(srcU + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
             fv = (__ldg(srcV + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
+        }
+        if (MODE == 2 && lane < nin) {
+            fu = (__ldg(srcU + (c0 + lane) * (size_t)n + n - 1) >> 31) ? 0xFFFFFFFFu : 0u;
+            fv = (__ldg(srcV + (c0 + lane) * (size_t)n + n - 1) >> 31) ? 0xFFFFFFFFu : 0u;
         }
         constexpr int ROWS = B * E, ITER = (ROWS + NP - 1) / NP;
         uint32_t xu[ITER], xv[ITER];
@@ -252,7 +261,7 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
             xv[q] = 0;
             if (r < ROWS && lane < nin) {
                 if (t < len) {
-                    if (TOP) {
+                    if (MODE != 0) {
                         xu[q] = __ldg(srcU + (c0 + lane) * (size_t)n + limb);
                         xv[q] = __ldg(srcV + (c0 + lane) * (size_t)n + limb);
                     } else {
@@ -378,11 +387,11 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
                 cin = (y < x) ? 1u : 0u;
                 OUT[(P0 + r) * G + lane] = y;
             }
-            if (!TOP)
+            if (MODE == 0)
                 for (int r = 0; r < len; ++r) out[(size_t)(P0 + r) * count + c] = OUT[(P0 + r) * G + lane];
         }
     }
-    if (TOP) {
+    if (MODE != 0) {
         __syncthreads();
         // coalesced row-major copy: w[c0 + i][P]
         const size_t c0 = (size_t)blockIdx.x * G;

@@ -33,7 +33,7 @@ namespace tg {
 
 constexpr int LV_MAXT = 40;     // terms per op
 constexpr int LV_NT = 256;      // threads per tile
-constexpr int LV_CH = 16;       // limbs per thread
+constexpr int LV_CH = 16;       // limbs per thread (long vectors; 4 for short ones)
 constexpr int LV_TL = LV_NT * LV_CH;
 constexpr int LV_MAXHALO = 8;   // look-ahead limbs of the final right shift (shr < 32*7)
 
@@ -47,7 +47,7 @@ struct LTermDev {
     long long m;                // multiplier
 };
 
-struct LOpDev {
+struct __align__(16) LOpDev {
     uint32_t* dst;
     long long dst_inst_stride, dst_limb_stride;
     int W;                      // output limbs
@@ -58,6 +58,7 @@ struct LOpDev {
     int sa, sr;                 // final right shift shr = 32 sa + sr
     int tiles_per_inst;
     int nthreads;               // threads per tile (multiple of 32, <= LV_NT)
+    int ch;                     // limbs per thread (4 or 16)
     int count;
     int wide;                   // 128-bit accumulators
     LTermDev t[LV_MAXT];
@@ -151,17 +152,25 @@ __device__ __forceinline__ uint32_t lv_slice(const LTermDev& T, const uint32_t* 
     return __ldg(src + (long long)i * T.limb_stride);
 }
 
-// accumulate sum_i m_i * limb_p(S_i << s_i) for positions p0 .. p0+N-1
+// accumulate sum_i m_i * limb_p(S_i << s_i) for positions p0 .. p0+N-1.
+// A term whose slice starts above the chunk contributes nothing; one whose
+// slice ended below it contributes the constant m * fill per limb.
 template <typename Acc, int N>
 __device__ __forceinline__ void lv_lincomb(const LOpDev& op, int nt, long long inst, int p0, Acc (&lin)[N]) {
+    Acc cst = 0;
 #pragma unroll
     for (int q = 0; q < N; ++q) lin[q] = 0;
     for (int k = 0; k < nt; ++k) {
         const LTermDev& T = op.t[k];
+        const int i0 = p0 - T.a;
+        if (i0 + N - 1 < 0) continue;
         const uint32_t* src = T.base + inst * T.inst_stride;
         uint32_t fill = 0;
         if (T.sign && T.len > 0) fill = (__ldg(src + (long long)(T.len - 1) * T.limb_stride) >> 31) ? 0xFFFFFFFFu : 0u;
-        const int i0 = p0 - T.a;
+        if (i0 - 1 >= T.len) {
+            cst += (Acc)T.m * (Acc)fill;
+            continue;
+        }
         uint32_t v[N + 1];
 #pragma unroll
         for (int q = 0; q <= N; ++q) v[q] = lv_slice(T, src, i0 - 1 + q, fill);
@@ -172,39 +181,49 @@ __device__ __forceinline__ void lv_lincomb(const LOpDev& op, int nt, long long i
             lin[q] += (Acc)m * (Acc)x;
         }
     }
+#pragma unroll
+    for (int q = 0; q < N; ++q) lin[q] += cst;
 }
 
-template <bool WIDE>
+template <bool WIDE, int CH>
 __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ opp, LStatus* __restrict__ status,
                                                    unsigned epoch, unsigned* __restrict__ tile_ctr) {
     using Acc = typename std::conditional<WIDE, __int128, long long>::type;
-    const LOpDev& op = *opp;
+    // the op descriptor (terms included) is cached in shared memory
+    __shared__ __align__(16) LOpDev s_op;
+    {
+        const int4* srcd = reinterpret_cast<const int4*>(opp);
+        int4* dstd = reinterpret_cast<int4*>(&s_op);
+        constexpr int NQ = (int)(sizeof(LOpDev) / 16);
+        for (int i = threadIdx.x; i < NQ; i += blockDim.x) dstd[i] = __ldg(srcd + i);
+    }
+    const LOpDev& op = s_op;
     __shared__ unsigned s_tile;
     __shared__ LAgg s_wagg[LV_NT / 32];
     __shared__ long long s_c;
     __shared__ unsigned s_beta;
-    __shared__ uint32_t Q[LV_TL + LV_MAXHALO + 1];
+    extern __shared__ uint32_t Q[];               // [NT * CH + halo] quotient limbs
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int NT = blockDim.x, NW = NT >> 5, TL = NT * LV_CH;   // NT: a multiple of 32, <= LV_NT
+    const int NT = blockDim.x, NW = NT >> 5, TL = NT * CH;   // NT: a multiple of 32, <= LV_NT
     if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
     const long long inst = tile / op.tiles_per_inst;
     const int k = (int)(tile - inst * op.tiles_per_inst);
     const int tstart = k * TL;
-    const int p0 = tstart + tid * LV_CH;
+    const int p0 = tstart + tid * CH;
     const uint32_t o = op.o;
     const LMod M{op.o, op.orcp};
     const int nt = op.nt;
 
-    Acc lin[LV_CH];
-    lv_lincomb<Acc, LV_CH>(op, nt, inst, p0, lin);
+    Acc lin[CH];
+    lv_lincomb<Acc, CH>(op, nt, inst, p0, lin);
 
     // local normalisation (carry-in 0) -> thread aggregate
-    uint32_t x[LV_CH];
+    uint32_t x[CH];
     long long c = 0;
 #pragma unroll
-    for (int q = 0; q < LV_CH; ++q) {
+    for (int q = 0; q < CH; ++q) {
         const Acc v = lin[q] + (Acc)c;
         x[q] = (uint32_t)v;
         c = (long long)(v >> 32);
@@ -214,7 +233,7 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
         const unsigned long long L64 = (unsigned long long)x[0] | ((unsigned long long)x[1] << 32);
         bool tz = true, to = true;
 #pragma unroll
-        for (int q = 2; q < LV_CH; ++q) { tz &= (x[q] == 0u); to &= (x[q] == 0xFFFFFFFFu); }
+        for (int q = 2; q < CH; ++q) { tz &= (x[q] == 0u); to &= (x[q] == 0xFFFFFFFFu); }
         A.lo = (tz && L64 <= 0x8000000000000000ull) ? (long long)(0ull - L64) : LLONG_MIN;
         const unsigned long long comp = 0ull - L64;   // 2^64 - L64
         A.hi = (to && L64 != 0 && comp <= (unsigned long long)LLONG_MAX) ? (long long)comp : LLONG_MAX;
@@ -224,7 +243,7 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
         if (o > 1) {
             uint32_t r = 0;
 #pragma unroll
-            for (int q = LV_CH - 1; q >= 0; --q) r = lv_mod((unsigned long long)r * op.p32 + x[q], M);
+            for (int q = CH - 1; q >= 0; --q) r = lv_mod((unsigned long long)r * op.p32 + x[q], M);
             A.m = op.mi;
 #pragma unroll
             for (int p = 0; p < 3; ++p) {
@@ -348,12 +367,12 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
     c = cin;
     uint32_t beta = bin;
 #pragma unroll
-    for (int q = 0; q < LV_CH; ++q) {
+    for (int q = 0; q < CH; ++q) {
         const Acc v = lin[q] + (Acc)c;
         uint32_t xq = (uint32_t)v;
         c = (long long)(v >> 32);
         if (o > 1) xq = tg_divexact_step(xq, beta, op.oinv, o);
-        Q[tid * LV_CH + q] = xq;
+        Q[tid * CH + q] = xq;
     }
     const int halo = op.sa + (op.sr ? 1 : 0);
     if (tid == NT - 1 && halo > 0) {
@@ -430,24 +449,28 @@ struct LOpBuilder {
         op.count = count;
         op.o = o;
         op.oinv = host_inv32(o);
+        // limbs per thread: 16 for long vectors, 4 for short ones; tile size:
+        // the fewest padded limbs, then the largest tile
+        op.ch = W > 4096 ? 16 : 4;
+        // the largest tile that pads the vector by at most 1/8 (else the least padding)
+        int best = LV_NT;
+        long long bestw = -1;
+        for (int nt = LV_NT; nt >= 32; nt -= 32) {
+            const long long tl = (long long)nt * op.ch, tiles = (W + tl - 1) / tl;
+            const long long pad = tiles * tl;
+            if (pad * 8 <= (long long)W * 9) { best = nt; bestw = pad; break; }
+            if (bestw < 0 || pad < bestw) { bestw = pad; best = nt; }
+        }
+        op.nthreads = best;
+        op.tiles_per_inst = (W + best * op.ch - 1) / (best * op.ch);
         if (o > 1) {
             op.orcp = ~0ull / o;   // floor((2^64 - 1) / o) == floor(2^64 / o) for odd o > 1
             op.p32 = host_powmod(2, 32, o);
-            op.Mch = host_powmod(2, 32ull * LV_CH, o);
+            op.Mch = host_powmod(2, 32ull * op.ch, o);
             op.mi = host_invmod(op.Mch, o);
         }
         op.sa = shr / 32;
         op.sr = shr % 32;
-        // tile size: the fewest padded limbs, then the largest tile
-        int best = LV_NT;
-        long long bestw = -1;
-        for (int nt = LV_NT; nt >= 64; nt -= 32) {
-            const long long tl = (long long)nt * LV_CH, tiles = (W + tl - 1) / tl;
-            const long long pad = tiles * tl;
-            if (bestw < 0 || pad < bestw) { bestw = pad; best = nt; }
-        }
-        op.nthreads = best;
-        op.tiles_per_inst = (W + best * LV_CH - 1) / (best * LV_CH);
     }
     // term m * (slice << s), slice = limbs [start, start+len) of v (len clipped to v.len)
     bool add(const LVec& v, long long m, long long s, int start = 0, int len = -1, int sign = -1) {

@@ -395,6 +395,11 @@ struct Plan {
     // long-vector levels: slot pool, scan status, tile counters, op descriptors
     size_t offSlots = 0, offStatus = 0, offCtr = 0, offDesc = 0;
     size_t nStatus = 0, nCtr = 0, nDesc = 0;
+    // boundary long level (its children feed an instance-parallel level):
+    // row-major staging of its children / their products, transposed to and
+    // from the interleaved layout of the level below
+    int bnd = -1;
+    size_t offT = 0;
 };
 
 // generated long-vector tables of a point set
@@ -422,7 +427,7 @@ static int long_Wt(const Level& L) {
     long_tables(L.B, T);
     return L.Lw + T.lag;
 }
-static size_t long_tiles(size_t count, int W) { return count * (size_t)((W + 64 * LV_CH - 1) / (64 * LV_CH)); }
+static size_t long_tiles(size_t count, int W) { return count * (size_t)((W + 32 * 4 - 1) / (32 * 4)); }
 
 // base widths with a fused bottom-level instantiation (C1 33, C2 18, C3/C4/C5 23, ...)
 static bool fused_E_supported(int E) {
@@ -492,6 +497,10 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
     }
     // fused bottom level?
     plan.fused = false;
+    auto fusable = [&](const Level& Bt) {
+        return (Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
+               2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e;
+    };
     if (plan.lv.size() >= 2 && !g_disable_fused && !plan.lv[plan.lv.size() - 2].lng) {
         const Level& Bt = plan.lv[plan.lv.size() - 2];
         if ((Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
@@ -520,6 +529,17 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         slot_limbs = std::max(slot_limbs, (size_t)T.nslots * L.count * Wt);
         tiles = std::max(tiles, long_tiles(L.count, std::max(std::max(Wt, L.e), 2 * L.n)));
         nops += 2 * (size_t)T.neo + T.nio + 1;
+    }
+    {
+        size_t Tl = 0;
+        while (Tl + 1 < plan.lv.size() && plan.lv[Tl].lng) ++Tl;
+        const size_t nTL = plan.lv.size() - 1;
+        if (Tl >= 1 && Tl < nstaged) {   // level Tl is a staged instance-parallel Toom level
+            const Level& L = plan.lv[Tl - 1];
+            plan.bnd = (int)(Tl - 1);
+            plan.offT = take((size_t)2 * L.e * L.count * L.npts);
+        }
+        (void)nTL;
     }
     if (nops) {
         plan.offSlots = take(slot_limbs);
@@ -652,7 +672,7 @@ static toom_status launch_base(int E, const uint32_t* U, const uint32_t* V, uint
     return TOOM_OK;
 }
 
-template <int B, int E, bool TOP>
+template <int B, int E, int TOP>
 static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out, cudaStream_t st) {
     const int nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
     const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg, Lv.n);
@@ -667,14 +687,16 @@ static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* 
                                                                     2 * Lv.n, nseg);
 }
 
-static toom_status launch_fused(const Level& Lv, bool top, const uint32_t* su, const uint32_t* sv, uint32_t* out,
+// mode: 0 interleaved signed parents, 1 row-major unsigned (top), 2 row-major signed
+static toom_status launch_fused(const Level& Lv, int mode, const uint32_t* su, const uint32_t* sv, uint32_t* out,
                                 cudaStream_t st) {
     if (Lv.count == 0) return TOOM_OK;
     ProfScope ps(CAT_BASE, st);
 #define TG_F(BB, EE)                                                      \
     if (Lv.B == BB && Lv.e == EE) {                                       \
-        if (top) launch_fused_t<BB, EE, true>(Lv, su, sv, out, st);       \
-        else launch_fused_t<BB, EE, false>(Lv, su, sv, out, st);          \
+        if (mode == 1) launch_fused_t<BB, EE, 1>(Lv, su, sv, out, st);    \
+        else if (mode == 2) launch_fused_t<BB, EE, 2>(Lv, su, sv, out, st); \
+        else launch_fused_t<BB, EE, 0>(Lv, su, sv, out, st);              \
         ps.done(st);                                                      \
         ++t_launches;                                                     \
         return TOOM_OK;                                                   \
@@ -787,6 +809,27 @@ __global__ void k_transpose_out(const uint32_t* __restrict__ src, uint32_t* __re
     dst[gid] = src[(size_t)i * count + c];
 }
 
+// out[c][r] = in[r][c] for an R x C row-major matrix (32 x 32 smem tiles)
+__global__ void k_transpose(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, size_t R, size_t C) {
+    __shared__ uint32_t tile[32][33];
+    const size_t r0 = (size_t)blockIdx.y * 32, c0 = (size_t)blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const size_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < R && c < C) tile[i][threadIdx.x] = in[r * C + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const size_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < R && c < C) out[c * R + r] = tile[threadIdx.x][i];
+    }
+}
+
+static void launch_transpose(const uint32_t* in, uint32_t* out, size_t R, size_t C, cudaStream_t st) {
+    dim3 grid((unsigned)((C + 31) / 32), (unsigned)((R + 31) / 32));
+    k_transpose<<<grid, dim3(32, 8), 0, st>>>(in, out, R, C);
+    ++t_launches;
+}
+
 // ------------------------------------------------------------------------
 // long-vector levels: op descriptors for one call (down: evaluation of both
 // operands at every point; up: the interpolation program, then the
@@ -799,8 +842,14 @@ struct LongCall {
 // layout of level l's child operand / product families
 static LVec child_vec(const Plan& plan, size_t l, const uint8_t* ws, size_t off, int width, int k) {
     const Level& L = plan.lv[l];
-    const bool next_long = (l + 1 < plan.lv.size() - 1) && plan.lv[l + 1].lng &&
-                           !(plan.fused && l + 1 == plan.lv.size() - 2);
+    if ((int)l == plan.bnd) {   // row-major staging, transposed to/from the level below
+        size_t o = plan.offT;
+        if (off == L.offV) o += (size_t)L.e * L.count * L.npts * 4;
+        const uint32_t* base = (const uint32_t*)(ws + o);
+        return LVec{base + (size_t)k * L.count * width, width, 1, width, 1};
+    }
+    const bool next_fused = plan.fused && l + 1 == plan.lv.size() - 2;
+    const bool next_long = (l + 1 < plan.lv.size() - 1) && (plan.lv[l + 1].lng || next_fused);
     const uint32_t* base = (const uint32_t*)(ws + off);
     if (next_long)   // row-major [npts*count][width], child k*count + c
         return LVec{base + (size_t)k * L.count * width, width, 1, width, 1};
@@ -832,11 +881,26 @@ static void long_eval_ops(const Level& L, const LVec& par, ChildF child, std::ve
 // interpolation program (steps a4) over the slot pool, then the
 // recomposition w = sum_j w_j 2^(32 b j) (Eq. 1.3, step a5) into dst
 // (row-major [count][2n], two's complement)
+static bool g_long_comb = true;   // T3/T4 long levels: one combined interp+recompose op
+
 template <class YF>
 static void long_interp_ops(const Level& L, YF yv, uint32_t* slots, uint32_t* dst, std::vector<LOpDev>& out) {
     LongTables T;
     long_tables(L.B, T);
     const int cnt = (int)L.count;
+    if (g_long_comb && (L.B == 3 || L.B == 4) && L.Lw == 2 * L.b + 1) {
+        // Dc w = sum_j 2^(32 b j) sum_k A'_jk y_k, then / Dc (Eq. 1.3)
+        const long long* A = L.B == 3 ? &tg_lcomb_T3[0][0] : &tg_lcomb_T4[0][0];
+        const uint32_t o = L.B == 3 ? tg_lcombO_T3 : tg_lcombO_T4;
+        const int sh = L.B == 3 ? tg_lcombS_T3 : tg_lcombS_T4;
+        LOpBuilder b(dst, 2 * L.n, 1, 2 * L.n, cnt, o, sh);
+        for (int j = 0; j < L.npts; ++j)
+            for (int k = 0; k < L.npts; ++k)
+                if (A[j * L.npts + k]) b.add(yv(k), A[j * L.npts + k], 32ll * L.b * j);
+        b.op.wide = 0;
+        out.push_back(b.op);
+        return;
+    }
     const int Wt = long_Wt(L);
     auto slot_vec = [&](int sl) { return LVec{slots + (size_t)sl * cnt * Wt, Wt, 1, Wt, 0}; };
     for (int i = 0; i < T.nio; ++i) {
@@ -915,8 +979,16 @@ static toom_status launch_long_ops(const std::vector<LOpDev>& ops, size_t first,
         const unsigned grid = (unsigned)((size_t)o.count * o.tiles_per_inst);
         if (grid == 0) continue;
         ProfScope ps(cat, st);
-        if (o.wide) k_long_op<true><<<grid, o.nthreads, 0, st>>>(ddesc + first + i, status, epoch, ctr + first + i);
-        else k_long_op<false><<<grid, o.nthreads, 0, st>>>(ddesc + first + i, status, epoch, ctr + first + i);
+        const LOpDev* d = ddesc + first + i;
+        unsigned* cp = ctr + first + i;
+        const size_t qs = ((size_t)o.nthreads * o.ch + LV_MAXHALO + 1) * 4;
+        if (o.ch == 16) {
+            if (o.wide) k_long_op<true, 16><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
+            else k_long_op<false, 16><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
+        } else {
+            if (o.wide) k_long_op<true, 4><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
+            else k_long_op<false, 4><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
+        }
         ps.done(st);
         ++epoch;
         ++t_launches;
@@ -950,6 +1022,14 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         if (lc.down.size() + lc.up.size() > plan.nDesc) return TOOM_EINVAL;
         if ((s = long_prepare(lc.down, lc.up, ddesc, status, plan.nStatus, ctr, plan.nCtr, st))) return s;
         if ((s = launch_long_ops(lc.down, 0, ddesc, status, ctr, epoch, CAT_EVAL, st))) return s;
+        if (plan.bnd >= 0) {   // row-major children -> interleaved [e][npts*count]
+            const Level& Lb = plan.lv[plan.bnd];
+            const size_t cc = Lb.count * Lb.npts;
+            ProfScope ps(CAT_OTHER, st);
+            launch_transpose((const uint32_t*)(ws + plan.offT), (uint32_t*)(ws + Lb.offU), cc, Lb.e, st);
+            launch_transpose((const uint32_t*)(ws + plan.offT) + cc * Lb.e, (uint32_t*)(ws + Lb.offV), cc, Lb.e, st);
+            ps.done(st);
+        }
     }
     if (L == 0) {
         // schoolbook only (n <= 64): the base kernel multiplies signed
@@ -987,7 +1067,8 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         const uint32_t* su = top ? u : (const uint32_t*)(ws + plan.lv[L - 2].offU);
         const uint32_t* sv = top ? v : (const uint32_t*)(ws + plan.lv[L - 2].offV);
         uint32_t* out = top ? w : (uint32_t*)(ws + plan.lv[L - 2].offP);
-        if ((s = launch_fused(Lv, top, su, sv, out, st))) return s;
+        const int mode = top ? 1 : (plan.lv[L - 2].lng ? 2 : 0);   // a long parent level writes row-major children
+        if ((s = launch_fused(Lv, mode, su, sv, out, st))) return s;
     } else {
         const Level& Lv = plan.lv[L - 1];
         if ((s = launch_base(Lv.e, (const uint32_t*)(ws + Lv.offU), (const uint32_t*)(ws + Lv.offV),
@@ -1007,6 +1088,13 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             return s;
     }
     if (Tl) {
+        if (plan.bnd >= 0) {   // interleaved products [2e][npts*count] -> row-major
+            const Level& Lb = plan.lv[plan.bnd];
+            const size_t cc = Lb.count * Lb.npts;
+            ProfScope ps(CAT_OTHER, st);
+            launch_transpose((const uint32_t*)(ws + Lb.offP), (uint32_t*)(ws + plan.offT), 2 * Lb.e, cc, st);
+            ps.done(st);
+        }
         if ((s = launch_long_ops(lc.up, lc.down.size(), ddesc, status, ctr, epoch, CAT_INTERP, st))) return s;
     }
     return TOOM_OK;

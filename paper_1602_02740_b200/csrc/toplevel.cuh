@@ -369,15 +369,33 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     const size_t c0 = (size_t)blockIdx.x * G;
     const int nin = (int)min((size_t)G, count - c0);
     const size_t S = (size_t)NP * count;
-    // ---- phase 0
+    // ---- phase 0: rows (k, t) of G contiguous words, 16-byte copies when aligned
     {
-        const int total = NP * ywidth * G;
-        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-            const int g = idx % G;
-            const int row = idx / G;                    // k * ywidth + t
-            const int k = row / ywidth, t = row - k * ywidth;
-            if (g < nin) cp_async4(Y + idx, P1 + (size_t)t * S + (size_t)k * count + c0 + g);
-            else Y[idx] = 0u;
+        const int nw = blockDim.x >> 5;
+        const bool v16 = ((count & 3) == 0) && ((G & 3) == 0);
+        const int q4 = G >> 2;
+        for (int k = 0; k < NP; ++k) {
+            const uint32_t* src = P1 + (size_t)k * count + c0;
+            uint32_t* dst = Y + (size_t)k * ywidth * G;
+            for (int t = warp; t < ywidth; t += nw) {
+                const uint32_t* sr = src + (size_t)t * S;
+                uint32_t* dr = dst + t * G;
+                if (v16) {
+                    if (lane < q4) {
+                        const int g = lane * 4;
+                        if (g + 3 < nin) {
+                            const unsigned d = (unsigned)__cvta_generic_to_shared(dr + g);
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(sr + g));
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) dr[g + q] = (g + q < nin) ? __ldg(sr + g + q) : 0u;
+                        }
+                    }
+                } else if (lane < G) {
+                    if (lane < nin) cp_async4(dr + lane, sr + lane);
+                    else dr[lane] = 0u;
+                }
+            }
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     }
@@ -414,22 +432,31 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
             __syncthreads();
         }
     }
-    // ---- phase 2: recomposition (every w_j >= 0 at the top level)
-    auto wl = [&](int j, int t) -> uint32_t { return Y[(j * ywidth + t) * G + lane]; };
-    auto seg_sum = [&](int s, int r) -> uint64_t {
-        uint64_t x = 0;
-        if (s < NP) x += wl(s, r);
-        if (s >= 1 && s - 1 < NP) x += wl(s - 1, b + r);
-        if (r == 0 && s >= 2 && s - 2 < NP) x += wl(s - 2, 2 * b);
-        return x;
+    // ---- phase 2: recomposition (every w_j >= 0 at the top level).  Segment
+    // s limb r = w_s[r] + w_{s-1}[b + r] (+ w_{s-2}[2b] at r = 0); absent rows
+    // read a zero row of shared memory.
+    __shared__ uint32_t zrow[32];
+    if (threadIdx.x < 32) zrow[threadIdx.x] = 0u;
+    __syncthreads();
+    auto rowA = [&](int s) -> const uint32_t* { return s < NP ? Y + (size_t)(s * ywidth) * G + lane : nullptr; };
+    auto rowB = [&](int s) -> const uint32_t* {
+        return (s >= 1 && s - 1 < NP) ? Y + (size_t)((s - 1) * ywidth + b) * G + lane : nullptr;
+    };
+    auto extraC = [&](int s) -> uint32_t {
+        return (s >= 2 && s - 2 < NP) ? Y[(size_t)((s - 2) * ywidth + 2 * b) * G + lane] : 0u;
     };
     if (act) {
         for (int s = warp; s < nseg; s += NP) {
             const int len = min(b, wout - s * b);
-            uint64_t carry = 0;
+            const uint32_t* pa = rowA(s);
+            const uint32_t* pb = rowB(s);
+            const int sa = pa ? G : 0, sb = pb ? G : 0;
+            if (!pa) pa = zrow + lane;
+            if (!pb) pb = zrow + lane;
+            uint64_t carry = extraC(s);
             uint32_t ones = 0xFFFFFFFFu, l0 = 0;
             for (int r = 0; r < len; ++r) {
-                const uint64_t y = carry + seg_sum(s, r);
+                const uint64_t y = carry + pa[r * sa] + pb[r * sb];
                 const uint32_t lo = (uint32_t)y;
                 if (r == 0) l0 = lo; else ones &= lo;
                 carry = y >> 32;
@@ -457,14 +484,20 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
         uint32_t* row = w + (c0 + lane) * (size_t)wout;
         for (int s = warp; s < nseg; s += NP) {
             const int len = min(b, wout - s * b);
-            uint64_t carry = CI[s * G + lane];
+            const uint32_t* pa = rowA(s);
+            const uint32_t* pb = rowB(s);
+            const int sa = pa ? G : 0, sb = pb ? G : 0;
+            if (!pa) pa = zrow + lane;
+            if (!pb) pb = zrow + lane;
+            // carry-in of the segment; the w_{s-2}[2b] term enters at r = 0
+            uint64_t carry = (uint64_t)CI[s * G + lane] + extraC(s);
             int r = 0;
             if (((s * b) & 3) == 0 && (wout & 3) == 0) {
                 for (; r + 4 <= len; r += 4) {
                     uint32_t o[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint64_t y = carry + seg_sum(s, r + q);
+                        const uint64_t y = carry + pa[(r + q) * sa] + pb[(r + q) * sb];
                         o[q] = (uint32_t)y;
                         carry = y >> 32;
                     }
@@ -472,7 +505,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
                 }
             }
             for (; r < len; ++r) {
-                const uint64_t y = carry + seg_sum(s, r);
+                const uint64_t y = carry + pa[r * sa] + pb[r * sb];
                 row[s * b + r] = (uint32_t)y;
                 carry = y >> 32;
             }

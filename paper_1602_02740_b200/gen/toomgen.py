@@ -1113,6 +1113,31 @@ def emit_long_tables(ps: PointSet) -> str:
     lines = [f"// long-vector tables for {ps.name} (csrc/longvec.cuh)"]
     nm = ps.name
     lines.append(f"constexpr unsigned long long tg_growthS_{nm} = {_growth_S(ps)}ull;")
+    if ps.B <= 4:
+        # combined interpolation + recomposition over the common denominator
+        # (PAPER.md:162 matrix form, Eq. 1.3): Dc w = sum_j 2^(32 b j) sum_k A'_jk y_k
+        it0 = build_interp(ps)
+        rows = per_output_programs(it0, f"lc_{nm}")
+        NP = ps.npoints
+        A, Ds = [], []
+        for pr in rows:
+            coef = [0] * NP
+            if pr.ops:
+                op = pr.ops[0]
+                for t in op.terms:
+                    coef[pr.inputs.index(t.var)] += t.m << t.s
+                D = op.odiv << op.shr
+            else:
+                coef[pr.inputs.index(pr.outputs[0])] = 1
+                D = 1
+            A.append(coef)
+            Ds.append(D)
+        Dc = reduce(_lcm, Ds, 1)
+        sc = (Dc & -Dc).bit_length() - 1
+        lines.append(f"static const long long tg_lcomb_{nm}[{NP}][{NP}] = {{" +
+                     ", ".join("{" + ", ".join(str(A[j][k] * (Dc // Ds[j])) for k in range(NP)) + "}" for j in range(NP)) + "};")
+        lines.append(f"constexpr unsigned tg_lcombO_{nm} = {Dc >> sc}u;")
+        lines.append(f"constexpr int tg_lcombS_{nm} = {sc};")
     for tag, lp in (("eval", ev), ("interp", it)):
         terms, ops = [], []
         for d, ts, o, shr in lp["ops"]:

@@ -161,6 +161,24 @@ def test_toom_batched_threads_deterministic():
         assert I(w1[i]) == I(u[i]) * I(v[i])
 
 
+@pytest.mark.parametrize("B", [4, 16])
+def test_toom_top_level_threads_eq25(B):
+    """O2 with the 2B-1 top-level products on P host threads (Eq. 2.5,
+    PAPER.md:44-46): identical to CPython's product, identical to P = 1, and
+    the per-depth product counts (Eq. 2.1) are merged from the workers."""
+    rng = random.Random(25 + B)
+    n = 3000
+    u, v = rand_limbs(rng, n), rand_limbs(rng, n)
+    oracle.reset_counters()
+    w8 = oracle.toom(u, v, top_B=B, threads=8)
+    d1 = oracle.products_at_depth(1)
+    oracle.reset_counters()
+    w1 = oracle.toom(u, v, top_B=B, threads=1)
+    assert d1 == oracle.products_at_depth(1) == 2 * B - 1
+    assert np.array_equal(w1, w8)
+    assert I(w8) == I(u) * I(v)
+
+
 # ---------------------------------------------------------------- §3 listings
 
 
