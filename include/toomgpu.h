@@ -144,11 +144,13 @@ double toom_probe_limb_products(double *ms, void *stream);
  * staged launches through HBM; results are identical (tests compare both). */
 void toom_set_fused(int on);
 
-/* Top-level interpolation of batched Toom-3/Toom-4 products: 2 (default) =
- * products of a group of instances staged in shared memory, rows in place,
- * then recomposition (k_interp_top_smem); 1 = one streaming pass per product
- * over the common-denominator matrix form (k_interp_top_stream); 0 = the
- * per-row kernel (k_interp_top_rows).  All are exact; tests compare them. */
+/* Top-level interpolation of batched Toom-3/Toom-4 products: 3 = one warp
+ * per product over the common-denominator matrix form with a warp
+ * carry/borrow scan (k_interp_top_warp; used when the fused level is directly
+ * below, else mode 2); 2 (default) = products of a group of instances staged
+ * in shared memory, rows in place, then recomposition (k_interp_top_smem); 1 = one
+ * streaming pass per product (k_interp_top_stream); 0 = the per-row kernel
+ * (k_interp_top_rows).  All are exact; tests compare them. */
 void toom_set_top_stream(int on);
 
 /* ---- stage exports (tests, bench) ------------------------------------- */

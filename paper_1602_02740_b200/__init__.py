@@ -235,8 +235,9 @@ def set_fused(on: bool = True):
 
 
 def set_top_stream(mode: int = 2):
-    """Top-level interpolation kernel: 2 smem-staged (default), 1 one-pass
-    stream, 0 per-row (all exact)."""
+    """Top-level interpolation kernel: 3 one warp per product (when the fused
+    level is directly below), 2 smem-staged (default), 1 one-pass stream,
+    0 per-row (all exact)."""
     lib().toom_set_top_stream(int(mode))
 
 

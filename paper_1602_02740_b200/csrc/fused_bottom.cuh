@@ -206,7 +206,9 @@ __host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nse
 
 // MODE: 0 = parents interleaved [n][count], signed (a lower level of a batch);
 //       1 = parents row-major [count][n], unsigned (the top level);
-//       2 = parents row-major [count][n], signed (below a long-vector level).
+//       2 = parents row-major [count][n], signed (below a long-vector level);
+//       3 = parents interleaved, signed, products row-major (below a top level
+//           whose interpolation runs one warp per product).
 // Output products: interleaved [2n][count] for MODE 0, row-major [count][2n]
 // otherwise.
 template <int B, int E, int MODE>
@@ -241,7 +243,7 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
         // rows t of block j: source limb j*b + t when t < len_j; all loads of
         // a warp are issued before its stores (compile-time trip count)
         uint32_t fu = 0, fv = 0;
-        if (MODE == 0 && lane < nin) {
+        if ((MODE == 0 || MODE == 3) && lane < nin) {
             fu = (__ldg(srcU + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
             fv = (__ldg(srcV + (size_t)(n - 1) * count + c0 + lane) >> 31) ? 0xFFFFFFFFu : 0u;
         }
@@ -261,7 +263,7 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
             xv[q] = 0;
             if (r < ROWS && lane < nin) {
                 if (t < len) {
-                    if (MODE != 0) {
+                    if (MODE == 1 || MODE == 2) {
                         xu[q] = __ldg(srcU + (c0 + lane) * (size_t)n + limb);
                         xv[q] = __ldg(srcV + (c0 + lane) * (size_t)n + limb);
                     } else {

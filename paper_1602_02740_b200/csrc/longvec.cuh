@@ -185,40 +185,35 @@ __device__ __forceinline__ void lv_lincomb(const LOpDev& op, int nt, long long i
     for (int q = 0; q < N; ++q) lin[q] += cst;
 }
 
-template <bool WIDE, int CH>
-__global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ opp, LStatus* __restrict__ status,
-                                                   unsigned epoch, unsigned* __restrict__ tile_ctr) {
-    using Acc = typename std::conditional<WIDE, __int128, long long>::type;
-    // the op descriptor (terms included) is cached in shared memory
-    __shared__ __align__(16) LOpDev s_op;
-    {
-        const int4* srcd = reinterpret_cast<const int4*>(opp);
-        int4* dstd = reinterpret_cast<int4*>(&s_op);
-        constexpr int NQ = (int)(sizeof(LOpDev) / 16);
-        for (int i = threadIdx.x; i < NQ; i += blockDim.x) dstd[i] = __ldg(srcd + i);
-    }
-    const LOpDev& op = s_op;
-    __shared__ unsigned s_tile;
-    __shared__ LAgg s_wagg[LV_NT / 32];
-    __shared__ long long s_c;
-    __shared__ unsigned s_beta;
-    extern __shared__ uint32_t Q[];               // [NT * CH + halo] quotient limbs
+// Parameters of the carry/borrow scan and the final division + shift + store
+// of one output of one tile (shared by k_long_op and k_long_eval).
+struct LFinish {
+    uint32_t oinv, p32, Mch, mi;
+    int sa, sr, W;
+    LStatus* st_base;          // status of tile j at st_base + j * st_stride
+    int st_stride;
+    uint32_t* dst;             // this instance's output
+    long long dst_limb_stride;
+};
+
+struct LTileSmem {
+    LAgg wagg[LV_NT / 32];
+    long long c;
+    unsigned beta;
+};
+
+// local normalisation of the tile's linear combination, carry / borrow scan
+// (warp shuffles + decoupled look-back), exact limbs, exact division, right
+// shift, coalesced store.  lin: this thread's CH positions p0 = tstart + tid*CH.
+template <typename Acc, int CH, class HaloF>
+__device__ __forceinline__ void lv_finish(const Acc (&lin)[CH], const LMod& M, const LFinish& P, unsigned epoch,
+                                          unsigned tile, int k, int tstart, LTileSmem& sh, uint32_t* Q, HaloF halo_fn) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int NT = blockDim.x, NW = NT >> 5, TL = NT * CH;   // NT: a multiple of 32, <= LV_NT
-    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-    __syncthreads();
-    const unsigned tile = s_tile;
-    const long long inst = tile / op.tiles_per_inst;
-    const int k = (int)(tile - inst * op.tiles_per_inst);
-    const int tstart = k * TL;
-    const int p0 = tstart + tid * CH;
-    const uint32_t o = op.o;
-    const LMod M{op.o, op.orcp};
-    const int nt = op.nt;
-
-    Acc lin[CH];
-    lv_lincomb<Acc, CH>(op, nt, inst, p0, lin);
-
+    const int NT = blockDim.x, NW = NT >> 5, TL = NT * CH;
+    const uint32_t o = M.o;
+    LAgg* s_wagg = sh.wagg;
+    long long& s_c = sh.c;
+    unsigned& s_beta = sh.beta;
     // local normalisation (carry-in 0) -> thread aggregate
     uint32_t x[CH];
     long long c = 0;
@@ -243,13 +238,13 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
         if (o > 1) {
             uint32_t r = 0;
 #pragma unroll
-            for (int q = CH - 1; q >= 0; --q) r = lv_mod((unsigned long long)r * op.p32 + x[q], M);
-            A.m = op.mi;
+            for (int q = CH - 1; q >= 0; --q) r = lv_mod((unsigned long long)r * P.p32 + x[q], M);
+            A.m = P.mi;
 #pragma unroll
             for (int p = 0; p < 3; ++p) {
                 // g[p] = (-Lmod + (p-1) M) * mi mod o
-                unsigned long long t = (unsigned long long)(o - r) + (p == 2 ? op.Mch : 0u) + (p == 0 ? (o - op.Mch) : 0u);
-                A.g[p] = lv_mulmod(lv_mod(t, M), op.mi, M);
+                unsigned long long t = (unsigned long long)(o - r) + (p == 2 ? P.Mch : 0u) + (p == 0 ? (o - P.Mch) : 0u);
+                A.g[p] = lv_mulmod(lv_mod(t, M), P.mi, M);
             }
         } else {
             A.m = 0;
@@ -268,7 +263,7 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
     __syncthreads();
     // tile aggregate, published before the look-back
     const bool first = (k == 0);
-    LStatus* st = status + tile;
+    LStatus* st = P.st_base + (long long)tile * P.st_stride;
     if (warp == 0) {
         LAgg T = s_wagg[0];
         for (int w = 1; w < NW; ++w) T = lv_compose(T, s_wagg[w], M);
@@ -295,7 +290,7 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
                 long long ic = 0;
                 unsigned ib = 0;
                 if (j >= base) {
-                    LStatus* ps = status + j;
+                    LStatus* ps = P.st_base + j * P.st_stride;
                     do { f = *(volatile unsigned*)&ps->flag; } while (f != epoch * 4u + 1u && f != epoch * 4u + 2u);
                     __threadfence();
                     if (f == epoch * 4u + 2u) {
@@ -371,35 +366,235 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
         const Acc v = lin[q] + (Acc)c;
         uint32_t xq = (uint32_t)v;
         c = (long long)(v >> 32);
-        if (o > 1) xq = tg_divexact_step(xq, beta, op.oinv, o);
+        if (o > 1) xq = tg_divexact_step(xq, beta, P.oinv, o);
         Q[tid * CH + q] = xq;
     }
-    const int halo = op.sa + (op.sr ? 1 : 0);
+    const int halo = P.sa + (P.sr ? 1 : 0);
     if (tid == NT - 1 && halo > 0) {
         // quotient limbs just past the tile (the next tile's first limbs),
         // continuing this tile's carry / borrow chain
         Acc hl[LV_MAXHALO];
-        lv_lincomb<Acc, LV_MAXHALO>(op, nt, inst, tstart + TL, hl);
+        halo_fn(hl);
 #pragma unroll
         for (int h = 0; h < LV_MAXHALO; ++h) {
             if (h >= halo) break;
             const Acc v = hl[h] + (Acc)c;
             uint32_t xq = (uint32_t)v;
             c = (long long)(v >> 32);
-            if (o > 1) xq = tg_divexact_step(xq, beta, op.oinv, o);
+            if (o > 1) xq = tg_divexact_step(xq, beta, P.oinv, o);
             Q[TL + h] = xq;
         }
     }
     __syncthreads();
     // right shift, coalesced stores
-    uint32_t* dst = op.dst + inst * op.dst_inst_stride;
+    uint32_t* dst = P.dst;
     for (int i = tid; i < TL; i += NT) {
         const int t = tstart + i;
-        if (t >= op.W) break;
-        const uint32_t lo = Q[i + op.sa];
-        const uint32_t y = op.sr ? __funnelshift_r(lo, Q[i + op.sa + 1], op.sr) : lo;
-        dst[(long long)t * op.dst_limb_stride] = y;
+        if (t >= P.W) break;
+        const uint32_t lo = Q[i + P.sa];
+        const uint32_t y = P.sr ? __funnelshift_r(lo, Q[i + P.sa + 1], P.sr) : lo;
+        dst[(long long)t * P.dst_limb_stride] = y;
     }
+}
+
+template <bool WIDE, int CH>
+__global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ opp, LStatus* __restrict__ status,
+                                                   unsigned epoch, unsigned* __restrict__ tile_ctr) {
+    using Acc = typename std::conditional<WIDE, __int128, long long>::type;
+    // the op descriptor (terms included) is cached in shared memory
+    __shared__ __align__(16) LOpDev s_op;
+    {
+        const int4* srcd = reinterpret_cast<const int4*>(opp);
+        int4* dstd = reinterpret_cast<int4*>(&s_op);
+        constexpr int NQ = (int)(sizeof(LOpDev) / 16);
+        for (int i = threadIdx.x; i < NQ; i += blockDim.x) dstd[i] = __ldg(srcd + i);
+    }
+    const LOpDev& op = s_op;
+    __shared__ unsigned s_tile;
+    __shared__ LTileSmem s_sh;
+    extern __shared__ uint32_t Q[];               // [NT * CH + halo] quotient limbs
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int NT = blockDim.x, NW = NT >> 5, TL = NT * CH;   // NT: a multiple of 32, <= LV_NT
+    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const long long inst = tile / op.tiles_per_inst;
+    const int k = (int)(tile - inst * op.tiles_per_inst);
+    const int tstart = k * TL;
+    const int p0 = tstart + tid * CH;
+    const uint32_t o = op.o;
+    const LMod M{op.o, op.orcp};
+    const int nt = op.nt;
+
+    Acc lin[CH];
+    (void)p0;
+    // the linear combination, one term at a time: the tile's slice of the term
+    // is loaded coalesced into shared memory (position i of the tile at
+    // Sx[(i % CH)][i / CH], row pitch NT + 1: conflict-free reads), then every
+    // thread accumulates its CH positions.  Terms whose slice lies entirely
+    // above the tile are skipped, terms entirely past their slice add m * fill.
+    {
+        uint32_t* Sx = Q + TL + LV_MAXHALO + 1;   // [CH][NT + 1] (+1 row for position -1)
+        const int NP1 = NT + 1;
+        Acc cst = 0;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) lin[q] = 0;
+        for (int kk = 0; kk < nt; ++kk) {
+            const LTermDev& T = op.t[kk];
+            const int ilo = tstart - T.a - 1, ihi = tstart + TL - 1 - T.a;   // slice indices the tile needs
+            if (ihi < 0) continue;
+            const uint32_t* src = T.base + inst * T.inst_stride;
+            uint32_t fill = 0;
+            if (T.sign && T.len > 0) fill = (__ldg(src + (long long)(T.len - 1) * T.limb_stride) >> 31) ? 0xFFFFFFFFu : 0u;
+            if (ilo >= T.len) {
+                cst += (Acc)T.m * (Acc)fill;
+                continue;
+            }
+            __syncthreads();   // previous term's reads done
+            // Sx row CH holds position -1 of each thread's chunk's predecessor:
+            // store slice index ilo + 1 + i at (i % CH, i / CH); index ilo at the extra slot
+            {
+                // positions tid + q*NT (all loads issued before the stores)
+                uint32_t xv[CH];
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const int idx = ilo + 1 + tid + q * NT;
+                    xv[q] = idx < 0 ? 0u : (idx >= T.len ? fill : __ldg(src + (long long)idx * T.limb_stride));
+                }
+                if (tid == 0) {
+                    const int idx = ilo;      // position tstart - 1
+                    Sx[CH * NP1] = idx < 0 ? 0u : (idx >= T.len ? fill : __ldg(src + (long long)idx * T.limb_stride));
+                }
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const int pos = tid + q * NT;
+                    Sx[(pos % CH) * NP1 + pos / CH] = xv[q];
+                }
+            }
+            __syncthreads();
+            const long long m = T.m;
+            const int r = T.r;
+            // previous limb of my chunk's first position
+            uint32_t prev = tid ? Sx[(CH - 1) * NP1 + tid - 1] : Sx[CH * NP1];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const uint32_t cur = Sx[q * NP1 + tid];
+                const uint32_t x = r ? __funnelshift_l(prev, cur, r) : cur;
+                lin[q] += (Acc)m * (Acc)x;
+                prev = cur;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q) lin[q] += cst;
+        __syncthreads();   // Sx / Q reuse below
+    }
+
+    lv_finish<Acc, CH>(lin, M, LFinish{op.oinv, op.p32, op.Mch, op.mi, op.sa, op.sr, op.W, status, 1,
+                                        op.dst + inst * op.dst_inst_stride, op.dst_limb_stride},
+                       epoch, tile, k, tstart, s_sh, Q,
+                       [&](Acc (&hl)[LV_MAXHALO]) { lv_lincomb<Acc, LV_MAXHALO>(op, nt, inst, tstart + TL, hl); });
+}
+
+// ------------------------------------------------------------------------
+// Multi-output op: NO outputs that are linear combinations of the SAME NS
+// source slices, out_o = ((sum_s m[o][s] src_s) / o_o) >> shr_o.  A tile
+// stages its limb range of every source in shared memory once, then runs the
+// carry / borrow scan of every output in turn (status entries tile*NO + o).
+// Serves the evaluation of a long level (sources = the B blocks, outputs =
+// the 2B-1 points, Eq. 1.1-1.2) and its interpolation rows (sources = the
+// 2B-1 products, outputs = the coefficient rows w_j = (sum_k A_jk y_k)/D_j of
+// the even-odd + listing program).
+// ------------------------------------------------------------------------
+constexpr int LM_MAXS = 16, LM_MAXO = 31, LM_HALO = 8;
+
+struct LMSrc {
+    const uint32_t* base;       // slice start of instance 0 (row-major: limb stride 1)
+    long long is;               // limbs between instances
+    int len, sign;
+};
+struct LMOut {
+    uint32_t* dst;              // instance 0
+    unsigned long long orcp;
+    uint32_t o, oinv, p32, Mch, mi;
+    int sa, sr;
+};
+struct __align__(16) LMultiDev {
+    int ns, no, W, tiles_per_inst, nthreads, ch, count, wide;
+    long long dst_is, dst_ls;
+    LMSrc src[LM_MAXS];
+    LMOut out[LM_MAXO];
+    long long m[LM_MAXO][LM_MAXS];
+};
+
+template <bool WIDE, int CH>
+__global__ void __launch_bounds__(LV_NT) k_long_multi(const LMultiDev* __restrict__ dp, LStatus* __restrict__ status,
+                                                      unsigned epoch, unsigned* __restrict__ tile_ctr) {
+    using Acc = typename std::conditional<WIDE, __int128, long long>::type;
+    __shared__ __align__(16) LMultiDev s_d;
+    {
+        const int4* srcd = reinterpret_cast<const int4*>(dp);
+        int4* dstd = reinterpret_cast<int4*>(&s_d);
+        constexpr int NQ = (int)(sizeof(LMultiDev) / 16);
+        for (int i = threadIdx.x; i < NQ; i += blockDim.x) dstd[i] = __ldg(srcd + i);
+    }
+    __shared__ unsigned s_tile;
+    __shared__ LTileSmem s_sh;
+    extern __shared__ uint32_t dsm[];
+    const int tid = threadIdx.x, NT = blockDim.x, TL = NT * CH, NP1 = NT + 1 + (LM_HALO + CH - 1) / CH;
+    uint32_t* Q = dsm;                                  // [TL + halo]
+    uint32_t* Sb = dsm + TL + LV_MAXHALO + 1;           // [ns][CH][NP1]: position i at (i % CH, i / CH)
+    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const LMultiDev& d = s_d;
+    const unsigned tile = s_tile;
+    const long long inst = tile / d.tiles_per_inst;
+    const int kt = (int)(tile - inst * d.tiles_per_inst);
+    const int tstart = kt * TL;
+    // stage positions [tstart, tstart + TL + LM_HALO) of every source
+    for (int sI = 0; sI < d.ns; ++sI) {
+        const LMSrc& S = d.src[sI];
+        const uint32_t* sp = S.base + inst * S.is;
+        uint32_t fill = 0;
+        if (S.sign && S.len > 0) fill = (__ldg(sp + (S.len - 1)) >> 31) ? 0xFFFFFFFFu : 0u;
+        uint32_t* sj = Sb + (size_t)sI * CH * NP1;
+        for (int i = tid; i < TL + LM_HALO; i += NT) {
+            const int t = tstart + i;
+            sj[(i % CH) * NP1 + i / CH] = (t < S.len) ? __ldg(sp + t) : fill;
+        }
+    }
+    __syncthreads();
+    for (int o = 0; o < d.no; ++o) {
+        const LMOut& O = d.out[o];
+        Acc lin[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) lin[q] = 0;
+        for (int sI = 0; sI < d.ns; ++sI) {
+            const long long m = d.m[o][sI];
+            if (m == 0) continue;
+            const uint32_t* sj = Sb + (size_t)sI * CH * NP1 + tid;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) lin[q] += (Acc)m * (Acc)sj[q * NP1];
+        }
+        const LMod M{O.o, O.orcp};
+        lv_finish<Acc, CH>(lin, M, LFinish{O.oinv, O.p32, O.Mch, O.mi, O.sa, O.sr, d.W, status + o, d.no,
+                                           O.dst + inst * d.dst_is, d.dst_ls},
+                           epoch, tile, kt, tstart, s_sh, Q, [&](Acc (&hl)[LV_MAXHALO]) {
+                               // positions TL .. TL + LV_MAXHALO - 1 from the staged halo
+#pragma unroll
+                               for (int h = 0; h < LV_MAXHALO; ++h) {
+                                   Acc v = 0;
+                                   const int i = TL + h;
+                                   for (int s2 = 0; s2 < d.ns; ++s2)
+                                       v += (Acc)d.m[o][s2] * (Acc)Sb[(size_t)s2 * CH * NP1 + (i % CH) * NP1 + i / CH];
+                                   hl[h] = v;
+                               }
+                           });
+    }
+}
+
+inline size_t long_multi_smem(int nthreads, int ch, int ns) {
+    const int np1 = nthreads + 1 + (LM_HALO + ch - 1) / ch;
+    return 4 * ((size_t)nthreads * ch + LV_MAXHALO + 1 + (size_t)ns * ch * np1);
 }
 
 // ------------------------------------------------------------------------
@@ -451,7 +646,7 @@ struct LOpBuilder {
         op.oinv = host_inv32(o);
         // limbs per thread: 16 for long vectors, 4 for short ones; tile size:
         // the fewest padded limbs, then the largest tile
-        op.ch = W > 4096 ? 16 : 4;
+        op.ch = 16;   // the scan costs ~1k instructions per thread: amortise over 16 limbs
         // the largest tile that pads the vector by at most 1/8 (else the least padding)
         int best = LV_NT;
         long long bestw = -1;

@@ -368,8 +368,8 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 
 }  // namespace tg
 #include "fused_bottom.cuh"
-#include "toplevel.cuh"
 #include "longvec.cuh"
+#include "toplevel.cuh"
 namespace tg {
 
 // ------------------------------------------------------------------------
@@ -400,6 +400,8 @@ struct Plan {
     // from the interleaved layout of the level below
     int bnd = -1;
     size_t offT = 0;
+    size_t offEDesc = 0;     // multi-output evaluation descriptors
+    bool top_warp = false;   // top interpolation one warp per product (fused level writes row-major)
 };
 
 // generated long-vector tables of a point set
@@ -453,6 +455,23 @@ static int choose_B(const toom_plan_t& p, int depth, int n) {
     return B;
 }
 
+static int g_top_stream = 2;   // 3: one warp per product, 2: smem kernel, 1: one-pass stream, 0: per-row kernel
+// default long-vector rule: levels whose operands exceed this many limbs
+static int g_long_min_n = [] {
+    const char* e = getenv("TOOM_LONG_MIN_N");
+    return e ? atoi(e) : 2048;
+}();
+
+// one warp per product (k_interp_top_warp) needs the products row-major; CH
+// positions per lane, CH = ceil((2n+1)/32) rounded up to an instantiated size
+static int top_warp_ch(const Level& Lv) {
+    const int need = (2 * Lv.n + 1 + 31) / 32;
+    if (Lv.B != 3 && Lv.B != 4) return 0;
+    for (int c : {9, 17, 33})
+        if (need <= c) return c;
+    return 0;
+}
+
 static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& plan, bool top_long = false) {
     plan.lv.clear();
     size_t count = batch;
@@ -488,7 +507,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         for (size_t l = 0; l + 1 < plan.lv.size(); ++l) {
             Level& L = plan.lv[l];
             const bool want = L.B == 16 || (top_long && l == 0) ||   // T16: no instance-parallel program
-                              (p.long_count == 0 ? (L.n > 2048) : (p.long_count > 1 && L.count < p.long_count));
+                              (p.long_count == 0 ? (L.n > g_long_min_n) : (p.long_count > 1 && L.count < p.long_count));
             if (want && long_tables(L.B, T)) L.lng = true;
             else break;
         }
@@ -497,16 +516,16 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
     }
     // fused bottom level?
     plan.fused = false;
-    auto fusable = [&](const Level& Bt) {
-        return (Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
-               2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e;
-    };
     if (plan.lv.size() >= 2 && !g_disable_fused && !plan.lv[plan.lv.size() - 2].lng) {
         const Level& Bt = plan.lv[plan.lv.size() - 2];
         if ((Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
             2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e)
             plan.fused = true;
     }
+    // a batched top level directly above the fused level: its interpolation
+    // can run one warp per product on row-major products (fused MODE 3)
+    plan.top_warp = plan.fused && plan.lv.size() == 3 && !plan.lv[0].lng && g_top_stream == 3 &&
+                    top_warp_ch(plan.lv[0]) > 0 && plan.lv[0].Lw == 2 * plan.lv[0].b + 1;
     // workspace layout
     size_t off = 0;
     auto take = [&](size_t limbs) { size_t o = off; off += ((limbs * 4 + 255) / 256) * 256; return o; };
@@ -528,7 +547,8 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         const int Wt = long_Wt(L);
         slot_limbs = std::max(slot_limbs, (size_t)T.nslots * L.count * Wt);
         tiles = std::max(tiles, long_tiles(L.count, std::max(std::max(Wt, L.e), 2 * L.n)));
-        nops += 2 * (size_t)T.neo + T.nio + 1;
+        tiles = std::max(tiles, long_tiles(L.count, std::max(L.e, L.Lw)) * (size_t)L.npts);   // multi-output ops
+        nops += 2 * (size_t)T.neo + T.nio + 1 + 2;
     }
     {
         size_t Tl = 0;
@@ -549,6 +569,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         plan.offCtr = take(nops);
         plan.nDesc = nops;
         plan.offDesc = take((nops * sizeof(LOpDev) + 3) / 4);
+        plan.offEDesc = take((nops * sizeof(LMultiDev) + 3) / 4);
     }
     plan.bytes = off;
     return TOOM_OK;
@@ -696,6 +717,7 @@ static toom_status launch_fused(const Level& Lv, int mode, const uint32_t* su, c
     if (Lv.B == BB && Lv.e == EE) {                                       \
         if (mode == 1) launch_fused_t<BB, EE, 1>(Lv, su, sv, out, st);    \
         else if (mode == 2) launch_fused_t<BB, EE, 2>(Lv, su, sv, out, st); \
+        else if (mode == 3) launch_fused_t<BB, EE, 3>(Lv, su, sv, out, st); \
         else launch_fused_t<BB, EE, 0>(Lv, su, sv, out, st);              \
         ps.done(st);                                                      \
         ++t_launches;                                                     \
@@ -740,7 +762,6 @@ static void launch_interp_top_rows_t(const Level& Lv, const uint32_t* P1, uint32
     k_interp_top_rows<B><<<grid, 32 * (2 * B - 1), smem, st>>>(P1, w, Lv.count, 2 * Lv.e, Lv.Lw, Lv.b, 2 * Lv.n, nseg);
 }
 
-static int g_top_stream = 2;   // 2: smem kernel, 1: one-pass stream, 0: per-row kernel
 
 template <int B>
 static bool launch_interp_top_smem_t(const Level& Lv, const uint32_t* P1, uint32_t* w, cudaStream_t st) {
@@ -760,6 +781,35 @@ static bool launch_interp_top_smem_t(const Level& Lv, const uint32_t* P1, uint32
     const unsigned grid = (unsigned)((Lv.count + G - 1) / G);
     k_interp_top_smem<B><<<grid, 32 * NP, smem, st>>>(P1, w, Lv.count, ywidth, Lv.Lw, Lv.b, 2 * Lv.n, G, nseg);
     return true;
+}
+
+template <int B, int CH>
+static void launch_interp_top_warp_t(const Level& Lv, const uint32_t* P1, uint32_t* w, cudaStream_t st) {
+    const uint32_t o = B == 3 ? tg_combO_T3 : tg_combO_T4;
+    WarpInterpConst K;
+    K.o = o;
+    K.oinv = B == 3 ? tg_combInv_T3 : tg_combInv_T4;
+    K.sh = B == 3 ? tg_combS_T3 : tg_combS_T4;
+    K.orcp = o > 1 ? ~0ull / o : 0ull;
+    K.p32 = host_powmod(2, 32, o);
+    K.Mch = host_powmod(2, 32ull * CH, o);
+    K.mi = host_invmod(K.Mch, o);
+    const int wpb = 8;
+    const size_t smem = interp_top_warp_smem(B, 2 * Lv.e, CH, wpb);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_interp_top_warp<B, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    const unsigned grid = (unsigned)((Lv.count + wpb - 1) / wpb);
+    k_interp_top_warp<B, CH><<<grid, 32 * wpb, smem, st>>>(P1, w, Lv.count, 2 * Lv.e, Lv.b, 2 * Lv.n, K);
+}
+
+static void launch_interp_top_warp(const Level& Lv, const uint32_t* P1, uint32_t* w, cudaStream_t st) {
+    const int ch = top_warp_ch(Lv);
+#define TG_W(BB, CC) if (Lv.B == BB && ch == CC) launch_interp_top_warp_t<BB, CC>(Lv, P1, w, st);
+    TG_W(3, 9) TG_W(3, 17) TG_W(3, 33) TG_W(4, 9) TG_W(4, 17) TG_W(4, 33)
+#undef TG_W
 }
 
 static toom_status launch_interp_top_rows(const Level& Lv, const uint32_t* P1, uint32_t* w, cudaStream_t st) {
@@ -836,7 +886,10 @@ static void launch_transpose(const uint32_t* in, uint32_t* out, size_t R, size_t
 // recomposition op), built on the host and uploaded once per call
 // ------------------------------------------------------------------------
 struct LongCall {
-    std::vector<LOpDev> down, up;
+    std::vector<LOpDev> down, up;        // single-output ops (per level, in launch order)
+    std::vector<LMultiDev> mdown, mup;   // multi-output ops
+    // launch order of a level: (kind 0 = op, 1 = multi, index into the level's vectors)
+    std::vector<std::pair<int, int>> sdown, sup;
 };
 
 // layout of level l's child operand / product families
@@ -924,6 +977,111 @@ static void long_interp_ops(const Level& L, YF yv, uint32_t* slots, uint32_t* ds
     out.push_back(b.op);
 }
 
+// tile shape of a multi-output op: the largest tile within the shared-memory
+// budget that pads the vector by at most 1/8
+static bool multi_shape(LMultiDev& d) {
+    d.ch = 16;   // the per-output scan costs ~1k instructions per thread: amortise over 16 limbs
+    int best = 0;
+    long long bestw = -1;
+    for (int nt = LV_NT; nt >= 32; nt -= 32) {
+        if (long_multi_smem(nt, d.ch, d.ns) > 96 * 1024) continue;
+        const long long tl = (long long)nt * d.ch, tiles = (d.W + tl - 1) / tl, pad = tiles * tl;
+        if (pad * 8 <= (long long)d.W * 9) { best = nt; break; }
+        if (bestw < 0 || pad < bestw) { bestw = pad; best = nt; }
+    }
+    if (!best) return false;
+    d.nthreads = best;
+    d.tiles_per_inst = (d.W + best * d.ch - 1) / (best * d.ch);
+    return true;
+}
+
+static void multi_out(LMOut& O, uint32_t* dst, uint32_t o, int shr, int ch) {
+    memset(&O, 0, sizeof O);
+    O.dst = dst;
+    O.o = o;
+    O.oinv = host_inv32(o);
+    if (o > 1) {
+        O.orcp = ~0ull / o;
+        O.p32 = host_powmod(2, 32, o);
+        O.Mch = host_powmod(2, 32ull * ch, o);
+        O.mi = host_invmod(O.Mch, o);
+    }
+    O.sa = shr / 32;
+    O.sr = shr % 32;
+}
+
+static bool g_long_meval = true;
+
+// evaluation of a long level: all 2B-1 points of one operand family (sources:
+// the B blocks of Eq. 1.1; multipliers p^j q^(n-j))
+template <class ChildF>
+static bool long_multi_eval(const Level& L, const LVec& par, ChildF child, LMultiDev& d) {
+    LongTables T;
+    long_tables(L.B, T);
+    if (!g_long_meval || L.B > LM_MAXS || L.npts > LM_MAXO || par.ls != 1) return false;
+    memset(&d, 0, sizeof d);
+    d.ns = L.B;
+    d.no = L.npts;
+    d.W = L.e;
+    d.count = (int)L.count;
+    for (int j = 0; j < L.B; ++j) {
+        const int len = (j == L.B - 1) ? L.lentop : L.b;
+        d.src[j] = LMSrc{par.base + (size_t)j * L.b, par.is, len, (j == L.B - 1) ? par.sign : 0};
+    }
+    for (int k = 0; k < T.neo; ++k) {
+        const tg_lop& o = T.eo[k];
+        for (int t = 0; t < o.nt; ++t) {
+            const tg_lterm& tm = T.et[o.t0 + t];
+            d.m[o.dst][-tm.src - 1] += tm.m * (1ll << tm.s);
+        }
+    }
+    unsigned long long sum = 0;
+    for (int k = 0; k < L.npts; ++k) {
+        unsigned long long r = 0;
+        for (int j = 0; j < L.B; ++j) r += (unsigned long long)(d.m[k][j] < 0 ? -d.m[k][j] : d.m[k][j]);
+        sum = std::max(sum, r);
+    }
+    d.wide = sum >= (1ull << 30);
+    if (!multi_shape(d)) return false;
+    for (int k = 0; k < L.npts; ++k) {
+        const LVec c = child(k);
+        if (c.ls != 1 && k == 0) { /* interleaved children are fine: strided stores */ }
+        multi_out(d.out[k], (uint32_t*)c.base, 1, 0, d.ch);
+        d.dst_is = c.is;
+        d.dst_ls = c.ls;
+    }
+    return true;
+}
+
+// interpolation rows of a Toom-3/4 long level: w_j = (sum_k A_jk y_k)/D_j for
+// the interior rows j = 1 .. 2B-3 (w_0 = y_0, w_2n = y_inf), into the slots
+template <class YF>
+static bool long_multi_rows(const Level& L, YF yv, uint32_t* slots, LMultiDev& d) {
+    if (!g_long_meval || (L.B != 3 && L.B != 4) || L.Lw != 2 * L.b + 1) return false;
+    const long long* A = L.B == 3 ? &tg_lrowA_T3[0][0] : &tg_lrowA_T4[0][0];
+    const unsigned* O = L.B == 3 ? tg_lrowO_T3 : tg_lrowO_T4;
+    const int* S = L.B == 3 ? tg_lrowS_T3 : tg_lrowS_T4;
+    memset(&d, 0, sizeof d);
+    d.ns = L.npts;
+    d.no = L.npts - 2;
+    d.W = L.Lw;
+    d.count = (int)L.count;
+    for (int k = 0; k < L.npts; ++k) {
+        const LVec y = yv(k);
+        if (y.ls != 1) return false;
+        d.src[k] = LMSrc{y.base, y.is, 2 * L.e, 1};
+    }
+    for (int j = 1; j <= L.npts - 2; ++j)
+        for (int k = 0; k < L.npts; ++k) d.m[j - 1][k] = A[j * L.npts + k];
+    d.wide = 0;
+    if (!multi_shape(d)) return false;
+    for (int j = 1; j <= L.npts - 2; ++j)
+        multi_out(d.out[j - 1], slots + (size_t)(j - 1) * L.count * L.Lw, O[j], S[j], d.ch);
+    d.dst_is = L.Lw;
+    d.dst_ls = 1;
+    return true;
+}
+
 static void build_long_level(const Plan& plan, size_t l, uint32_t* w, const uint32_t* u, const uint32_t* v, uint8_t* ws,
                              LongCall& lc) {
     const Level& L = plan.lv[l];
@@ -932,11 +1090,38 @@ static void build_long_level(const Plan& plan, size_t l, uint32_t* w, const uint
         if (l == 0) par = LVec{opd ? v : u, L.n, 1, L.n, plan.signed_in ? 1 : 0};   // user operands, row-major
         else par = LVec{(const uint32_t*)(ws + (opd ? plan.lv[l - 1].offV : plan.lv[l - 1].offU)), L.n, 1, L.n, 1};
         const size_t off = opd ? L.offV : L.offU;
-        long_eval_ops(L, par, [&](int k) { return child_vec(plan, l, ws, off, L.e, k); }, lc.down);
+        auto child = [&](int k) { return child_vec(plan, l, ws, off, L.e, k); };
+        LMultiDev d;
+        if (long_multi_eval(L, par, child, d)) {
+            lc.sdown.push_back({1, (int)lc.mdown.size()});
+            lc.mdown.push_back(d);
+        } else {
+            const size_t a = lc.down.size();
+            long_eval_ops(L, par, child, lc.down);
+            for (size_t i = a; i < lc.down.size(); ++i) lc.sdown.push_back({0, (int)i});
+        }
     }
     uint32_t* dst = (l == 0) ? w : (uint32_t*)(ws + plan.lv[l - 1].offP);
-    long_interp_ops(L, [&](int k) { return child_vec(plan, l, ws, L.offP, 2 * L.e, k); }, (uint32_t*)(ws + plan.offSlots),
-                    dst, lc.up);
+    uint32_t* slots = (uint32_t*)(ws + plan.offSlots);
+    auto yv = [&](int k) { return child_vec(plan, l, ws, L.offP, 2 * L.e, k); };
+    LMultiDev d;
+    if (long_multi_rows(L, yv, slots, d)) {
+        // rows w_1 .. w_2n-1 into the slots, then w = sum_j w_j 2^(32 b j)
+        lc.sup.push_back({1, (int)lc.mup.size()});
+        lc.mup.push_back(d);
+        LOpBuilder b(dst, 2 * L.n, 1, 2 * L.n, (int)L.count);
+        for (int j = 0; j < L.npts; ++j) {
+            if (j == 0 || j == L.npts - 1) b.add(yv(j), 1, 32ll * L.b * j);
+            else b.add(LVec{slots + (size_t)(j - 1) * L.count * L.Lw, L.Lw, 1, L.Lw, 1}, 1, 32ll * L.b * j);
+        }
+        b.op.wide = 0;
+        lc.sup.push_back({0, (int)lc.up.size()});
+        lc.up.push_back(b.op);
+        return;
+    }
+    const size_t a = lc.up.size();
+    long_interp_ops(L, yv, slots, dst, lc.up);
+    for (size_t i = a; i < lc.up.size(); ++i) lc.sup.push_back({0, (int)i});
 }
 
 static std::mutex g_desc_mu;
@@ -944,31 +1129,68 @@ static LOpDev* g_desc_host = nullptr;   // pinned staging for the descriptor upl
 static size_t g_desc_cap = 0;
 static cudaEvent_t g_desc_ev = nullptr;
 
-// upload the call's op descriptors (pinned staging, one copy) and reset the
-// scan status / tile counters, all stream-ordered
-static toom_status long_prepare(const std::vector<LOpDev>& a, const std::vector<LOpDev>& b, LOpDev* ddesc,
-                                LStatus* status, size_t nStatus, unsigned* ctr, size_t nCtr, cudaStream_t st) {
-    const size_t nd = a.size() + b.size();
+// upload the call's op descriptors (pinned staging, one copy per kind) and
+// reset the scan status / tile counters, all stream-ordered
+static toom_status long_prepare(const std::vector<LOpDev>& ops, const std::vector<LMultiDev>& mops, LOpDev* ddesc,
+                                LMultiDev* mdesc, LStatus* status, size_t nStatus, unsigned* ctr, size_t nCtr,
+                                cudaStream_t st) {
+    const size_t nd = ops.size(), ne = mops.size();
+    const size_t bytes = nd * sizeof(LOpDev) + ne * sizeof(LMultiDev);
     std::lock_guard<std::mutex> g(g_desc_mu);
     if (g_desc_ev) cudaEventSynchronize(g_desc_ev);   // previous upload finished reading the staging
-    if (nd > g_desc_cap) {
+    if (bytes > g_desc_cap * sizeof(LOpDev)) {
         if (g_desc_host) cudaFreeHost(g_desc_host);
-        if (cudaMallocHost((void**)&g_desc_host, nd * sizeof(LOpDev)) != cudaSuccess) {
+        const size_t cap = (bytes + sizeof(LOpDev) - 1) / sizeof(LOpDev);
+        if (cudaMallocHost((void**)&g_desc_host, cap * sizeof(LOpDev)) != cudaSuccess) {
             cudaGetLastError();
             g_desc_host = nullptr;
             g_desc_cap = 0;
             return TOOM_ENOMEM;
         }
-        g_desc_cap = nd;
+        g_desc_cap = cap;
     }
-    if (!a.empty()) memcpy(g_desc_host, a.data(), a.size() * sizeof(LOpDev));
-    if (!b.empty()) memcpy(g_desc_host + a.size(), b.data(), b.size() * sizeof(LOpDev));
-    if (cudaMemcpyAsync(ddesc, g_desc_host, nd * sizeof(LOpDev), cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return TOOM_ECUDA;
+    if (nd) {
+        memcpy(g_desc_host, ops.data(), nd * sizeof(LOpDev));
+        if (cudaMemcpyAsync(ddesc, g_desc_host, nd * sizeof(LOpDev), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return TOOM_ECUDA;
+    }
+    if (ne) {
+        uint8_t* hb = (uint8_t*)(g_desc_host + nd);
+        memcpy(hb, mops.data(), ne * sizeof(LMultiDev));
+        if (cudaMemcpyAsync(mdesc, hb, ne * sizeof(LMultiDev), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return TOOM_ECUDA;
+    }
     if (!g_desc_ev) cudaEventCreateWithFlags(&g_desc_ev, cudaEventDisableTiming);
     cudaEventRecord(g_desc_ev, st);
     cudaMemsetAsync(status, 0, nStatus * sizeof(LStatus), st);
     cudaMemsetAsync(ctr, 0, nCtr * sizeof(unsigned), st);
+    return TOOM_OK;
+}
+
+static toom_status launch_long_multi(const LMultiDev& d, const LMultiDev* dd, LStatus* status, unsigned* ctr,
+                                     unsigned& epoch, int cat, cudaStream_t st) {
+    const unsigned grid = (unsigned)((size_t)d.count * d.tiles_per_inst);
+    if (grid == 0) return TOOM_OK;
+    ProfScope ps(cat, st);
+    const size_t sm = long_multi_smem(d.nthreads, d.ch, d.ns);
+#define TG_LM(W, C)                                                                                        \
+    {                                                                                                      \
+        static bool attr = false;                                                                          \
+        if (!attr) {                                                                                       \
+            cudaFuncSetAttribute(k_long_multi<W, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+            attr = true;                                                                                   \
+        }                                                                                                  \
+        k_long_multi<W, C><<<grid, d.nthreads, sm, st>>>(dd, status, epoch, ctr);                         \
+    }
+    if (d.ch == 16) {
+        if (d.wide) TG_LM(true, 16) else TG_LM(false, 16)
+    } else {
+        if (d.wide) TG_LM(true, 4) else TG_LM(false, 4)
+    }
+#undef TG_LM
+    ps.done(st);
+    ++epoch;
+    ++t_launches;
     return TOOM_OK;
 }
 
@@ -981,7 +1203,15 @@ static toom_status launch_long_ops(const std::vector<LOpDev>& ops, size_t first,
         ProfScope ps(cat, st);
         const LOpDev* d = ddesc + first + i;
         unsigned* cp = ctr + first + i;
-        const size_t qs = ((size_t)o.nthreads * o.ch + LV_MAXHALO + 1) * 4;
+        const size_t qs = ((size_t)o.nthreads * o.ch + LV_MAXHALO + 1 + (size_t)(o.ch + 1) * (o.nthreads + 1)) * 4;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_long_op<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+            cudaFuncSetAttribute(k_long_op<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+            cudaFuncSetAttribute(k_long_op<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+            cudaFuncSetAttribute(k_long_op<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+            attr = true;
+        }
         if (o.ch == 16) {
             if (o.wide) k_long_op<true, 16><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
             else k_long_op<false, 16><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
@@ -1003,25 +1233,52 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
     // long-vector prefix of the recursion
     size_t Tl = 0;
     while (Tl < L && plan.lv[Tl].lng) ++Tl;
-    LongCall lc;
-    std::vector<size_t> up_first(Tl + 1, 0);
+    // all ops of the long levels: single-output ops `ops`, multi-output `mops`;
+    // launch steps (kind, global index): down in level order, up deepest first
+    std::vector<LOpDev> ops;
+    std::vector<LMultiDev> mops;
+    std::vector<std::pair<int, int>> sdown, sup;
     LOpDev* ddesc = (LOpDev*)(ws + plan.offDesc);
+    LMultiDev* mdesc = (LMultiDev*)(ws + plan.offEDesc);
     LStatus* status = (LStatus*)(ws + plan.offStatus);
     unsigned* ctr = (unsigned*)(ws + plan.offCtr);
     unsigned epoch = 1;
+    auto run_steps = [&](const std::vector<std::pair<int, int>>& steps, int cat) -> toom_status {
+        const size_t nops = ops.size();
+        for (const auto& stp : steps) {
+            toom_status r;
+            if (stp.first == 0) {
+                std::vector<LOpDev> one(1, ops[stp.second]);
+                r = launch_long_ops(one, (size_t)stp.second, ddesc, status, ctr, epoch, cat, st);
+            } else {
+                r = launch_long_multi(mops[stp.second], mdesc + stp.second, status, ctr + nops + stp.second, epoch, cat,
+                                      st);
+            }
+            if (r) return r;
+        }
+        return TOOM_OK;
+    };
     if (Tl) {
-        std::vector<std::vector<LOpDev>> ups(Tl);
+        std::vector<std::vector<std::pair<int, int>>> ups(Tl);
         for (size_t l = 0; l < Tl; ++l) {
             LongCall one;
             build_long_level(plan, l, w, u, v, ws, one);
-            lc.down.insert(lc.down.end(), one.down.begin(), one.down.end());
-            ups[l] = one.up;
+            const int od = (int)ops.size();
+            ops.insert(ops.end(), one.down.begin(), one.down.end());
+            const int ou = (int)ops.size();
+            ops.insert(ops.end(), one.up.begin(), one.up.end());
+            const int md = (int)mops.size();
+            mops.insert(mops.end(), one.mdown.begin(), one.mdown.end());
+            const int mu = (int)mops.size();
+            mops.insert(mops.end(), one.mup.begin(), one.mup.end());
+            for (auto x : one.sdown) sdown.push_back({x.first, x.second + (x.first ? md : od)});
+            for (auto x : one.sup) ups[l].push_back({x.first, x.second + (x.first ? mu : ou)});
         }
-        // up order: deepest long level first
-        for (size_t l = Tl; l-- > 0;) lc.up.insert(lc.up.end(), ups[l].begin(), ups[l].end());
-        if (lc.down.size() + lc.up.size() > plan.nDesc) return TOOM_EINVAL;
-        if ((s = long_prepare(lc.down, lc.up, ddesc, status, plan.nStatus, ctr, plan.nCtr, st))) return s;
-        if ((s = launch_long_ops(lc.down, 0, ddesc, status, ctr, epoch, CAT_EVAL, st))) return s;
+        for (size_t l = Tl; l-- > 0;) sup.insert(sup.end(), ups[l].begin(), ups[l].end());
+        if (ops.size() > plan.nDesc || mops.size() > plan.nDesc || ops.size() + mops.size() > plan.nCtr)
+            return TOOM_EINVAL;
+        if ((s = long_prepare(ops, mops, ddesc, mdesc, status, plan.nStatus, ctr, plan.nCtr, st))) return s;
+        if ((s = run_steps(sdown, CAT_EVAL))) return s;
         if (plan.bnd >= 0) {   // row-major children -> interleaved [e][npts*count]
             const Level& Lb = plan.lv[plan.bnd];
             const size_t cc = Lb.count * Lb.npts;
@@ -1067,7 +1324,9 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         const uint32_t* su = top ? u : (const uint32_t*)(ws + plan.lv[L - 2].offU);
         const uint32_t* sv = top ? v : (const uint32_t*)(ws + plan.lv[L - 2].offV);
         uint32_t* out = top ? w : (uint32_t*)(ws + plan.lv[L - 2].offP);
-        const int mode = top ? 1 : (plan.lv[L - 2].lng ? 2 : 0);   // a long parent level writes row-major children
+        // a long parent level writes row-major children; a warp-per-product top
+        // interpolation reads row-major products
+        const int mode = top ? 1 : (plan.lv[L - 2].lng ? 2 : (plan.top_warp ? 3 : 0));
         if ((s = launch_fused(Lv, mode, su, sv, out, st))) return s;
     } else {
         const Level& Lv = plan.lv[L - 1];
@@ -1079,6 +1338,13 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
     for (size_t l = Lt; l-- > Tl;) {
         const Level& Lv = plan.lv[l];
         uint32_t* out = l == 0 ? w : (uint32_t*)(ws + plan.lv[l - 1].offP);
+        if (l == 0 && plan.top_warp) {
+            ProfScope ps(CAT_INTERP, st);
+            launch_interp_top_warp(Lv, (const uint32_t*)(ws + Lv.offP), w, st);
+            ps.done(st);
+            ++t_launches;
+            continue;
+        }
         if (l == 0 && top_rows_ok(Lv)) {
             if ((s = launch_interp_top_rows(Lv, (const uint32_t*)(ws + Lv.offP), w, st))) return s;
             continue;
@@ -1095,7 +1361,7 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             launch_transpose((const uint32_t*)(ws + Lb.offP), (uint32_t*)(ws + plan.offT), 2 * Lb.e, cc, st);
             ps.done(st);
         }
-        if ((s = launch_long_ops(lc.up, lc.down.size(), ddesc, status, ctr, epoch, CAT_INTERP, st))) return s;
+        if ((s = run_steps(sup, CAT_INTERP))) return s;
     }
     return TOOM_OK;
 }
@@ -1185,10 +1451,11 @@ static toom_status run_long_standalone(size_t slot_limbs, size_t tiles, size_t n
     LStatus* status = (LStatus*)(base + bS);
     unsigned* ctr = (unsigned*)(base + bS + bT);
     LOpDev* ddesc = (LOpDev*)(base + bS + bT + bC);
-    std::vector<LOpDev> ops, none;
+    std::vector<LOpDev> ops;
+    std::vector<LMultiDev> none;
     build((uint32_t*)base, ops);
     if (ops.size() > nops) return TOOM_EINVAL;
-    if ((s = long_prepare(ops, none, ddesc, status, tiles, ctr, nops, st))) return s;
+    if ((s = long_prepare(ops, none, ddesc, nullptr, status, tiles, ctr, nops, st))) return s;
     unsigned epoch = 1;
     return launch_long_ops(ops, 0, ddesc, status, ctr, epoch, CAT_OTHER, st);
 }

@@ -353,6 +353,61 @@ __device__ __forceinline__ void cp_async4(uint32_t* dst_smem, const uint32_t* sr
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
 }
 
+template <int B, int J>
+__device__ __forceinline__ uint32_t rowstep_j(const uint32_t (&y)[2 * B - 1], tg_rowstate& st) {
+    if constexpr (B == 3) {
+        if constexpr (J == 1) return tg_rowstep_T3_1(y, st);
+        else if constexpr (J == 2) return tg_rowstep_T3_2(y, st);
+        else return tg_rowstep_T3_3(y, st);
+    } else {
+        if constexpr (J == 1) return tg_rowstep_T4_1(y, st);
+        else if constexpr (J == 2) return tg_rowstep_T4_2(y, st);
+        else if constexpr (J == 3) return tg_rowstep_T4_3(y, st);
+        else if constexpr (J == 4) return tg_rowstep_T4_4(y, st);
+        else return tg_rowstep_T4_5(y, st);
+    }
+}
+
+// phase 1 of k_interp_top_smem for coefficient row J (every warp of the CTA
+// runs the chunk loop so that the block barriers match; `work` = this warp
+// owns row J).  Outputs of a chunk are written in place over y_J after all
+// warps have read the chunk.
+template <int B, int J>
+__device__ __forceinline__ void interp_rows_inplace(uint32_t* Y, int ywidth, int G, int Lw, int lane, bool work) {
+    constexpr int NP = 2 * B - 1, CK = 8;
+    const uint32_t* yb[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) yb[k] = Y + (size_t)k * ywidth * G + lane;
+    uint32_t* dst = Y + (size_t)J * ywidth * G + lane;
+    tg_rowstate st{0, 0, 0};
+    for (int t0 = 0; t0 <= Lw; t0 += CK) {
+        uint32_t ob[CK];
+        if (work) {
+#pragma unroll
+            for (int tt = 0; tt < CK; ++tt) {
+                const int t = t0 + tt;
+                ob[tt] = 0;
+                if (t <= Lw) {
+                    const int off = t * G;
+                    uint32_t y[NP];
+#pragma unroll
+                    for (int k = 0; k < NP; ++k) y[k] = yb[k][off];
+                    ob[tt] = rowstep_j<B, J>(y, st);
+                }
+            }
+        }
+        __syncthreads();
+        if (work) {
+#pragma unroll
+            for (int tt = 0; tt < CK; ++tt) {
+                const int t = t0 + tt;
+                if (t >= 1 && t <= Lw) dst[(t - 1) * G] = ob[tt];
+            }
+        }
+        __syncthreads();
+    }
+}
+
 template <int B>
 __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint32_t* __restrict__ P1,
                                                                        uint32_t* __restrict__ w, size_t count,
@@ -369,29 +424,36 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     const size_t c0 = (size_t)blockIdx.x * G;
     const int nin = (int)min((size_t)G, count - c0);
     const size_t S = (size_t)NP * count;
-    // ---- phase 0: rows (k, t) of G contiguous words, 16-byte copies when aligned
+    // ---- phase 0: rows (k, t) of G contiguous words; 16-byte copies when
+    // aligned, several rows per warp instruction
     {
         const int nw = blockDim.x >> 5;
+        const int nrows = NP * ywidth;
         const bool v16 = ((count & 3) == 0) && ((G & 3) == 0);
-        const int q4 = G >> 2;
-        for (int k = 0; k < NP; ++k) {
-            const uint32_t* src = P1 + (size_t)k * count + c0;
-            uint32_t* dst = Y + (size_t)k * ywidth * G;
-            for (int t = warp; t < ywidth; t += nw) {
-                const uint32_t* sr = src + (size_t)t * S;
-                uint32_t* dr = dst + t * G;
-                if (v16) {
-                    if (lane < q4) {
-                        const int g = lane * 4;
-                        if (g + 3 < nin) {
-                            const unsigned d = (unsigned)__cvta_generic_to_shared(dr + g);
-                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(sr + g));
-                        } else {
+        if (v16) {
+            const int q4 = G >> 2, rp = 32 / q4;
+            const int sub = lane / q4, q = lane - sub * q4;
+            if (sub < rp) {
+                for (int R = warp * rp + sub; R < nrows; R += nw * rp) {
+                    const int k = R / ywidth, t = R - k * ywidth;
+                    const uint32_t* sr = P1 + (size_t)t * S + (size_t)k * count + c0;
+                    uint32_t* dr = Y + (size_t)R * G;
+                    const int g = q * 4;
+                    if (g + 3 < nin) {
+                        const unsigned d = (unsigned)__cvta_generic_to_shared(dr + g);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(sr + g));
+                    } else {
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) dr[g + q] = (g + q < nin) ? __ldg(sr + g + q) : 0u;
-                        }
+                        for (int x = 0; x < 4; ++x) dr[g + x] = (g + x < nin) ? __ldg(sr + g + x) : 0u;
                     }
-                } else if (lane < G) {
+                }
+            }
+        } else {
+            for (int R = warp; R < nrows; R += nw) {
+                const int k = R / ywidth, t = R - k * ywidth;
+                const uint32_t* sr = P1 + (size_t)t * S + (size_t)k * count + c0;
+                uint32_t* dr = Y + (size_t)R * G;
+                if (lane < G) {
                     if (lane < nin) cp_async4(dr + lane, sr + lane);
                     else dr[lane] = 0u;
                 }
@@ -401,35 +463,27 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     }
     __syncthreads();
     const bool act = lane < G;
-    // ---- phase 1: rows 1..NP-2, in place
+    // ---- phase 1: rows 1..NP-2, in place (one specialised loop per row)
     {
-        const int j = warp;
-        const bool rw = act && j >= 1 && j <= NP - 2;
-        tg_rowstate st{0, 0, 0};
-        for (int t0 = 0; t0 <= Lw; t0 += CK) {
-            uint32_t ob[CK];
-            if (rw) {
-#pragma unroll
-                for (int tt = 0; tt < CK; ++tt) {
-                    const int t = t0 + tt;
-                    ob[tt] = 0;
-                    if (t <= Lw) {
-                        uint32_t y[NP];
-#pragma unroll
-                        for (int k = 0; k < NP; ++k) y[k] = Y[(k * ywidth + t) * G + lane];
-                        ob[tt] = rowstep<B>(j, y, st);
-                    }
-                }
+        // the branch is warp-uniform (every lane of a warp reaches the same
+        // barriers); lanes >= G only skip the work
+        const int wj = (warp >= 1 && warp <= NP - 2) ? warp : 0;
+        if constexpr (B == 3) {
+            switch (wj) {
+                case 1: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, act); break;
+                case 2: interp_rows_inplace<B, 2>(Y, ywidth, G, Lw, lane, act); break;
+                case 3: interp_rows_inplace<B, 3>(Y, ywidth, G, Lw, lane, act); break;
+                default: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, false); break;
             }
-            __syncthreads();
-            if (rw) {
-#pragma unroll
-                for (int tt = 0; tt < CK; ++tt) {
-                    const int t = t0 + tt;
-                    if (t >= 1 && t <= Lw) Y[(j * ywidth + t - 1) * G + lane] = ob[tt];
-                }
+        } else {
+            switch (wj) {
+                case 1: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, act); break;
+                case 2: interp_rows_inplace<B, 2>(Y, ywidth, G, Lw, lane, act); break;
+                case 3: interp_rows_inplace<B, 3>(Y, ywidth, G, Lw, lane, act); break;
+                case 4: interp_rows_inplace<B, 4>(Y, ywidth, G, Lw, lane, act); break;
+                case 5: interp_rows_inplace<B, 5>(Y, ywidth, G, Lw, lane, act); break;
+                default: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, false); break;
             }
-            __syncthreads();
         }
     }
     // ---- phase 2: recomposition (every w_j >= 0 at the top level).  Segment
@@ -511,6 +565,174 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
             }
         }
     }
+}
+
+}  // namespace tg
+
+namespace tg {
+
+// ------------------------------------------------------------------------
+// Top-level interpolation + recomposition, ONE WARP PER PRODUCT (steps a4 +
+// a5; C1, C2).  The combined matrix form over the common denominator Dc
+// (PAPER.md:162 + Eq. 1.3, reading 12):
+//     Dc * w = sum_j 2^(32 b j) sum_k A'_jk y_k
+// The warp stages the 2B-1 products y_k (row-major, coalesced) in shared
+// memory; lane L forms positions [L*CH, L*CH+CH) of the linear combination,
+// normalises them locally and the carry / 2-adic borrow of the exact division
+// by the odd part of Dc is resolved with a warp scan of the composable
+// carry/borrow maps (csrc/longvec.cuh); then the quotient is shifted by the
+// power of two of Dc and stored coalesced.  y_k are sign-extended (their
+// fills enter as per-row constants).
+// ------------------------------------------------------------------------
+struct WarpInterpConst {
+    uint32_t o, oinv, p32, Mch, mi;
+    unsigned long long orcp;
+    int sh;
+};
+
+template <int B, int CH>
+__global__ void __launch_bounds__(256) k_interp_top_warp(const uint32_t* __restrict__ P1, uint32_t* __restrict__ w,
+                                                         size_t count, int ywidth, int b, int wout, WarpInterpConst K) {
+    constexpr int NP = 2 * B - 1;
+    extern __shared__ uint32_t wsm[];
+    __shared__ long long sA[NP][NP];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x < NP * NP) {
+        const int j = threadIdx.x / NP, k = threadIdx.x % NP;
+        sA[j][k] = (B == 3) ? tg_combA_T3[j][k] : tg_combA_T4[j][k];
+    }
+    const size_t c = (size_t)blockIdx.x * nw + warp;
+    const int P = wout + 1;                       // positions 0..wout (one extra for the shift)
+    const int ysz = max(NP * ywidth, 64 * CH);     // products, later the 64-bit transpose scratch
+    const int wstride = (ysz + 32 * CH + 1 + 3) & ~3;
+    uint32_t* Ys = wsm + (size_t)warp * wstride;
+    uint32_t* Qs = Ys + ysz;
+    long long* Fs = reinterpret_cast<long long*>(wsm + (size_t)nw * wstride) + warp * NP;
+    __syncthreads();
+    if (c >= count) return;                       // warp-uniform
+    // stage the products (row k*count + c of the row-major [NP*count][ywidth] buffer)
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        const uint32_t* src = P1 + ((size_t)k * count + c) * ywidth;
+        for (int i = lane; i < ywidth; i += 32) Ys[k * ywidth + i] = __ldg(src + i);
+    }
+    __syncwarp();
+    long long fillv[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) fillv[k] = (Ys[k * ywidth + ywidth - 1] >> 31) ? 0xFFFFFFFFll : 0ll;
+    const int p0 = lane * CH;
+    long long lin[CH];
+    {
+        // pass 1: positions p = lane + 32 q (the warp covers 32 consecutive
+        // positions per q, so the set of active rows j is warp-uniform);
+        // rows entirely past their products add the constant F_j.
+        if (lane < NP) {
+            long long f = 0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) f += sA[lane][k] * fillv[k];
+            Fs[lane] = f;
+        }
+        __syncwarp();
+        const long long* F = Fs;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            const int pw = 32 * q;                  // first position of this row of the warp
+            const int p = pw + lane;
+            // rows with b*j <= p (started) and p - b*j < ywidth (not yet past)
+            const int jhi = min(NP - 1, (pw + 31) / b);
+            const int jlo = max(0, (pw - ywidth) / b);   // rows below jlo are past for the whole warp row
+            long long acc = 0;
+            for (int j = 0; j < jlo; ++j) acc += F[j];
+            for (int j = jlo; j <= jhi; ++j) {
+                const int i = p - b * j;
+                if (i >= ywidth) {
+                    acc += F[j];
+                } else if (i >= 0) {
+                    long long sj = 0;
+#pragma unroll
+                    for (int k = 0; k < NP; ++k) sj += sA[j][k] * (long long)Ys[k * ywidth + i];
+                    acc += sj;
+                }
+            }
+            lin[q] = acc;
+        }
+    }
+    // transpose through shared memory: lane L takes positions [L*CH, L*CH+CH)
+    {
+        long long* T64 = reinterpret_cast<long long*>(Ys);   // the products are no longer needed
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < CH; ++q) T64[32 * q + lane] = lin[q];
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < CH; ++q) lin[q] = T64[p0 + q];
+        __syncwarp();
+    }
+    // local normalisation -> this lane's carry / borrow map
+    const LMod M{K.o, K.orcp};
+    uint32_t x[CH];
+    long long cy = 0;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+        const long long v = lin[q] + cy;
+        x[q] = (uint32_t)v;
+        cy = v >> 32;
+    }
+    LAgg A;
+    {
+        const unsigned long long L64 = (unsigned long long)x[0] | ((unsigned long long)x[1] << 32);
+        bool tz = true, to = true;
+#pragma unroll
+        for (int q = 2; q < CH; ++q) { tz &= (x[q] == 0u); to &= (x[q] == 0xFFFFFFFFu); }
+        A.lo = (tz && L64 <= 0x8000000000000000ull) ? (long long)(0ull - L64) : LLONG_MIN;
+        const unsigned long long comp = 0ull - L64;
+        A.hi = (to && L64 != 0 && comp <= (unsigned long long)LLONG_MAX) ? (long long)comp : LLONG_MAX;
+        A.cout[0] = cy - 1;
+        A.cout[1] = cy;
+        A.cout[2] = cy + 1;
+        uint32_t r = 0;
+#pragma unroll
+        for (int q = CH - 1; q >= 0; --q) r = lv_mod((unsigned long long)r * K.p32 + x[q], M);
+        A.m = K.mi;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            const unsigned long long t = (unsigned long long)(K.o - r) + (p == 2 ? K.Mch : 0u) + (p == 0 ? (K.o - K.Mch) : 0u);
+            A.g[p] = lv_mulmod(lv_mod(t, M), K.mi, M);
+        }
+    }
+    LAgg inc = A;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const LAgg prev = lv_shfl_up(inc, d);
+        if (lane >= d) inc = lv_compose(prev, inc, M);
+    }
+    const LAgg excl = lv_shfl_up(inc, 1);
+    long long cin = 0;
+    uint32_t bin = 0;
+    if (lane > 0) lv_apply(excl, cin, bin, M);
+    // exact limbs, exact division by the odd part of Dc
+    cy = cin;
+    uint32_t beta = bin;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+        const long long v = lin[q] + cy;
+        cy = v >> 32;
+        Qs[p0 + q] = tg_divexact_step((uint32_t)v, beta, K.oinv, K.o);
+    }
+    __syncwarp();
+    // shift by the power of two of Dc, coalesced row-major store
+    uint32_t* row = w + c * (size_t)wout;
+    for (int t = lane; t < wout; t += 32) {
+        const uint32_t lo = Qs[t];
+        row[t] = K.sh ? __funnelshift_r(lo, Qs[t + 1], K.sh) : lo;
+    }
+    (void)P;
+}
+
+inline size_t interp_top_warp_smem(int B, int ywidth, int CH, int wpb) {
+    const int ysz = std::max((2 * B - 1) * ywidth, 64 * CH);
+    const int wstride = (ysz + 32 * CH + 1 + 3) & ~3;
+    return (size_t)4 * wpb * wstride + (size_t)8 * wpb * (2 * B - 1);
 }
 
 }  // namespace tg

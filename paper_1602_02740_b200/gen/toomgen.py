@@ -1138,6 +1138,13 @@ def emit_long_tables(ps: PointSet) -> str:
                      ", ".join("{" + ", ".join(str(A[j][k] * (Dc // Ds[j])) for k in range(NP)) + "}" for j in range(NP)) + "};")
         lines.append(f"constexpr unsigned tg_lcombO_{nm} = {Dc >> sc}u;")
         lines.append(f"constexpr int tg_lcombS_{nm} = {sc};")
+        # per-row form w_j = (sum_k A_jk y_k) / (o_j 2^s_j) (multi-output interpolation)
+        lines.append(f"static const long long tg_lrowA_{nm}[{NP}][{NP}] = {{" +
+                     ", ".join("{" + ", ".join(str(A[j][k]) for k in range(NP)) + "}" for j in range(NP)) + "};")
+        ro = [D >> ((D & -D).bit_length() - 1) for D in Ds]
+        rs = [(D & -D).bit_length() - 1 for D in Ds]
+        lines.append(f"static const unsigned tg_lrowO_{nm}[{NP}] = {{" + ", ".join(f"{x}u" for x in ro) + "};")
+        lines.append(f"static const int tg_lrowS_{nm}[{NP}] = {{" + ", ".join(str(x) for x in rs) + "};")
     for tag, lp in (("eval", ev), ("interp", it)):
         terms, ops = [], []
         for d, ts, o, shr in lp["ops"]:

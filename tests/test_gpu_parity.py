@@ -411,7 +411,8 @@ def test_sharded_mul_single_rank_cuda():
 
 
 @pytest.mark.parametrize("B,n,t4,t3", [(3, 96, 10**9, 10**9), (4, 256, 32, 32), (4, 250, 32, 32), (3, 301, 256, 64),
-                                       (4, 1000, 256, 64), (3, 13, 256, 64)])
+                                       (4, 1000, 256, 64), (3, 13, 256, 64), (3, 96, 24, 24), (4, 120, 24, 24),
+                                       (4, 520, 130, 130)])
 def test_top_stream_vs_rows(B, n, t4, t3):
     rng = np.random.default_rng(n + 17 * B)
     batch = 77
@@ -422,7 +423,7 @@ def test_top_stream_vs_rows(B, n, t4, t3):
     u[1] = 0
     want = oracle.schoolbook_batched(u, v)
     try:
-        for mode in (0, 1, 2):
+        for mode in (0, 1, 2, 3):
             tg.set_top_stream(mode)
             got = run_batched(u, v, B, t4=t4, t3=t3, long_count=1)
             assert np.array_equal(got, want), mode
