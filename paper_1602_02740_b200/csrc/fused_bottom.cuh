@@ -113,6 +113,30 @@ __device__ __forceinline__ void interp_row(int j, const uint32_t* __restrict__ Y
 }
 
 template <int B, int E>
+__device__ __forceinline__ void eval_point_regs(int k, const uint32_t* PU, const uint32_t* PV, uint32_t (&a)[E],
+                                                uint32_t (&b)[E]) {
+    if constexpr (B == 3) {
+        switch (k) {
+            case 0: tg_evalreg_T3_0<E>(PU, PV, a, b); break;
+            case 1: tg_evalreg_T3_1<E>(PU, PV, a, b); break;
+            case 2: tg_evalreg_T3_2<E>(PU, PV, a, b); break;
+            case 3: tg_evalreg_T3_3<E>(PU, PV, a, b); break;
+            default: tg_evalreg_T3_4<E>(PU, PV, a, b); break;
+        }
+    } else {
+        switch (k) {
+            case 0: tg_evalreg_T4_0<E>(PU, PV, a, b); break;
+            case 1: tg_evalreg_T4_1<E>(PU, PV, a, b); break;
+            case 2: tg_evalreg_T4_2<E>(PU, PV, a, b); break;
+            case 3: tg_evalreg_T4_3<E>(PU, PV, a, b); break;
+            case 4: tg_evalreg_T4_4<E>(PU, PV, a, b); break;
+            case 5: tg_evalreg_T4_5<E>(PU, PV, a, b); break;
+            default: tg_evalreg_T4_6<E>(PU, PV, a, b); break;
+        }
+    }
+}
+
+template <int B, int E>
 __device__ __forceinline__ void eval_point_rows(int k, const uint32_t* PU, const uint32_t* PV, uint32_t* dU, uint32_t* dV) {
     if constexpr (B == 3) {
         switch (k) {
@@ -204,6 +228,11 @@ __host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nse
     return (size_t)4 * ((size_t)NP * 2 * E * 32 + wreg + 4 * 32 * (size_t)nseg);
 }
 
+// diagnostic phase mask (bench/debug only; all phases by default): bit 0
+// products, bit 1 rows, bit 2 recomposition.  Results are wrong when a phase
+// is masked; used to measure the phases' share of the kernel time.
+__device__ int tg_fused_phase_mask = 7;
+
 // MODE: 0 = parents interleaved [n][count], signed (a lower level of a batch);
 //       1 = parents row-major [count][n], unsigned (the top level);
 //       2 = parents row-major [count][n], signed (below a long-vector level);
@@ -287,20 +316,23 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
     }
     __syncthreads();
 
+    const int pmask = tg_fused_phase_mask;
     // ---- phase A: evaluate point `warp` of both operands (from smem) into
     // the warp's own Y[k] slot, load to registers, multiply into the same slot
     if (valid) {
+        // (the rolled smem evaluation keeps the kernel small enough for the
+        // instruction cache; a fully unrolled register version measured slower)
         uint32_t* slot = Y + (warp * 2 * E) * G + lane;
         eval_point_rows<B, E>(warp, Pu + lane, Pv + lane, slot, slot + E * G);
         uint32_t a[E], bb[E];
 #pragma unroll
         for (int t = 0; t < E; ++t) { a[t] = slot[t * G]; bb[t] = slot[(E + t) * G]; }
-        mul_twos_to_smem<E>(a, bb, slot);
+        if (pmask & 1) mul_twos_to_smem<E>(a, bb, slot);
     }
     __syncthreads();
 
     // ---- phase B: coefficient w_warp (w_0 = y_0 and w_2n = y_inf are copies)
-    if (valid) {
+    if (valid && (pmask & 2)) {
         const uint32_t* Yl = Y + lane;
         uint32_t* dst = Wb + (warp * Lw) * G + lane;
         if (warp == 0 || warp == NP - 1) {
@@ -308,23 +340,24 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
             for (int t = 0; t < Lw; ++t) dst[t * G] = src[t * G];
         } else if constexpr (B == 3) {
             switch (warp) {
-                case 1: tg_row_T3_1(Yl, 2 * E, dst, Lw); break;
-                case 2: tg_row_T3_2(Yl, 2 * E, dst, Lw); break;
-                default: tg_row_T3_3(Yl, 2 * E, dst, Lw); break;
+                case 1: tg_row_T3_1<2 * E>(Yl, dst, Lw); break;
+                case 2: tg_row_T3_2<2 * E>(Yl, dst, Lw); break;
+                default: tg_row_T3_3<2 * E>(Yl, dst, Lw); break;
             }
         } else {
             switch (warp) {
-                case 1: tg_row_T4_1(Yl, 2 * E, dst, Lw); break;
-                case 2: tg_row_T4_2(Yl, 2 * E, dst, Lw); break;
-                case 3: tg_row_T4_3(Yl, 2 * E, dst, Lw); break;
-                case 4: tg_row_T4_4(Yl, 2 * E, dst, Lw); break;
-                default: tg_row_T4_5(Yl, 2 * E, dst, Lw); break;
+                case 1: tg_row_T4_1<2 * E>(Yl, dst, Lw); break;
+                case 2: tg_row_T4_2<2 * E>(Yl, dst, Lw); break;
+                case 3: tg_row_T4_3<2 * E>(Yl, dst, Lw); break;
+                case 4: tg_row_T4_4<2 * E>(Yl, dst, Lw); break;
+                default: tg_row_T4_5<2 * E>(Yl, dst, Lw); break;
             }
         }
     }
     __syncthreads();
 
     // ---- phase C1: segment sums with local carries (OUT aliases Y)
+    if (!(pmask & 4)) return;
     uint32_t* OUT = Y;
     if (valid) {
         for (int s = warp; s < nseg; s += NP) {

@@ -699,6 +699,10 @@ static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* 
     const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg, Lv.n);
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
+        if (const char* m = getenv("TOOM_DBG_FUSED_MASK")) {   // diagnostics only
+            const int v = atoi(m);
+            cudaMemcpyToSymbol(tg_fused_phase_mask, &v, sizeof v);
+        }
         cudaFuncSetAttribute(k_fused_bottom<B, E, TOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         cudaFuncSetAttribute(k_fused_bottom<B, E, TOP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
@@ -768,8 +772,14 @@ static bool launch_interp_top_smem_t(const Level& Lv, const uint32_t* P1, uint32
     const int ywidth = 2 * Lv.e, nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
     constexpr int NP = 2 * B - 1;
     // instances per CTA: up to 32, two CTAs per SM if possible
+    // instances per CTA: the shared-memory budget per CTA sets the occupancy
+    // (2 CTAs per SM at ~113 KB)
+    static const int budget_kb = [] {
+        const char* e = getenv("TOOM_ITS_SMEM_KB");
+        return e ? atoi(e) : 113;
+    }();
     int G = 32;
-    while (G > 8 && interp_top_smem_bytes(B, ywidth, G, nseg) > 113 * 1024) G -= 4;
+    while (G > 4 && interp_top_smem_bytes(B, ywidth, G, nseg) > (size_t)budget_kb * 1024) G -= 4;
     if (interp_top_smem_bytes(B, ywidth, G, nseg) > 220 * 1024 || Lv.Lw >= ywidth || Lv.Lw != 2 * Lv.b + 1) return false;
     const size_t smem = interp_top_smem_bytes(B, ywidth, G, nseg);
     static bool attr = false;

@@ -463,27 +463,37 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     }
     __syncthreads();
     const bool act = lane < G;
-    // ---- phase 1: rows 1..NP-2, in place (one specialised loop per row)
+    // ---- phase 1: rows 1..NP-2, in place (lock-stepped chunks; the barriers
+    // are outside the per-lane work so every thread reaches them)
     {
-        // the branch is warp-uniform (every lane of a warp reaches the same
-        // barriers); lanes >= G only skip the work
-        const int wj = (warp >= 1 && warp <= NP - 2) ? warp : 0;
-        if constexpr (B == 3) {
-            switch (wj) {
-                case 1: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, act); break;
-                case 2: interp_rows_inplace<B, 2>(Y, ywidth, G, Lw, lane, act); break;
-                case 3: interp_rows_inplace<B, 3>(Y, ywidth, G, Lw, lane, act); break;
-                default: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, false); break;
+        constexpr int CK = 16;
+        const int j = warp;
+        const bool rw = act && j >= 1 && j <= NP - 2;
+        tg_rowstate st{0, 0, 0};
+        for (int t0 = 0; t0 <= Lw; t0 += CK) {
+            uint32_t ob[CK];
+            if (rw) {
+#pragma unroll
+                for (int tt = 0; tt < CK; ++tt) {
+                    const int t = t0 + tt;
+                    ob[tt] = 0;
+                    if (t <= Lw) {
+                        uint32_t y[NP];
+#pragma unroll
+                        for (int k = 0; k < NP; ++k) y[k] = Y[(k * ywidth + t) * G + lane];
+                        ob[tt] = rowstep<B>(j, y, st);
+                    }
+                }
             }
-        } else {
-            switch (wj) {
-                case 1: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, act); break;
-                case 2: interp_rows_inplace<B, 2>(Y, ywidth, G, Lw, lane, act); break;
-                case 3: interp_rows_inplace<B, 3>(Y, ywidth, G, Lw, lane, act); break;
-                case 4: interp_rows_inplace<B, 4>(Y, ywidth, G, Lw, lane, act); break;
-                case 5: interp_rows_inplace<B, 5>(Y, ywidth, G, Lw, lane, act); break;
-                default: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, false); break;
+            __syncthreads();
+            if (rw) {
+#pragma unroll
+                for (int tt = 0; tt < CK; ++tt) {
+                    const int t = t0 + tt;
+                    if (t >= 1 && t <= Lw) Y[(j * ywidth + t - 1) * G + lane] = ob[tt];
+                }
             }
+            __syncthreads();
         }
     }
     // ---- phase 2: recomposition (every w_j >= 0 at the top level).  Segment

@@ -765,17 +765,18 @@ def emit_row_functions(ps: PointSet) -> str:
         idx = [(pr.inputs.index(t.var), t.m) for t in op.terms]
         assert all(t.s == 0 for t in op.terms) and op.shr < 32
         L.append(f"// w_{j} = ({' '.join(f'{m:+d}*y{k}' for k, m in idx)}) / {op.odiv << op.shr}")
-        L.append(f"__device__ __forceinline__ void tg_row_{ps.name}_{j}(const uint32_t* __restrict__ Y, int w2, uint32_t* __restrict__ dst, int Lw) {{")
+        # W2 (the child product width) is a template parameter so that the
+        # row offsets k*W2*32 fold into the shared-memory load immediates
+        L.append(f"template <int W2> __device__ __forceinline__ void tg_row_{ps.name}_{j}(const uint32_t* __restrict__ Y, uint32_t* __restrict__ dst, int Lw) {{")
         L.append("  uint64_t acc = 0; uint32_t qp = 0;")
         if op.odiv != 1:
             L.append("  uint32_t bor = 0;")
-        for k, _ in idx:
-            L.append(f"  const uint32_t* __restrict__ y{k}p = Y + {k} * w2 * 32;")
         L.append("  #pragma unroll 2")
         L.append("  for (int t = 0; t <= Lw; ++t) {")
         L.append("    uint64_t lin = acc;")
+        L.append("    const uint32_t* __restrict__ yt = Y + t * 32;")
         for k, m in idx:
-            L.append(f"    const uint32_t y{k} = y{k}p[t * 32];")
+            L.append(f"    const uint32_t y{k} = yt[{k} * W2 * 32];")
         for k, m in idx:
             if m > 0:
                 L.append(f"    lin = tg_madw({m}u, y{k}, lin);")
@@ -863,6 +864,27 @@ def emit_evalrow_functions(ps: PointSet) -> str:
             else:
                 L.append(f"      lu = tg_msubw({-c}u, x, lu); lv = tg_msubw({-c}u, y, lv); }}")
         L.append("    dU[t * 32] = (uint32_t)lu; dV[t * 32] = (uint32_t)lv;")
+        L.append("    au = (uint64_t)((int64_t)lu >> 32); av = (uint64_t)((int64_t)lv >> 32);")
+        L.append("  }")
+        L.append("}")
+    # register versions (fully unrolled): the evaluated operands go straight
+    # into the product's register arrays
+    for k, (p, q) in enumerate(ps.points):
+        coef = [p**j * q ** (n - j) for j in range(ps.B)]
+        terms = [(j, c) for j, c in enumerate(coef) if c != 0]
+        L.append(f"template <int E> __device__ __forceinline__ void tg_evalreg_{ps.name}_{k}("
+                 "const uint32_t* __restrict__ PU, const uint32_t* __restrict__ PV, uint32_t (&a)[E], uint32_t (&b)[E]) {")
+        L.append("  uint64_t au = 0, av = 0;")
+        L.append("  #pragma unroll")
+        L.append("  for (int t = 0; t < E; ++t) {")
+        L.append("    uint64_t lu = au, lv = av;")
+        for j, c in terms:
+            L.append(f"    {{ const uint32_t x = PU[({j} * E + t) * 33], y = PV[({j} * E + t) * 33];")
+            if c > 0:
+                L.append(f"      lu = tg_madw({c}u, x, lu); lv = tg_madw({c}u, y, lv); }}")
+            else:
+                L.append(f"      lu = tg_msubw({-c}u, x, lu); lv = tg_msubw({-c}u, y, lv); }}")
+        L.append("    a[t] = (uint32_t)lu; b[t] = (uint32_t)lv;")
         L.append("    au = (uint64_t)((int64_t)lu >> 32); av = (uint64_t)((int64_t)lv >> 32);")
         L.append("  }")
         L.append("}")
