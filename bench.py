@@ -236,19 +236,21 @@ def main():
     lv = plan["levels"]
     pk, pk_kind = peaks()
     hbm_peak = pk.get("hbm_gbs")
-    lp_rate, _ = tg.probe_limb_products()
+    lp_wide, _ = tg.probe_limb_products()      # IMAD.WIDE.U32 + 64-bit accumulate chains
+    lp_chain, _ = tg.probe_carry_chain()       # the base case's mad.lo.cc/madc.hi.cc/addc sequence
+    lp_rate = max(lp_wide, lp_chain)
     L0, L1 = lv[0], lv[1]
     E = lv[-1]["n"]
     # per-launch algorithmic work of the three kernels of a C2 step:
     #   eval   (k_eval_top_rows<4>)   : read u, v; write the 7 evaluated pairs
     #   fused  (k_fused_bottom<4,18>) : 7 * E^2 limb-products per level-1 parent
-    #   interp (k_interp_top_stream<4>): read the 7 products; write w
+    #   interp (k_interp_top_smem<4>) : read the 7 products; write w
     kern = {
         "eval": dict(name="k_eval_top_rows<4>", bound="hbm",
                      units=2 * (L0["count"] * L0["n"] + L0["count"] * L0["npts"] * L0["e"]) * 4),
         "base": dict(name="k_fused_bottom<4,18>", bound="alu", units=L1["count"] * L1["npts"] * E * E,
                      bytes=(2 * L1["count"] * L1["n"] + L1["count"] * 2 * L1["n"]) * 4),
-        "interp": dict(name="k_interp_top_stream<4>", bound="hbm",
+        "interp": dict(name="k_interp_top_smem<4>", bound="hbm",
                        units=(L0["count"] * L0["npts"] * 2 * L0["e"] + L0["count"] * 2 * L0["n"]) * 4),
     }
     traffic = {}
@@ -272,8 +274,9 @@ def main():
                           "unit": "T limb-products/s", "frac": ach / lp_rate, "traffic": traffic.get(d["name"]),
                           "ms_per_launch": ms_l, "limb_products_per_launch": d["units"],
                           "hbm_GBps": d["bytes"] / (ms_l * 1e-3) / 1e9,
-                          "peak_kind": "measured live by toom_probe_limb_products (mad.lo.cc/madc.hi.cc/addc chains, "
-                                       "148 SMs x 8 CTAs)"}
+                          "peak_kind": "measured live: max of toom_probe_limb_products (IMAD.WIDE.U32 chains, "
+                                       "%.2f T LP/s) and toom_probe_carry_chain (mad.lo.cc/madc.hi.cc/addc, %.2f T LP/s), "
+                                       "148 SMs x 8 CTAs x 256 threads x 8 chains" % (lp_wide / 1e12, lp_chain / 1e12)}
     dominant = max(shares, key=shares.get)
     roofline = dict(kernels[dominant])
     roofline["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roofline["bound"] == "hbm" else "live probe") \

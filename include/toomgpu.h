@@ -132,11 +132,16 @@ int toom_profile_collect(double *ms, size_t *launches, int ncat);
  * (NUL-terminated); returns the length needed including the NUL, 0 on error. */
 size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t *plan, char *buf, size_t len);
 
-/* Microbenchmark of the integer-MAD limb-product rate (the base case's inner
- * operation: mad.lo.cc / madc.hi.cc / addc), used as the "alu" roofline
+/* Microbenchmark of the limb-product peak: the issue rate of the 32x32->64
+ * integer MAD (mad.wide.u32 -> IMAD.WIDE.U32; one limb-product each), 148 SMs
+ * x 8 CTAs x 256 threads x 8 independent chains.  Used as the "alu" roofline
  * peak.  Runs on `stream`, synchronizes, returns limb-products per second
  * (and the elapsed ms in *ms), or a negative value on error. */
 double toom_probe_limb_products(double *ms, void *stream);
+
+/* As above for the schoolbook kernel's own per-limb-product sequence
+ * (mad.lo.cc / madc.hi.cc / addc carry-flag chains), for context. */
+double toom_probe_carry_chain(double *ms, void *stream);
 
 /* Enable (default) or disable the fused bottom-level kernel (evaluation,
  * base-case products, interpolation and recomposition of the last Toom level

@@ -64,6 +64,7 @@ SIGNATURES = {
     "toom_profile_collect": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_size_t), _I]),
     "toom_plan_describe": (_SZ, [_SZ, _SZ, ctypes.POINTER(ToomPlan), ctypes.c_char_p, _SZ]),
     "toom_probe_limb_products": (ctypes.c_double, [ctypes.POINTER(ctypes.c_double), _P]),
+    "toom_probe_carry_chain": (ctypes.c_double, [ctypes.POINTER(ctypes.c_double), _P]),
     "toom_eval_points": (_I, [_P, _P, _SZ, _SZ, _I, _I, _P]),
     "toom_interp_recompose": (_I, [_P, _P, _SZ, _SZ, _I, _P]),
     "toom_mul_signed_batched": (_I, [_P, _P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
@@ -253,9 +254,19 @@ def profile_collect() -> dict:
 
 
 def probe_limb_products(stream=None) -> tuple:
-    """(limb-products/s, elapsed ms) of the integer-MAD peak probe."""
+    """(limb-products/s, elapsed ms) of the integer-MAD peak probe
+    (IMAD.WIDE.U32 issue rate)."""
     ms = ctypes.c_double(0)
     r = lib().toom_probe_limb_products(ctypes.byref(ms), _stream(stream))
+    if r < 0:
+        raise RuntimeError("probe failed")
+    return r, ms.value
+
+
+def probe_carry_chain(stream=None) -> tuple:
+    """(limb-products/s, elapsed ms) of the mad.lo.cc/madc.hi.cc/addc sequence."""
+    ms = ctypes.c_double(0)
+    r = lib().toom_probe_carry_chain(ctypes.byref(ms), _stream(stream))
     if r < 0:
         raise RuntimeError("probe failed")
     return r, ms.value

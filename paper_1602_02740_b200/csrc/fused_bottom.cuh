@@ -336,8 +336,11 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
         const uint32_t* Yl = Y + lane;
         uint32_t* dst = Wb + (warp * Lw) * G + lane;
         if (warp == 0 || warp == NP - 1) {
-            const uint32_t* src = Yl + (warp * 2 * E) * G;
-            for (int t = 0; t < Lw; ++t) dst[t * G] = src[t * G];
+            // MODE 0 reads w_0 = y_0 and w_2n = y_inf straight from the products
+            if constexpr (MODE != 0) {
+                const uint32_t* src = Yl + (warp * 2 * E) * G;
+                for (int t = 0; t < Lw; ++t) dst[t * G] = src[t * G];
+            }
         } else if constexpr (B == 3) {
             switch (warp) {
                 case 1: tg_row_T3_1<2 * E>(Yl, dst, Lw); break;
@@ -356,8 +359,90 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
     }
     __syncthreads();
 
-    // ---- phase C1: segment sums with local carries (OUT aliases Y)
     if (!(pmask & 4)) return;
+    if constexpr (MODE == 0) {
+        // ---- phase C (interleaved output): recompose w = sum_j w_j 2^(32 b j)
+        // segment by segment; the products stay intact (w_0, w_2n are read
+        // from them), so a carry-out pass, the carry resolution between
+        // segments and a final pass that writes straight to global memory.
+        auto rowp = [&](int j) -> const uint32_t* {
+            return (j == 0 || j == NP - 1) ? Y + (j * 2 * E) * G + lane : Wb + (j * Lw) * G + lane;
+        };
+        auto fillj = [&](int j) -> uint32_t { return rowp(j)[(Lw - 1) * G] >> 31; };
+        // segment s: limb r = w_s[r] + w_{s-1}[b + r] (+ w_{s-2}[2b] at r = 0)
+        // + the sign fills of the rows that have ended
+        auto seg = [&](int s, uint64_t cin, bool write, uint32_t* l0o, uint32_t* oneso) -> uint64_t {
+            uint32_t lowfills = 0, fillC = 0;
+            for (int j = 0; j <= s - 2 && j < NP; ++j) {
+                const uint32_t f = fillj(j);
+                if (j == s - 2) fillC = f;
+                else lowfills += f;
+            }
+            const bool hasA = s < NP, hasB = s >= 1 && s - 1 < NP, hasC = s >= 2 && s - 2 < NP;
+            const uint32_t* pA = hasA ? rowp(s) : nullptr;
+            const uint32_t* pB = hasB ? rowp(s - 1) + b * G : nullptr;
+            const int P0 = s * b;
+            const int len = min(b, wout - P0);
+            uint64_t x = cin + (uint64_t)lowfills * 0xFFFFFFFFull;
+            if (hasA) x += pA[0];
+            if (hasB) x += pB[0];
+            if (hasC) x += rowp(s - 2)[(2 * b) * G];
+            uint32_t lo = (uint32_t)x;
+            if (l0o) *l0o = lo;
+            if (write) out[(size_t)P0 * count + c] = lo;
+            uint64_t carry = x >> 32;
+            const uint64_t cc = (uint64_t)(lowfills + fillC) * 0xFFFFFFFFull;
+            uint32_t ones = 0xFFFFFFFFu;
+            if (hasA && hasB) {
+                for (int r = 1; r < len; ++r) {
+                    const uint64_t y = carry + cc + pA[r * G] + pB[r * G];
+                    lo = (uint32_t)y;
+                    if (write) out[(size_t)(P0 + r) * count + c] = lo;
+                    ones &= lo;
+                    carry = y >> 32;
+                }
+            } else {
+                for (int r = 1; r < len; ++r) {
+                    uint64_t y = carry + cc;
+                    if (hasA) y += pA[r * G];
+                    if (hasB) y += pB[r * G];
+                    lo = (uint32_t)y;
+                    if (write) out[(size_t)(P0 + r) * count + c] = lo;
+                    ones &= lo;
+                    carry = y >> 32;
+                }
+            }
+            if (oneso) *oneso = ones;
+            return carry;
+        };
+        if (valid) {
+            for (int s = warp; s < nseg; s += NP) {
+                uint32_t l0, ones;
+                const uint64_t cout = seg(s, 0, false, &l0, &ones);
+                CO[s * G + lane] = (uint32_t)cout;
+                L0[s * G + lane] = l0;
+                ON[s * G + lane] = (ones == 0xFFFFFFFFu) ? 1u : 0u;
+            }
+        }
+        __syncthreads();
+        if (valid && warp == 0) {
+            uint32_t cin = 0;
+            for (int s = 0; s < nseg; ++s) {
+                CI[s * G + lane] = cin;
+                uint32_t cout = CO[s * G + lane];
+                if (cin) {
+                    const uint32_t l0 = L0[s * G + lane];
+                    if (l0 + cin < l0 && ON[s * G + lane]) cout += 1;
+                }
+                cin = cout;
+            }
+        }
+        __syncthreads();
+        if (valid)
+            for (int s = warp; s < nseg; s += NP) seg(s, CI[s * G + lane], true, nullptr, nullptr);
+        return;
+    }
+    // ---- phase C1: segment sums with local carries (OUT aliases Y)
     uint32_t* OUT = Y;
     if (valid) {
         for (int s = warp; s < nseg; s += NP) {

@@ -518,7 +518,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
     plan.fused = false;
     if (plan.lv.size() >= 2 && !g_disable_fused && !plan.lv[plan.lv.size() - 2].lng) {
         const Level& Bt = plan.lv[plan.lv.size() - 2];
-        if ((Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
+        if ((Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.e == Bt.b + 1 && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
             2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e)
             plan.fused = true;
     }
