@@ -76,9 +76,10 @@ def lib():
     """Load libtoomgpu.so (built in-tree by build.py / __graft_entry__.build())."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            raise RuntimeError(f"libtoomgpu.so not built ({LIB}); run python -m paper_1602_02740_b200.build")
-        L = ctypes.CDLL(LIB)
+        path = os.environ.get("TOOM_LIB") or LIB   # experiments: an alternative build of the same sources
+        if not os.path.exists(path):
+            raise RuntimeError(f"libtoomgpu.so not built ({path}); run python -m paper_1602_02740_b200.build")
+        L = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             f = getattr(L, name)
             f.restype = res

@@ -22,6 +22,9 @@
 // Phases A and B are table driven (one code path for every point / row) so the
 // kernel stays small enough for the instruction cache.
 #pragma once
+#ifndef TG_FUSED_REG18
+#define TG_FUSED_REG18 64   // 64 registers: four CTAs per SM (measured 650 -> 596 us on C2)
+#endif
 
 namespace tg {
 
@@ -221,11 +224,19 @@ __device__ __forceinline__ void mul_signed_to_smem(uint32_t (&a)[E], uint32_t (&
 }
 
 // shared memory bytes for a launch (Y | W | per-segment carries)
-__host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nseg, int n) {
+// shared memory words of the W region (coefficient rows; the parents are
+// staged there first).  MODE 0 keeps only the interior rows 1..2B-3 (w_0 and
+// w_2n are read from the products) and two carry arrays, so that four CTAs
+// fit per SM.
+__host__ __device__ inline size_t fused_wreg(int B, int E, int Lw, int mode) {
     const int NP = 2 * B - 1;
-    size_t wreg = (size_t)NP * Lw * 32;
+    size_t wreg = (size_t)(mode == 0 ? NP - 2 : NP) * Lw * 32;
     if ((size_t)2 * B * E * 33 > wreg) wreg = (size_t)2 * B * E * 33;   // parents staged in the W region
-    return (size_t)4 * ((size_t)NP * 2 * E * 32 + wreg + 4 * 32 * (size_t)nseg);
+    return wreg;
+}
+__host__ __device__ inline size_t fused_smem_bytes(int B, int E, int Lw, int nseg, int n, int mode) {
+    const int NP = 2 * B - 1;
+    return (size_t)4 * ((size_t)NP * 2 * E * 32 + fused_wreg(B, E, Lw, mode) + (mode == 0 ? 2 : 4) * 32 * (size_t)nseg);
 }
 
 // diagnostic phase mask (bench/debug only; all phases by default): bit 0
@@ -241,15 +252,15 @@ __device__ int tg_fused_phase_mask = 7;
 // Output products: interleaved [2n][count] for MODE 0, row-major [count][2n]
 // otherwise.
 template <int B, int E, int MODE>
-__global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
+__global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : 128) k_fused_bottom(
     const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV, uint32_t* __restrict__ out,
     size_t count, int n, int b, int Lw, int wout, int nseg) {
     constexpr int NP = 2 * B - 1;
     constexpr int G = 32;
     extern __shared__ uint32_t sm[];
     uint32_t* Y = sm;                          // [NP][2E][G], later OUT [wout][G]
-    uint32_t* Wb = Y + NP * 2 * E * G;         // [NP][Lw][G]
-    const int wreg = (NP * Lw * G > 2 * B * E * 33) ? NP * Lw * G : 2 * B * E * 33;
+    uint32_t* Wb = Y + NP * 2 * E * G;         // [NP][Lw][G]  (MODE 0: [NP-2][Lw][G])
+    const int wreg = (int)fused_wreg(B, E, Lw, MODE);
     uint32_t* CO = Wb + wreg;                  // [nseg][G] segment carry-out
     uint32_t* L0 = CO + nseg * G;              // [nseg][G] limb 0 of the segment
     uint32_t* ON = L0 + nseg * G;              // [nseg][G] limbs 1.. all ones
@@ -334,7 +345,7 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
     // ---- phase B: coefficient w_warp (w_0 = y_0 and w_2n = y_inf are copies)
     if (valid && (pmask & 2)) {
         const uint32_t* Yl = Y + lane;
-        uint32_t* dst = Wb + (warp * Lw) * G + lane;
+        uint32_t* dst = Wb + ((MODE == 0 ? warp - 1 : warp) * Lw) * G + lane;
         if (warp == 0 || warp == NP - 1) {
             // MODE 0 reads w_0 = y_0 and w_2n = y_inf straight from the products
             if constexpr (MODE != 0) {
@@ -366,7 +377,7 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
         // from them), so a carry-out pass, the carry resolution between
         // segments and a final pass that writes straight to global memory.
         auto rowp = [&](int j) -> const uint32_t* {
-            return (j == 0 || j == NP - 1) ? Y + (j * 2 * E) * G + lane : Wb + (j * Lw) * G + lane;
+            return (j == 0 || j == NP - 1) ? Y + (j * 2 * E) * G + lane : Wb + ((j - 1) * Lw) * G + lane;
         };
         auto fillj = [&](int j) -> uint32_t { return rowp(j)[(Lw - 1) * G] >> 31; };
         // segment s: limb r = w_s[r] + w_{s-1}[b + r] (+ w_{s-2}[2b] at r = 0)
@@ -415,31 +426,33 @@ __global__ void __maxnreg__(E <= 18 ? 80 : 128) k_fused_bottom(
             if (oneso) *oneso = ones;
             return carry;
         };
+        // CO[s] = carry-out | (limbs 1.. all ones) << 31, later the resolved carry-in
+        uint32_t* L0c = CO + nseg * G;
         if (valid) {
             for (int s = warp; s < nseg; s += NP) {
                 uint32_t l0, ones;
                 const uint64_t cout = seg(s, 0, false, &l0, &ones);
-                CO[s * G + lane] = (uint32_t)cout;
-                L0[s * G + lane] = l0;
-                ON[s * G + lane] = (ones == 0xFFFFFFFFu) ? 1u : 0u;
+                CO[s * G + lane] = (uint32_t)cout | ((ones == 0xFFFFFFFFu) ? 0x80000000u : 0u);
+                L0c[s * G + lane] = l0;
             }
         }
         __syncthreads();
         if (valid && warp == 0) {
             uint32_t cin = 0;
             for (int s = 0; s < nseg; ++s) {
-                CI[s * G + lane] = cin;
-                uint32_t cout = CO[s * G + lane];
+                const uint32_t co = CO[s * G + lane];
+                uint32_t cout = co & 0x7FFFFFFFu;
                 if (cin) {
-                    const uint32_t l0 = L0[s * G + lane];
-                    if (l0 + cin < l0 && ON[s * G + lane]) cout += 1;
+                    const uint32_t l0 = L0c[s * G + lane];
+                    if (l0 + cin < l0 && (co >> 31)) cout += 1;
                 }
+                CO[s * G + lane] = cin;
                 cin = cout;
             }
         }
         __syncthreads();
         if (valid)
-            for (int s = warp; s < nseg; s += NP) seg(s, CI[s * G + lane], true, nullptr, nullptr);
+            for (int s = warp; s < nseg; s += NP) seg(s, CO[s * G + lane], true, nullptr, nullptr);
         return;
     }
     // ---- phase C1: segment sums with local carries (OUT aliases Y)

@@ -696,7 +696,7 @@ static toom_status launch_base(int E, const uint32_t* U, const uint32_t* V, uint
 template <int B, int E, int TOP>
 static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out, cudaStream_t st) {
     const int nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
-    const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg, Lv.n);
+    const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg, Lv.n, TOP);
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
         if (const char* m = getenv("TOOM_DBG_FUSED_MASK")) {   // diagnostics only

@@ -434,8 +434,11 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
             const int q4 = G >> 2, rp = 32 / q4;
             const int sub = lane / q4, q = lane - sub * q4;
             if (sub < rp) {
-                for (int R = warp * rp + sub; R < nrows; R += nw * rp) {
-                    const int k = R / ywidth, t = R - k * ywidth;
+                // row R = k * ywidth + t, advanced incrementally (no division)
+                const int stride = nw * rp;
+                int R = warp * rp + sub;
+                int k = R / ywidth, t = R - k * ywidth;
+                for (; R < nrows; R += stride) {
                     const uint32_t* sr = P1 + (size_t)t * S + (size_t)k * count + c0;
                     uint32_t* dr = Y + (size_t)R * G;
                     const int g = q * 4;
@@ -446,6 +449,8 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
 #pragma unroll
                         for (int x = 0; x < 4; ++x) dr[g + x] = (g + x < nin) ? __ldg(sr + g + x) : 0u;
                     }
+                    t += stride;
+                    while (t >= ywidth) { t -= ywidth; ++k; }
                 }
             }
         } else {
