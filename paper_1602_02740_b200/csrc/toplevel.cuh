@@ -514,6 +514,11 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     auto extraC = [&](int s) -> uint32_t {
         return (s >= 2 && s - 2 < NP) ? Y[(size_t)((s - 2) * ywidth + 2 * b) * G + lane] : 0u;
     };
+    // one pass: each segment is written with carry-in 0 (row-major, 16-byte
+    // stores); the resolved carry-ins are added afterwards (they rarely ripple
+    // past the segment's first limb)
+    uint32_t* row = w + (c0 + lane) * (size_t)wout;
+    const bool wr = act && lane < nin;
     if (act) {
         for (int s = warp; s < nseg; s += NP) {
             const int len = min(b, wout - s * b);
@@ -524,10 +529,26 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
             if (!pb) pb = zrow + lane;
             uint64_t carry = extraC(s);
             uint32_t ones = 0xFFFFFFFFu, l0 = 0;
-            for (int r = 0; r < len; ++r) {
+            int r = 0;
+            if (((s * b) & 3) == 0 && (wout & 3) == 0) {
+                for (; r + 4 <= len; r += 4) {
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t y = carry + pa[(r + q) * sa] + pb[(r + q) * sb];
+                        o[q] = (uint32_t)y;
+                        carry = y >> 32;
+                    }
+                    if (r == 0) l0 = o[0]; else ones &= o[0];
+                    ones &= o[1] & o[2] & o[3];
+                    if (wr) *reinterpret_cast<uint4*>(row + s * b + r) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
+            }
+            for (; r < len; ++r) {
                 const uint64_t y = carry + pa[r * sa] + pb[r * sb];
                 const uint32_t lo = (uint32_t)y;
                 if (r == 0) l0 = lo; else ones &= lo;
+                if (wr) row[s * b + r] = lo;
                 carry = y >> 32;
             }
             CO[s * G + lane] = (uint32_t)carry;
@@ -549,34 +570,15 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
         }
     }
     __syncthreads();
-    if (act && lane < nin) {
-        uint32_t* row = w + (c0 + lane) * (size_t)wout;
+    if (wr) {
         for (int s = warp; s < nseg; s += NP) {
+            uint32_t cin = CI[s * G + lane];
             const int len = min(b, wout - s * b);
-            const uint32_t* pa = rowA(s);
-            const uint32_t* pb = rowB(s);
-            const int sa = pa ? G : 0, sb = pb ? G : 0;
-            if (!pa) pa = zrow + lane;
-            if (!pb) pb = zrow + lane;
-            // carry-in of the segment; the w_{s-2}[2b] term enters at r = 0
-            uint64_t carry = (uint64_t)CI[s * G + lane] + extraC(s);
-            int r = 0;
-            if (((s * b) & 3) == 0 && (wout & 3) == 0) {
-                for (; r + 4 <= len; r += 4) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint64_t y = carry + pa[(r + q) * sa] + pb[(r + q) * sb];
-                        o[q] = (uint32_t)y;
-                        carry = y >> 32;
-                    }
-                    *reinterpret_cast<uint4*>(row + s * b + r) = make_uint4(o[0], o[1], o[2], o[3]);
-                }
-            }
-            for (; r < len; ++r) {
-                const uint64_t y = carry + pa[r * sa] + pb[r * sb];
-                row[s * b + r] = (uint32_t)y;
-                carry = y >> 32;
+            for (int r = 0; r < len && cin; ++r) {
+                const uint32_t x = row[s * b + r];
+                const uint32_t y = x + cin;
+                row[s * b + r] = y;
+                cin = (y < x) ? 1u : 0u;
             }
         }
     }
