@@ -749,6 +749,35 @@ def emit_row_tables(ps: PointSet) -> str:
     return "\n".join(L)
 
 
+def _lincomb_lines(terms, acc, out, ind="  "):
+    """C lines computing out = acc + sum_k m_k * y_k (mod 2^64) with the
+    products spread over up to four independent mad.wide chains (two for
+    positive, two for negative multipliers) instead of one serial chain, so
+    the multiply-adds of one limb overlap."""
+    pos = [(y, m) for y, m in terms if m > 0]
+    neg = [(y, -m) for y, m in terms if m < 0]
+    L = []
+    chains = []
+    for tag, grp in (("p", pos), ("n", neg)):
+        for c in range(2):
+            sub = grp[c::2]
+            if not sub:
+                continue
+            name = f"_{tag}{c}"
+            L.append(f"{ind}uint64_t {name} = 0ull;")
+            for y, m in sub:
+                L.append(f"{ind}{name} = tg_madw({m}u, {y}, {name});")
+            chains.append((tag, name))
+    # the carry from the previous limb enters last: it is the only input on the
+    # limb-to-limb critical path
+    expr = " + ".join([n for t, n in chains if t == "p"] + [acc])
+    negs = [n for t, n in chains if t == "n"]
+    if negs:
+        expr = f"({expr}) - ({' + '.join(negs)})"
+    L.append(f"{ind}const uint64_t {out} = {expr};")
+    return L
+
+
 def emit_row_functions(ps: PointSet) -> str:
     """Specialised per-coefficient streams for the fused kernel's phase B:
     w_j = (sum_k A_jk y_k) / (o_j 2^s_j) with immediate multipliers and only
@@ -773,15 +802,10 @@ def emit_row_functions(ps: PointSet) -> str:
             L.append("  uint32_t bor = 0;")
         L.append("  #pragma unroll 2")
         L.append("  for (int t = 0; t <= Lw; ++t) {")
-        L.append("    uint64_t lin = acc;")
         L.append("    const uint32_t* __restrict__ yt = Y + t * 32;")
         for k, m in idx:
             L.append(f"    const uint32_t y{k} = yt[{k} * W2 * 32];")
-        for k, m in idx:
-            if m > 0:
-                L.append(f"    lin = tg_madw({m}u, y{k}, lin);")
-            else:
-                L.append(f"    lin = tg_msubw({-m}u, y{k}, lin);")
+        L += _lincomb_lines([(f"y{k}", m) for k, m in idx], "acc", "lin", "    ")
         L.append("    acc = (uint64_t)((int64_t)lin >> 32);")
         if op.odiv != 1:
             L.append(f"    const uint32_t q = tg_divexact_step((uint32_t)lin, bor, 0x{_inv32(op.odiv):08X}u, {op.odiv}u);")
@@ -807,9 +831,7 @@ def emit_rowstep_functions(ps: PointSet) -> str:
         op = pr.ops[0]
         idx = [(pr.inputs.index(t.var), t.m) for t in op.terms]
         L.append(f"__device__ __forceinline__ uint32_t tg_rowstep_{ps.name}_{j}(const uint32_t (&y)[{NP}], tg_rowstate& st) {{")
-        L.append("  uint64_t lin = st.acc;")
-        for k, m in idx:
-            L.append(f"  lin = {'tg_madw' if m > 0 else 'tg_msubw'}({abs(m)}u, y[{k}], lin);")
+        L += _lincomb_lines([(f"y[{k}]", m) for k, m in idx], "st.acc", "lin", "  ")
         L.append("  st.acc = (uint64_t)((int64_t)lin >> 32);")
         if op.odiv != 1:
             L.append(f"  const uint32_t q = tg_divexact_step((uint32_t)lin, st.bor, 0x{_inv32(op.odiv):08X}u, {op.odiv}u);")
