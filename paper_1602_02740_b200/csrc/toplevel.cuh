@@ -32,19 +32,20 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
     const uint32_t* __restrict__ u, const uint32_t* __restrict__ v, uint32_t* __restrict__ U1,
     uint32_t* __restrict__ V1, size_t count, int n, int b, int e) {
     constexpr int NP = 2 * B - 1, G = 32, CH = TOP_CH, PP = 33;
-    __shared__ uint32_t S[2][B][CH][PP];
+    // double-buffered chunks of CH limbs of every block of the G products,
+    // filled with cp.async (zero-filled past a block's end) while the
+    // previous chunk is evaluated
+    __shared__ uint32_t S[2][2][B][CH][PP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t c0 = (size_t)blockIdx.x * G;
     const int nin = (int)min((size_t)G, count - c0);
     const size_t c = c0 + lane;
     const int lentop = n - (B - 1) * b;
-    uint64_t cf[B];
+    long long cf[B];
 #pragma unroll
-    for (int j = 0; j < B; ++j) cf[j] = (uint64_t)evalc<B>(warp, j);
+    for (int j = 0; j < B; ++j) cf[j] = evalc<B>(warp, j);
     const size_t stride_limb = (size_t)NP * count;
-    uint64_t au = 0, av = 0;
-    for (int t0 = 0; t0 < e; t0 += CH) {
-        // stage: (op, i, j, tt) with tt fastest -> coalesced row segments
+    auto stage = [&](int buf, int t0) {
         for (int idx = threadIdx.x; idx < 2 * G * B * CH; idx += blockDim.x) {
             const int tt = idx % CH;
             const int j = (idx / CH) % B;
@@ -52,25 +53,43 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
             const int op = idx / (CH * B * G);
             const int t = t0 + tt;
             const int len = (j == B - 1) ? lentop : b;
-            uint32_t x = 0;
-            if (i < nin && t < len) x = __ldg((op ? v : u) + (c0 + i) * (size_t)n + (size_t)j * b + t);
-            S[op][j][tt][i] = x;
+            const bool ok = i < nin && t < len;
+            const uint32_t* src = ok ? (op ? v : u) + (c0 + i) * (size_t)n + (size_t)j * b + t : u;
+            const unsigned d = (unsigned)__cvta_generic_to_shared(&S[buf][op][j][tt][i]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 4 : 0));
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    long long au = 0, av = 0;
+    const int nch = (e + CH - 1) / CH;
+    stage(0, 0);
+    for (int ci = 0; ci < nch; ++ci) {
+        const int t0 = ci * CH;
+        if (ci + 1 < nch) {
+            stage((ci + 1) & 1, t0 + CH);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
         if (lane < nin) {
-            const int tmax = min(CH, e - t0);
-            for (int tt = 0; tt < tmax; ++tt) {
-                uint64_t lu = au, lv = av;
+            const int buf = ci & 1;
+#pragma unroll 4
+            for (int tt = 0; tt < CH; ++tt) {
+                if (t0 + tt >= e) break;
+                long long lu = 0, lv = 0;
 #pragma unroll
                 for (int j = 0; j < B; ++j) {
-                    lu += cf[j] * (uint64_t)S[0][j][tt][lane];
-                    lv += cf[j] * (uint64_t)S[1][j][tt][lane];
+                    lu += cf[j] * (long long)S[buf][0][j][tt][lane];
+                    lv += cf[j] * (long long)S[buf][1][j][tt][lane];
                 }
+                lu += au;
+                lv += av;
                 const size_t o = (size_t)(t0 + tt) * stride_limb + (size_t)warp * count + c;
                 U1[o] = (uint32_t)lu;
                 V1[o] = (uint32_t)lv;
-                au = (uint64_t)((int64_t)lu >> 32);
-                av = (uint64_t)((int64_t)lv >> 32);
+                au = lu >> 32;
+                av = lv >> 32;
             }
         }
         __syncthreads();
