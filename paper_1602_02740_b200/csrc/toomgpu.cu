@@ -1355,7 +1355,7 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             ++t_launches;
             continue;
         }
-        if (l == 0 && top_rows_ok(Lv)) {
+        if (l == 0 && top_rows_ok(Lv) && g_top_stream != 4) {   // mode 4: the per-thread streaming kernel
             if ((s = launch_interp_top_rows(Lv, (const uint32_t*)(ws + Lv.offP), w, st))) return s;
             continue;
         }
