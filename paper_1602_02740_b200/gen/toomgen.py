@@ -651,7 +651,7 @@ def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None
         L.append(f"    // {op.dst} = ({' + '.join(f'{t.m}*{t.var}<<{t.s}' for t in op.terms)}) / {op.odiv << op.shr}   [{op.note}]")
         L.append(f"    uint32_t {dn}_h0;")
         L.append("    {")
-        L.append(f"      uint64_t lin = {dn}_acc;")
+        srcs = []
         for t in op.terms:
             if t.var == "ZERO":
                 continue
@@ -662,11 +662,9 @@ def emit_stream_function(prog: Program, fname: str, outputs=None, out_index=None
                 src = f"{vn}_h{lag}"
             else:
                 src = f"tg_shl_limb({vn}_h{lag}, {vn}_h{lag - 1}, {r})"
-            m = t.m
-            if m > 0:
-                L.append(f"      lin = tg_madw({m}u, {src}, lin);")
-            else:
-                L.append(f"      lin = tg_msubw({-m}u, {src}, lin);")
+            srcs.append((src, t.m))
+        # independent mad.wide chains, the carry of the previous limb last
+        L += _lincomb_lines(srcs, f"{dn}_acc", "lin", "      ")
         L.append(f"      uint32_t t = (uint32_t)lin;")
         L.append(f"      {dn}_acc = (uint64_t)((int64_t)lin >> 32);")
         if op.odiv != 1:
