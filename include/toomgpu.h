@@ -57,7 +57,8 @@ typedef enum {
  * long_count: which recursion levels run on the limb-parallel long-vector
  *        kernels (the upper levels of one large product: few, long
  *        operands); the levels below run one thread (or lane) per instance.
- *        0 = default: levels whose operands exceed 2048 limbs; 1 = never;
+ *        0 = default: levels whose operands exceed 2048 limbs (environment
+ *        overrides TOOM_LONG_MIN_N / TOOM_LONG_MAX_COUNT for tuning); 1 = never;
  *        k >= 2: levels with fewer than k instances.  Always a prefix of
  *        the recursion.                                                    */
 typedef struct {

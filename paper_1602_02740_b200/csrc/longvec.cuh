@@ -83,6 +83,13 @@ struct LMod {
     unsigned long long rcp;
 };
 __device__ __forceinline__ uint32_t lv_mod(unsigned long long x, const LMod& M) {
+    if (M.o < 32768u && x < 0x100000000ull) {
+        // 32-bit Barrett: rcp32 = floor((2^32 - 1) / o) derived from the 64-bit one
+        const uint32_t x32 = (uint32_t)x, r32 = (uint32_t)(M.rcp >> 32);
+        uint32_t r = x32 - __umulhi(x32, r32) * M.o;
+        while (r >= M.o) r -= M.o;
+        return r;
+    }
     const unsigned long long q = __umul64hi(x, M.rcp);
     unsigned long long r = x - q * M.o;
     while (r >= M.o) r -= M.o;

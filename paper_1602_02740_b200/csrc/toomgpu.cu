@@ -461,6 +461,12 @@ static int g_long_min_n = [] {
     const char* e = getenv("TOOM_LONG_MIN_N");
     return e ? atoi(e) : 2048;
 }();
+// ... and fewer than this many instances (many instances: one thread per
+// instance has parallelism enough, the per-tile scans of the long kernels cost more)
+static int g_long_max_count = [] {
+    const char* e = getenv("TOOM_LONG_MAX_COUNT");
+    return e ? atoi(e) : 8000;   // C5: 220 -> 150 ms (levels 4, 5 instance-parallel); C4 unchanged
+}();
 
 // one warp per product (k_interp_top_warp) needs the products row-major; CH
 // positions per lane, CH = ceil((2n+1)/32) rounded up to an instantiated size
@@ -507,7 +513,8 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         for (size_t l = 0; l + 1 < plan.lv.size(); ++l) {
             Level& L = plan.lv[l];
             const bool want = L.B == 16 || (top_long && l == 0) ||   // T16: no instance-parallel program
-                              (p.long_count == 0 ? (L.n > g_long_min_n) : (p.long_count > 1 && L.count < p.long_count));
+                              (p.long_count == 0 ? (L.n > g_long_min_n && L.count < (size_t)g_long_max_count)
+                                                 : (p.long_count > 1 && L.count < p.long_count));
             if (want && long_tables(L.B, T)) L.lng = true;
             else break;
         }
