@@ -665,6 +665,18 @@ static toom_status launch_interp(int B, bool top, const uint32_t* Pc, uint32_t* 
             else k_interp<4, false><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
             break;
         case 8:
+            // (top-interpolation mode 0 keeps the one-lane-per-half-program kernel)
+            if (top && g_top_stream != 0 && Lw == 2 * b + 1 && (size_t)Lw >= 3 * (size_t)((wout + b - 1) / b)) {
+                // rows in parallel (one thread per row and product), then the
+                // segment-parallel recomposition (row 0's scratch holds the carries)
+                const int nseg = (wout + b - 1) / b;
+                k_interp_rows_p8<<<nblk(14 * count), 128, 0, st>>>(Pc, W, count, ywidth, Lw);
+                k_recomp_seg<<<nblk((size_t)nseg * count), 128, 0, st>>>(Pc, W, out, W, count, 15, Lw, b, wout, nseg);
+                k_recomp_fix<<<nblk(count), 128, 0, st>>>(W, count, nseg);
+                k_recomp_apply<<<nblk((size_t)nseg * count), 128, 0, st>>>(out, W, count, b, wout, nseg);
+                t_launches += 3;
+                break;
+            }
             if (top) k_interp_p8<true><<<nblk(2 * count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
             else k_interp_p8<false><<<nblk(2 * count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
             break;

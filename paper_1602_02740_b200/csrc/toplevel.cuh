@@ -798,3 +798,153 @@ inline size_t interp_top_warp_smem(int B, int ywidth, int CH, int wpb) {
 }
 
 }  // namespace tg
+
+namespace tg {
+
+// ------------------------------------------------------------------------
+// Top-level interpolation of the paper's Toom-8 (C3) with one thread per
+// (coefficient row, product) instead of per product: the per-coefficient
+// rows w_j = (sum_k m_jk y_k) / (2^s_j o1_j o2_j) composed from the even-odd
+// + listing program (generator emit_bigrow_tables), streamed
+// LSB-first with a 64-bit carry, two 2-adic exact divisions by the odd word
+// factors and the exact right shift.  Rows go to the scratch W [NP][Lw][count]
+// (row 0 = y_0 is not copied); then the recomposition w = sum_j w_j 2^(32bj)
+// (Eq. 1.3) runs one thread per (segment, product) with carry-in 0, and one
+// thread per product resolves the segment carries and adds them.
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_interp_rows_p8(const uint32_t* __restrict__ P1, uint32_t* __restrict__ W,
+                                                         size_t count, int ywidth, int Lw) {
+    constexpr int NP = 15;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)(NP - 1) * count) return;
+    const int j = 1 + (int)(idx / count);
+    const size_t c = idx - (size_t)(j - 1) * count;
+    const size_t S = (size_t)NP * count;
+    const uint32_t* yb = P1 + c;
+    long long m[NP];
+    uint32_t fill[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        m[k] = tg_brow_m_P8[j][k];
+        fill[k] = (__ldg(yb + (size_t)(ywidth - 1) * S + (size_t)k * count) >> 31) ? 0xFFFFFFFFu : 0u;
+    }
+    const uint32_t o1 = tg_brow_o1_P8[j], o2 = tg_brow_o2_P8[j], i1 = tg_brow_i1_P8[j], i2 = tg_brow_i2_P8[j];
+    const int sh = tg_brow_s_P8[j], a = sh >> 5, r = sh & 31;
+    long long acc = 0;
+    uint32_t b1 = 0, b2 = 0, qp = 0;
+    uint32_t* dst = W + (size_t)j * Lw * count + c;
+    const int tend = Lw + a + (r ? 1 : 0);
+    // limbs of the 15 products, two limbs ahead in registers
+    auto ld = [&](int t, uint32_t (&y)[NP]) {
+        if (t < ywidth) {
+            const uint32_t* yt = yb + (size_t)t * S;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) y[k] = __ldg(yt + (size_t)k * count);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NP; ++k) y[k] = fill[k];
+        }
+    };
+    uint32_t y0[NP], y1[NP];
+    ld(0, y0);
+    ld(1, y1);
+#pragma unroll 1
+    for (int t = 0; t < tend; ++t) {
+        uint32_t y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) { y[k] = y0[k]; y0[k] = y1[k]; }
+        ld(t + 2, y1);
+        __int128 lin = acc;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) lin += (__int128)m[k] * (__int128)y[k];
+        acc = (long long)(lin >> 32);
+        uint32_t q = tg_divexact_step((uint32_t)lin, b1, i1, o1);
+        if (o2 > 1) q = tg_divexact_step(q, b2, i2, o2);
+        // quotient limb t; output limb u = t - a (r = 0) or t - a - 1 (r > 0)
+        const int u = t - a - (r ? 1 : 0);
+        if (u >= 0 && u < Lw) dst[(size_t)u * count] = r ? __funnelshift_r(qp, q, r) : q;
+        qp = q;
+    }
+}
+
+// recomposition pass 1: thread per (segment s, product c); carry-in 0; w_j >= 0
+// at the top level.  Writes the row-major output and, per segment, the
+// carry-out, limb 0 and whether limbs 1.. are all ones (into R[3][nseg][count]).
+__global__ void __launch_bounds__(128) k_recomp_seg(const uint32_t* __restrict__ P1, const uint32_t* __restrict__ W,
+                                                     uint32_t* __restrict__ w, uint32_t* __restrict__ R, size_t count,
+                                                     int NP, int Lw, int b, int wout, int nseg) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)nseg * count) return;
+    const int s = (int)(idx / count);
+    const size_t c = idx - (size_t)s * count;
+    const size_t S = (size_t)NP * count;
+    // limb t of w_j (w_0 = y_0 from the products)
+    auto wl = [&](int j, int t) -> uint32_t {
+        return j == 0 ? __ldg(P1 + (size_t)t * S + c) : __ldg(W + ((size_t)j * Lw + t) * count + c);
+    };
+    const int len = min(b, wout - s * b);
+    const bool hA = s < NP, hB = s >= 1 && s - 1 < NP, hC = s >= 2 && s - 2 < NP;
+    uint64_t carry = hC ? wl(s - 2, 2 * b) : 0;
+    uint32_t ones = 0xFFFFFFFFu, l0 = 0;
+    uint32_t* row = w + c * (size_t)wout + (size_t)s * b;
+    for (int r0 = 0; r0 < len; r0 += 4) {
+        uint32_t xa[4], xb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            xa[q] = (hA && r0 + q < len) ? wl(s, r0 + q) : 0u;
+            xb[q] = (hB && r0 + q < len) ? wl(s - 1, b + r0 + q) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (r0 + q < len) {
+                const uint64_t y = carry + xa[q] + xb[q];
+                const uint32_t lo = (uint32_t)y;
+                if (r0 + q == 0) l0 = lo; else ones &= lo;
+                row[r0 + q] = lo;
+                carry = y >> 32;
+            }
+        }
+    }
+    R[(size_t)s * count + c] = (uint32_t)carry;
+    R[((size_t)nseg + s) * count + c] = l0;
+    R[((size_t)2 * nseg + s) * count + c] = ones == 0xFFFFFFFFu;
+}
+
+// recomposition pass 2: thread per product: resolve the segment carries
+// (the carry-in of segment s replaces its carry-out in R)
+__global__ void __launch_bounds__(128) k_recomp_fix(uint32_t* __restrict__ R, size_t count, int nseg) {
+    const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    uint32_t cin = 0;
+    for (int s = 0; s < nseg; ++s) {
+        uint32_t cout = R[(size_t)s * count + c];
+        if (cin) {
+            const uint32_t l0 = R[((size_t)nseg + s) * count + c];
+            if (l0 + cin < l0 && R[((size_t)2 * nseg + s) * count + c]) cout += 1;
+        }
+        R[(size_t)s * count + c] = cin;
+        cin = cout;
+    }
+}
+
+// recomposition pass 3: thread per (segment, product): add the carry-in (it
+// ripples through all-ones limbs, e.g. the all-ones operands of C3)
+__global__ void __launch_bounds__(128) k_recomp_apply(uint32_t* __restrict__ w, const uint32_t* __restrict__ R,
+                                                       size_t count, int b, int wout, int nseg) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)nseg * count) return;
+    const int s = (int)(idx / count);
+    const size_t c = idx - (size_t)s * count;
+    uint32_t cc = R[(size_t)s * count + c];
+    if (!cc) return;
+    uint32_t* row = w + c * (size_t)wout + (size_t)s * b;
+    const int len = min(b, wout - s * b);
+    for (int r = 0; r < len && cc; ++r) {
+        const uint32_t x = row[r];
+        const uint32_t y = x + cc;
+        row[r] = y;
+        cc = (y < x) ? 1u : 0u;
+    }
+}
+
+}  // namespace tg

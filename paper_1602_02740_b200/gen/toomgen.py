@@ -1207,6 +1207,53 @@ def emit_long_tables(ps: PointSet) -> str:
     return "\n".join(lines)
 
 
+def emit_bigrow_tables(ps: PointSet) -> str:
+    """Per-coefficient rows of a point set whose row denominators exceed one
+    word (the paper's Toom-8 points): w_j = (sum_k m_jk y_k) / (2^s_j o1_j o2_j)
+    with word-sized odd factors o1, o2 (PAPER.md:162 matrix form composed from
+    the even-odd + listing program; exactness checked by Program.add)."""
+    it = build_interp(ps)
+    env = input_forms(it)
+    NP = ps.npoints
+    M, O1, O2, S = [], [], [], []
+    for j, v in enumerate(it.outputs):
+        f = env[v]
+        D = 1
+        for c in f.values():
+            D = _lcm(D, c.denominator)
+        row = [0] * NP
+        for k, c in f.items():
+            row[it.inputs.index(k)] = int(c * D)
+        s = (D & -D).bit_length() - 1
+        o = D >> s
+        fs = _word_factors(o) if o > 1 else [1]
+        assert len(fs) <= 2, (ps.name, j, fs)
+        fs = fs + [1] * (2 - len(fs))
+        assert sum(abs(m) for m in row) < (1 << 62)
+        M.append(row)
+        O1.append(fs[0])
+        O2.append(fs[1])
+        S.append(s)
+        # exactness of the composed row on the symbolic forms
+        tot = [0] * it.nunk
+        for k, m in enumerate(row):
+            fk = it.forms[it.inputs[k]]
+            for u in range(it.nunk):
+                tot[u] += m * fk[u]
+        assert all(x % D == 0 for x in tot) and [x // D for x in tot] == it.forms[v]
+    nm = ps.name
+    L = [f"// per-coefficient rows of {nm} (k_interp_rows_big)"]
+    L.append(f"TG_CONST long long tg_brow_m_{nm}[{NP}][{NP}] = {{" +
+             ", ".join("{" + ", ".join(f"{x}ll" for x in r) + "}" for r in M) + "};")
+    L.append(f"TG_CONST unsigned tg_brow_o1_{nm}[{NP}] = {{" + ", ".join(f"{x}u" for x in O1) + "};")
+    L.append(f"TG_CONST unsigned tg_brow_o2_{nm}[{NP}] = {{" + ", ".join(f"{x}u" for x in O2) + "};")
+    L.append(f"TG_CONST unsigned tg_brow_i1_{nm}[{NP}] = {{" + ", ".join(f"0x{_inv32(x):08X}u" for x in O1) + "};")
+    L.append(f"TG_CONST unsigned tg_brow_i2_{nm}[{NP}] = {{" + ", ".join(f"0x{_inv32(x):08X}u" for x in O2) + "};")
+    L.append(f"TG_CONST int tg_brow_s_{nm}[{NP}] = {{" + ", ".join(str(x) for x in S) + "};")
+    L.append(f"constexpr int tg_brow_maxs_{nm} = {max(S)};")
+    return "\n".join(L)
+
+
 LONG_HEADER = """
 // one term m * (src << s) of a long-vector op; src >= 0 slot, src < 0 input -(k+1)
 struct tg_lterm { int src; int s; long long m; };
@@ -1245,6 +1292,7 @@ def generate_all():
             parts.append(emit_rowstep_functions(ps))
             parts.append("#endif")
         meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
+    parts.append(emit_bigrow_tables(pointset_paper(8)))
     parts.append(LONG_HEADER)
     for ps in [pointset_T3(), pointset_T4(), pointset_paper(8), pointset_T16_31()]:
         parts.append(emit_long_tables(ps))

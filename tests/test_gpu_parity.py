@@ -429,3 +429,27 @@ def test_top_stream_vs_rows(B, n, t4, t3):
             assert np.array_equal(got, want), mode
     finally:
         tg.set_top_stream(2)
+
+
+@pytest.mark.parametrize("n", [2048, 1500, 777])
+def test_p8_top_rows_vs_half_programs(n):
+    """C3's top level (the paper's Toom-8 points): the row-parallel
+    interpolation + segment recomposition against the one-lane-per-half
+    streaming kernel and the oracle."""
+    rng = np.random.default_rng(n)
+    batch = 40
+    u = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    v = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    u[0] = 0xFFFFFFFF
+    v[0] = 0xFFFFFFFF
+    u[1, 1::2] = 0xFFFFFFFF
+    u[1, ::2] = 0
+    v[1] = u[1]
+    want = oracle.schoolbook_batched(u, v)
+    try:
+        for mode in (0, 2):
+            tg.set_top_stream(mode)
+            got = run_batched(u, v, 8, long_count=1)
+            assert np.array_equal(got, want), mode
+    finally:
+        tg.set_top_stream(2)
