@@ -765,7 +765,8 @@ static toom_status launch_eval_top_rows(const Level& Lv, const uint32_t* u, cons
     ProfScope ps(CAT_EVAL, st);
     const unsigned grid = (unsigned)((Lv.count + 31) / 32);
     if (Lv.B == 3) k_eval_top_rows<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
-    else k_eval_top_rows<4><<<grid, 32 * 7, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
+    else if (Lv.B == 4) k_eval_top_rows<4><<<grid, 32 * 7, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
+    else k_eval_top_rows<8><<<grid, 32 * 15, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     ps.done(st);
     ++t_launches;
     return TOOM_OK;
@@ -1337,7 +1338,7 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         const Level& Lv = plan.lv[l];
         const uint32_t* su = l == 0 ? u : (const uint32_t*)(ws + plan.lv[l - 1].offU);
         const uint32_t* sv = l == 0 ? v : (const uint32_t*)(ws + plan.lv[l - 1].offV);
-        if (l == 0 && top_rows_ok(Lv)) {
+        if (l == 0 && top_rows_ok(Lv)) {   // (B = 8 via k_eval_top_rows<8> measured slower: 128 CTAs for C3)
             if ((s = launch_eval_top_rows(Lv, su, sv, (uint32_t*)(ws + Lv.offU), (uint32_t*)(ws + Lv.offV), st)))
                 return s;
             continue;

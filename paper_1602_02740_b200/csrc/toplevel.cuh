@@ -31,7 +31,9 @@ template <int B>
 __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
     const uint32_t* __restrict__ u, const uint32_t* __restrict__ v, uint32_t* __restrict__ U1,
     uint32_t* __restrict__ V1, size_t count, int n, int b, int e) {
-    constexpr int NP = 2 * B - 1, G = 32, CH = TOP_CH, PP = 33;
+    constexpr int NP = 2 * B - 1, G = 32, CH = (B == 8 ? 8 : TOP_CH), PP = 33;
+    // (B = 8: the paper's points 0, +-2^i; values up to 2^42 u_j need 128-bit sums)
+    using Acc = typename std::conditional<B == 8, __int128, long long>::type;
     // double-buffered chunks of CH limbs of every block of the G products,
     // filled with cp.async (zero-filled past a block's end) while the
     // previous chunk is evaluated
@@ -42,8 +44,17 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
     const size_t c = c0 + lane;
     const int lentop = n - (B - 1) * b;
     long long cf[B];
+    if constexpr (B == 8) {
+        // point 0 -> u_0; point 2i+1 -> +2^i; point 2i+2 -> -2^i (pointset_paper)
+        const int i = (warp - 1) >> 1;
+        const bool neg = warp > 0 && !(warp & 1);
 #pragma unroll
-    for (int j = 0; j < B; ++j) cf[j] = evalc<B>(warp, j);
+        for (int j = 0; j < B; ++j)
+            cf[j] = warp == 0 ? (j == 0 ? 1ll : 0ll) : ((neg && (j & 1)) ? -(1ll << (i * j)) : (1ll << (i * j)));
+    } else {
+#pragma unroll
+        for (int j = 0; j < B; ++j) cf[j] = evalc<B>(warp, j);
+    }
     const size_t stride_limb = (size_t)NP * count;
     auto stage = [&](int buf, int t0) {
         for (int idx = threadIdx.x; idx < 2 * G * B * CH; idx += blockDim.x) {
@@ -60,7 +71,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    long long au = 0, av = 0;
+    Acc au = 0, av = 0;
     const int nch = (e + CH - 1) / CH;
     stage(0, 0);
     for (int ci = 0; ci < nch; ++ci) {
@@ -77,11 +88,11 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
 #pragma unroll 4
             for (int tt = 0; tt < CH; ++tt) {
                 if (t0 + tt >= e) break;
-                long long lu = 0, lv = 0;
+                Acc lu = 0, lv = 0;
 #pragma unroll
                 for (int j = 0; j < B; ++j) {
-                    lu += cf[j] * (long long)S[buf][0][j][tt][lane];
-                    lv += cf[j] * (long long)S[buf][1][j][tt][lane];
+                    lu += (Acc)cf[j] * (Acc)S[buf][0][j][tt][lane];
+                    lv += (Acc)cf[j] * (Acc)S[buf][1][j][tt][lane];
                 }
                 lu += au;
                 lv += av;
