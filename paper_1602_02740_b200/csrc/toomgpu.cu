@@ -657,12 +657,32 @@ static toom_status launch_interp(int B, bool top, const uint32_t* Pc, uint32_t* 
     ProfScope ps(CAT_INTERP, st);
     switch (B) {
         case 3:
+        case 4:
+            // batched Toom-3/4 levels: row-parallel interpolation + segment
+            // recomposition only in top-interpolation mode 4 (measured slower
+            // than the per-thread programs at C2-C5's shapes: every row re-reads
+            // all 2B-1 products)
+            if (g_top_stream == 4 && Lw == 2 * b + 1 && (size_t)Lw >= 3 * (size_t)((wout + b - 1) / b) && ywidth > Lw) {
+                // rows in parallel (one thread per interior row and product) +
+                // segment-parallel recomposition; W row 0 holds the segment carries
+                const int nseg = (wout + b - 1) / b, NP = 2 * B - 1;
+                if (B == 3) k_interp_rows_w<3><<<nblk((size_t)(NP - 2) * count), 128, 0, st>>>(Pc, W, count, ywidth, Lw);
+                else k_interp_rows_w<4><<<nblk((size_t)(NP - 2) * count), 128, 0, st>>>(Pc, W, count, ywidth, Lw);
+                RecompArgs A{Pc, W, out, top ? (long long)wout : 1, top ? 1 : (long long)count, W, count, NP, Lw, b, wout,
+                             nseg, 1};
+                k_recomp_seg<<<nblk((size_t)nseg * count), 128, 0, st>>>(A);
+                k_recomp_fix<<<nblk(count), 128, 0, st>>>(W, count, nseg);
+                k_recomp_apply<<<nblk((size_t)nseg * count), 128, 0, st>>>(A);
+                t_launches += 3;
+                break;
+            }
+            if (B == 4) {
+                if (top) k_interp<4, true><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
+                else k_interp<4, false><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
+                break;
+            }
             if (top) k_interp<3, true><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
             else k_interp<3, false><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
-            break;
-        case 4:
-            if (top) k_interp<4, true><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
-            else k_interp<4, false><<<nblk(count), 128, 0, st>>>(Pc, W, out, count, ywidth, Lw, b, wout);
             break;
         case 8:
             // (top-interpolation mode 0 keeps the one-lane-per-half-program kernel)
@@ -671,9 +691,10 @@ static toom_status launch_interp(int B, bool top, const uint32_t* Pc, uint32_t* 
                 // segment-parallel recomposition (row 0's scratch holds the carries)
                 const int nseg = (wout + b - 1) / b;
                 k_interp_rows_p8<<<nblk(14 * count), 128, 0, st>>>(Pc, W, count, ywidth, Lw);
-                k_recomp_seg<<<nblk((size_t)nseg * count), 128, 0, st>>>(Pc, W, out, W, count, 15, Lw, b, wout, nseg);
+                RecompArgs A{Pc, W, out, (long long)wout, 1, W, count, 15, Lw, b, wout, nseg, 0};
+                k_recomp_seg<<<nblk((size_t)nseg * count), 128, 0, st>>>(A);
                 k_recomp_fix<<<nblk(count), 128, 0, st>>>(W, count, nseg);
-                k_recomp_apply<<<nblk((size_t)nseg * count), 128, 0, st>>>(out, W, count, b, wout, nseg);
+                k_recomp_apply<<<nblk((size_t)nseg * count), 128, 0, st>>>(A);
                 t_launches += 3;
                 break;
             }

@@ -878,26 +878,52 @@ __global__ void __launch_bounds__(128) k_interp_rows_p8(const uint32_t* __restri
     }
 }
 
-// recomposition pass 1: thread per (segment s, product c); carry-in 0; w_j >= 0
-// at the top level.  Writes the row-major output and, per segment, the
-// carry-out, limb 0 and whether limbs 1.. are all ones (into R[3][nseg][count]).
-__global__ void __launch_bounds__(128) k_recomp_seg(const uint32_t* __restrict__ P1, const uint32_t* __restrict__ W,
-                                                     uint32_t* __restrict__ w, uint32_t* __restrict__ R, size_t count,
-                                                     int NP, int Lw, int b, int wout, int nseg) {
+// recomposition pass 1: thread per (segment s, product c), carry-in 0.
+// Coefficient j: w_0 = y_0 and (last_copy) w_{NP-1} = y_inf come from the
+// products (interleaved [ywidth][NP*count]), the others from W [NP][Lw][count];
+// every w_j is an exact two's-complement value of Lw limbs (sign-extended past
+// them: below the top level they can be negative).  Segment s limb r sums
+// w_s[r] + w_{s-1}[b + r] + w_{s-2}[2b + r] (+ the fills of the rows that have
+// ended); the output limb goes to out[c*out_is + t*out_ls]; R[3][nseg][count]
+// receives the carry-out, limb 0 and whether limbs 1.. are all ones.
+struct RecompArgs {
+    const uint32_t* P1;
+    const uint32_t* W;
+    uint32_t* out;
+    long long out_is, out_ls;
+    uint32_t* R;
+    size_t count;
+    int NP, Lw, b, wout, nseg, last_copy;
+};
+
+__global__ void __launch_bounds__(128) k_recomp_seg(RecompArgs A) {
+    const size_t count = A.count;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)nseg * count) return;
+    if (idx >= (size_t)A.nseg * count) return;
     const int s = (int)(idx / count);
     const size_t c = idx - (size_t)s * count;
+    const int NP = A.NP, Lw = A.Lw, b = A.b;
     const size_t S = (size_t)NP * count;
-    // limb t of w_j (w_0 = y_0 from the products)
+    auto fromY = [&](int j) { return j == 0 || (A.last_copy && j == NP - 1); };
     auto wl = [&](int j, int t) -> uint32_t {
-        return j == 0 ? __ldg(P1 + (size_t)t * S + c) : __ldg(W + ((size_t)j * Lw + t) * count + c);
+        return fromY(j) ? __ldg(A.P1 + (size_t)t * S + (size_t)j * count + c) : __ldg(A.W + ((size_t)j * Lw + t) * count + c);
     };
-    const int len = min(b, wout - s * b);
+    auto fillj = [&](int j) -> uint32_t { return wl(j, Lw - 1) >> 31; };
+    uint32_t lowfills = 0, fillC = 0;
+    for (int j = 0; j <= s - 2 && j < NP; ++j) {
+        const uint32_t f = fillj(j);
+        if (j == s - 2) fillC = f;
+        else lowfills += f;
+    }
+    const int len = min(b, A.wout - s * b);
     const bool hA = s < NP, hB = s >= 1 && s - 1 < NP, hC = s >= 2 && s - 2 < NP;
-    uint64_t carry = hC ? wl(s - 2, 2 * b) : 0;
+    // per-limb constants: limb 0 gets the ended rows' fills and w_{s-2}[2b];
+    // limbs 1.. also the fill of w_{s-2} (its last limb is 2b)
+    const uint64_t k0 = (uint64_t)lowfills * 0xFFFFFFFFull + (hC ? wl(s - 2, 2 * b) : 0u);
+    const uint64_t k1 = (uint64_t)(lowfills + fillC) * 0xFFFFFFFFull;
+    uint64_t carry = 0;
     uint32_t ones = 0xFFFFFFFFu, l0 = 0;
-    uint32_t* row = w + c * (size_t)wout + (size_t)s * b;
+    uint32_t* o = A.out + (long long)c * A.out_is + (long long)s * b * A.out_ls;
     for (int r0 = 0; r0 < len; r0 += 4) {
         uint32_t xa[4], xb[4];
 #pragma unroll
@@ -908,17 +934,17 @@ __global__ void __launch_bounds__(128) k_recomp_seg(const uint32_t* __restrict__
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (r0 + q < len) {
-                const uint64_t y = carry + xa[q] + xb[q];
+                const uint64_t y = carry + xa[q] + xb[q] + (r0 + q > 0 ? k1 : k0);
                 const uint32_t lo = (uint32_t)y;
                 if (r0 + q == 0) l0 = lo; else ones &= lo;
-                row[r0 + q] = lo;
+                o[(long long)(r0 + q) * A.out_ls] = lo;
                 carry = y >> 32;
             }
         }
     }
-    R[(size_t)s * count + c] = (uint32_t)carry;
-    R[((size_t)nseg + s) * count + c] = l0;
-    R[((size_t)2 * nseg + s) * count + c] = ones == 0xFFFFFFFFu;
+    A.R[(size_t)s * count + c] = (uint32_t)carry;
+    A.R[((size_t)A.nseg + s) * count + c] = l0;
+    A.R[((size_t)2 * A.nseg + s) * count + c] = ones == 0xFFFFFFFFu;
 }
 
 // recomposition pass 2: thread per product: resolve the segment carries
@@ -940,21 +966,65 @@ __global__ void __launch_bounds__(128) k_recomp_fix(uint32_t* __restrict__ R, si
 
 // recomposition pass 3: thread per (segment, product): add the carry-in (it
 // ripples through all-ones limbs, e.g. the all-ones operands of C3)
-__global__ void __launch_bounds__(128) k_recomp_apply(uint32_t* __restrict__ w, const uint32_t* __restrict__ R,
-                                                       size_t count, int b, int wout, int nseg) {
+__global__ void __launch_bounds__(128) k_recomp_apply(RecompArgs A) {
+    const size_t count = A.count;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)nseg * count) return;
+    if (idx >= (size_t)A.nseg * count) return;
     const int s = (int)(idx / count);
     const size_t c = idx - (size_t)s * count;
-    uint32_t cc = R[(size_t)s * count + c];
+    uint32_t cc = A.R[(size_t)s * count + c];
     if (!cc) return;
-    uint32_t* row = w + c * (size_t)wout + (size_t)s * b;
-    const int len = min(b, wout - s * b);
+    uint32_t* o = A.out + (long long)c * A.out_is + (long long)s * A.b * A.out_ls;
+    const int len = min(A.b, A.wout - s * A.b);
     for (int r = 0; r < len && cc; ++r) {
-        const uint32_t x = row[r];
+        const uint32_t x = o[(long long)r * A.out_ls];
         const uint32_t y = x + cc;
-        row[r] = y;
+        o[(long long)r * A.out_ls] = y;
         cc = (y < x) ? 1u : 0u;
+    }
+}
+
+// Toom-3/4 coefficient rows, one thread per (row j in 1..NP-2, product):
+// w_j = (sum_k A_jk y_k) / (o_j 2^s_j) streamed LSB-first (the generated row
+// steps), y_k from the interleaved products two limbs ahead in registers,
+// w_j to W [NP][Lw][count].  With k_recomp_* this is the row-parallel
+// interpolation + recomposition of a batched level.
+template <int B>
+__global__ void __launch_bounds__(128) k_interp_rows_w(const uint32_t* __restrict__ P1, uint32_t* __restrict__ W,
+                                                        size_t count, int ywidth, int Lw) {
+    constexpr int NP = 2 * B - 1;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)(NP - 2) * count) return;
+    const int j = 1 + (int)(idx / count);
+    const size_t c = idx - (size_t)(j - 1) * count;
+    const size_t S = (size_t)NP * count;
+    const uint32_t* yb = P1 + c;
+    uint32_t fill[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) fill[k] = (__ldg(yb + (size_t)(ywidth - 1) * S + (size_t)k * count) >> 31) ? 0xFFFFFFFFu : 0u;
+    auto ld = [&](int t, uint32_t (&y)[NP]) {
+        if (t < ywidth) {
+            const uint32_t* yt = yb + (size_t)t * S;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) y[k] = __ldg(yt + (size_t)k * count);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NP; ++k) y[k] = fill[k];
+        }
+    };
+    uint32_t* dst = W + (size_t)j * Lw * count + c;
+    tg_rowstate st{0, 0, 0};
+    uint32_t y0[NP], y1[NP];
+    ld(0, y0);
+    ld(1, y1);
+#pragma unroll 1
+    for (int t = 0; t <= Lw; ++t) {
+        uint32_t y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) { y[k] = y0[k]; y0[k] = y1[k]; }
+        ld(t + 2, y1);
+        const uint32_t r = rowstep<B>(j, y, st);
+        if (t >= 1) dst[(size_t)(t - 1) * count] = r;
     }
 }
 

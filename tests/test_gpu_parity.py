@@ -423,7 +423,7 @@ def test_top_stream_vs_rows(B, n, t4, t3):
     u[1] = 0
     want = oracle.schoolbook_batched(u, v)
     try:
-        for mode in (0, 1, 2, 3):
+        for mode in (0, 1, 2, 3, 4):
             tg.set_top_stream(mode)
             got = run_batched(u, v, B, t4=t4, t3=t3, long_count=1)
             assert np.array_equal(got, want), mode
@@ -450,6 +450,30 @@ def test_p8_top_rows_vs_half_programs(n):
         for mode in (0, 2):
             tg.set_top_stream(mode)
             got = run_batched(u, v, 8, long_count=1)
+            assert np.array_equal(got, want), mode
+    finally:
+        tg.set_top_stream(2)
+
+
+@pytest.mark.parametrize("B,n,t4,t3", [(4, 1026, 256, 64), (3, 300, 64, 64), (4, 4100, 256, 64), (3, 66, 10, 10)])
+def test_rows_interp_lower_levels(B, n, t4, t3):
+    """Signed lower levels: the row-parallel interpolation + segment
+    recomposition (sign fills of negative coefficients) against the
+    per-thread streaming programs (mode 0) and the oracle."""
+    rng = np.random.default_rng(n * 5 + B)
+    batch = 50
+    u = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    v = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    u[0] = 0xFFFFFFFF
+    v[0] = 0xFFFFFFFF
+    u[1, ::2] = 0
+    u[2] = 0
+    u[2, -1] = 1
+    want = oracle.schoolbook_batched(u, v)
+    try:
+        for mode in (0, 2, 4):
+            tg.set_top_stream(mode)   # 4: row-parallel lower levels
+            got = run_batched(u, v, B, t4=t4, t3=t3, long_count=1)
             assert np.array_equal(got, want), mode
     finally:
         tg.set_top_stream(2)
