@@ -477,3 +477,43 @@ def test_rows_interp_lower_levels(B, n, t4, t3):
             assert np.array_equal(got, want), mode
     finally:
         tg.set_top_stream(2)
+
+
+def test_host_buffer_entry_point():
+    """toom_mul_batched_host (bench.py's e2e path): host buffers in and out,
+    copies and the multiplication in one C call."""
+    u, v = synth.config_inputs(2, batch=500, first=777)
+    w = tg.toom_mul_batched_host(u, v, B=4, t4=32, t3=32)
+    assert np.array_equal(w, oracle.toom_batched(u, v, top_B=4, threads=8))
+
+
+def test_workspace_user_provided():
+    """toom_set_workspace: a caller-owned buffer is used (and a too-small one
+    is an error, not a silent reallocation)."""
+    u, v = synth.config_inputs(2, batch=300)
+    need = tg.workspace_bytes(256, 300, B=4, t4=32, t3=32)
+    buf = torch.empty(need // 4 + 64, dtype=torch.int32, device="cuda")
+    try:
+        tg.lib().toom_set_workspace(buf.data_ptr(), buf.numel() * 4)
+        w = run_batched(u, v, 4, t4=32, t3=32)
+        assert np.array_equal(w, oracle.toom_batched(u, v, top_B=4, threads=8))
+        tg.lib().toom_set_workspace(buf.data_ptr(), 1024)
+        with pytest.raises(tg.ToomError) as ei:
+            run_batched(u, v, 4, t4=32, t3=32)
+        assert ei.value.status == tg.TOOM_ENOMEM
+    finally:
+        tg.lib().toom_set_workspace(None, 0)
+    assert np.array_equal(run_batched(u, v, 4, t4=32, t3=32), oracle.toom_batched(u, v, top_B=4, threads=8))
+
+
+def test_streams_and_repeat_determinism():
+    """The same call on a side stream and repeated calls give identical
+    limbs (positional results; no schedule dependence)."""
+    u, v = synth.config_inputs(3, batch=64, first=3000)
+    a = run_batched(u, v, 8)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        w = tg.toom_mul_batched(dev(u), dev(v), B=8, stream=s)
+    s.synchronize()
+    assert np.array_equal(a, host(w))
+    assert np.array_equal(a, run_batched(u, v, 8))
