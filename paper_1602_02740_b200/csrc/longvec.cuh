@@ -212,9 +212,14 @@ struct LTileSmem {
 // local normalisation of the tile's linear combination, carry / borrow scan
 // (warp shuffles + decoupled look-back), exact limbs, exact division, right
 // shift, coalesced store.  lin: this thread's CH positions p0 = tstart + tid*CH.
+// phase: 0 = single pass with the decoupled look-back; two-pass scan for long
+// vectors of many tiles: 1 = publish the tile aggregate and stop (k_long_scan
+// then writes every tile's carry-in / borrow-in), 2 = read the tile's in-state
+// and finish.
 template <typename Acc, int CH, class HaloF>
 __device__ __forceinline__ void lv_finish(const Acc (&lin)[CH], const LMod& M, const LFinish& P, unsigned epoch,
-                                          unsigned tile, int k, int tstart, LTileSmem& sh, uint32_t* Q, HaloF halo_fn) {
+                                          unsigned tile, int k, int tstart, LTileSmem& sh, uint32_t* Q, HaloF halo_fn,
+                                          int phase = 0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5, TL = NT * CH;
     const uint32_t o = M.o;
@@ -271,7 +276,20 @@ __device__ __forceinline__ void lv_finish(const Acc (&lin)[CH], const LMod& M, c
     // tile aggregate, published before the look-back
     const bool first = (k == 0);
     LStatus* st = P.st_base + (long long)tile * P.st_stride;
-    if (warp == 0) {
+    if (phase == 1) {
+        if (warp == 0 && lane == 0) {
+            LAgg T = s_wagg[0];
+            for (int w = 1; w < NW; ++w) T = lv_compose(T, s_wagg[w], M);
+            st->agg = T;
+        }
+        return;
+    }
+    if (phase == 2) {
+        if (tid == 0) {
+            s_c = first ? 0 : st->c;
+            s_beta = first ? 0u : st->beta;
+        }
+    } else if (warp == 0) {
         LAgg T = s_wagg[0];
         for (int w = 1; w < NW; ++w) T = lv_compose(T, s_wagg[w], M);
         long long cin = 0;
@@ -406,7 +424,7 @@ __device__ __forceinline__ void lv_finish(const Acc (&lin)[CH], const LMod& M, c
 
 template <bool WIDE, int CH>
 __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ opp, LStatus* __restrict__ status,
-                                                   unsigned epoch, unsigned* __restrict__ tile_ctr) {
+                                                   unsigned epoch, unsigned* __restrict__ tile_ctr, int phase) {
     using Acc = typename std::conditional<WIDE, __int128, long long>::type;
     // the op descriptor (terms included) is cached in shared memory
     __shared__ __align__(16) LOpDev s_op;
@@ -422,7 +440,9 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
     extern __shared__ uint32_t Q[];               // [NT * CH + halo] quotient limbs
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5, TL = NT * CH;   // NT: a multiple of 32, <= LV_NT
-    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    // single pass: dynamic tile ids (the look-back needs its predecessors
+    // scheduled); two-pass phases: the block index
+    if (tid == 0) s_tile = phase ? blockIdx.x : atomicAdd(tile_ctr, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
     const long long inst = tile / op.tiles_per_inst;
@@ -499,7 +519,70 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
     lv_finish<Acc, CH>(lin, M, LFinish{op.oinv, op.p32, op.Mch, op.mi, op.sa, op.sr, op.W, status, 1,
                                         op.dst + inst * op.dst_inst_stride, op.dst_limb_stride},
                        epoch, tile, k, tstart, s_sh, Q,
-                       [&](Acc (&hl)[LV_MAXHALO]) { lv_lincomb<Acc, LV_MAXHALO>(op, nt, inst, tstart + TL, hl); });
+                       [&](Acc (&hl)[LV_MAXHALO]) { lv_lincomb<Acc, LV_MAXHALO>(op, nt, inst, tstart + TL, hl); },
+                       phase);
+}
+
+// two-pass scan, pass 2: one CTA per instance turns the tile aggregates into
+// every tile's carry-in / borrow-in (status[tile].c / .beta).  Thread t owns a
+// contiguous run of tiles; runs are composed with a warp scan and the warps'
+// totals are chained by warp 0.
+__global__ void __launch_bounds__(1024) k_long_scan(LStatus* __restrict__ status, int tiles_per_inst, uint32_t o,
+                                                    unsigned long long orcp) {
+    const LMod M{o, orcp};
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
+    const long long base = (long long)blockIdx.x * tiles_per_inst;
+    const int per = (tiles_per_inst + blockDim.x - 1) / blockDim.x;
+    const int t0 = min(tid * per, tiles_per_inst), t1 = min(t0 + per, tiles_per_inst);
+    bool has = false;
+    LAgg A;
+    A.lo = LLONG_MIN; A.hi = LLONG_MAX;
+    A.cout[0] = A.cout[1] = A.cout[2] = 0; A.m = 1; A.g[0] = A.g[1] = A.g[2] = 0;
+    for (int t = t0; t < t1; ++t) {
+        const LAgg x = status[base + t].agg;
+        A = has ? lv_compose(A, x, M) : x;
+        has = true;
+    }
+    // warp inclusive scan (with identity flags)
+    LAgg inc = A;
+    bool ihas = has;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const LAgg prev = lv_shfl_up(inc, d);
+        const bool phas = __shfl_up_sync(0xffffffffu, ihas, d);
+        if (lane >= d && phas) {
+            inc = ihas ? lv_compose(prev, inc, M) : prev;
+            ihas = true;
+        }
+    }
+    const LAgg excl = lv_shfl_up(inc, 1);
+    const bool ehas = __shfl_up_sync(0xffffffffu, ihas, 1) && lane > 0;
+    __shared__ LAgg wtot[32];
+    __shared__ bool whas[32];
+    __shared__ long long wc[32];
+    __shared__ unsigned wb[32];
+    if (lane == 31) { wtot[warp] = inc; whas[warp] = ihas; }
+    __syncthreads();
+    if (tid == 0) {
+        long long c = 0;
+        uint32_t b = 0;
+        for (int w = 0; w < NW; ++w) {
+            wc[w] = c;
+            wb[w] = b;
+            if (whas[w]) lv_apply(wtot[w], c, b, M);
+        }
+    }
+    __syncthreads();
+    long long c = wc[warp];
+    uint32_t b = wb[warp];
+    if (ehas) lv_apply(excl, c, b, M);
+    for (int t = t0; t < t1; ++t) {
+        LStatus* st = status + base + t;
+        const LAgg x = st->agg;
+        st->c = c;
+        st->beta = b;
+        lv_apply(x, c, b, M);
+    }
 }
 
 // ------------------------------------------------------------------------

@@ -651,6 +651,13 @@ static toom_status launch_eval(int B, bool top, const uint32_t* su, const uint32
     return TOOM_OK;
 }
 
+// few instances (few threads for the per-thread programs) but long rows: the
+// row-parallel interpolation has 2B-3 times the threads (C5 level 4)
+static int g_rows_max_count = [] {
+    const char* e = getenv("TOOM_ROWS_MAX_COUNT");
+    return e ? atoi(e) : 12000;
+}();
+
 static toom_status launch_interp(int B, bool top, const uint32_t* Pc, uint32_t* W, uint32_t* out, size_t count,
                                  int ywidth, int Lw, int b, int wout, cudaStream_t st) {
     if (count == 0) return TOOM_OK;
@@ -662,7 +669,7 @@ static toom_status launch_interp(int B, bool top, const uint32_t* Pc, uint32_t* 
             // recomposition only in top-interpolation mode 4 (measured slower
             // than the per-thread programs at C2-C5's shapes: every row re-reads
             // all 2B-1 products)
-            if (g_top_stream == 4 && Lw == 2 * b + 1 && (size_t)Lw >= 3 * (size_t)((wout + b - 1) / b) && ywidth > Lw) {
+            if ((g_top_stream == 4 || (g_top_stream != 0 && count < (size_t)g_rows_max_count)) && Lw == 2 * b + 1 && (size_t)Lw >= 3 * (size_t)((wout + b - 1) / b) && ywidth > Lw) {
                 // rows in parallel (one thread per interior row and product) +
                 // segment-parallel recomposition; W row 0 holds the segment carries
                 const int nseg = (wout + b - 1) / b, NP = 2 * B - 1;
@@ -1245,6 +1252,12 @@ static toom_status launch_long_multi(const LMultiDev& d, const LMultiDev* dd, LS
     return TOOM_OK;
 }
 
+// long ops with at least this many tiles per instance use the two-pass scan
+static int g_two_pass_tiles = [] {
+    const char* e = getenv("TOOM_TWO_PASS_TILES");
+    return e ? atoi(e) : 1 << 30;   // off by default: measured slower (C4 7.4 -> 18 ms at 64)
+}();
+
 static toom_status launch_long_ops(const std::vector<LOpDev>& ops, size_t first, const LOpDev* ddesc, LStatus* status,
                                    unsigned* ctr, unsigned& epoch, int cat, cudaStream_t st) {
     for (size_t i = 0; i < ops.size(); ++i) {
@@ -1263,12 +1276,22 @@ static toom_status launch_long_ops(const std::vector<LOpDev>& ops, size_t first,
             cudaFuncSetAttribute(k_long_op<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
             attr = true;
         }
-        if (o.ch == 16) {
-            if (o.wide) k_long_op<true, 16><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
-            else k_long_op<false, 16><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
-        } else {
-            if (o.wide) k_long_op<true, 4><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
-            else k_long_op<false, 4><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp);
+        // many tiles per vector: two-pass scan (aggregates, one scan CTA per
+        // instance, finish) instead of the latency-bound look-back chain
+        const bool two = o.tiles_per_inst >= g_two_pass_tiles;
+        for (int ph = two ? 1 : 0; ph <= (two ? 2 : 0); ++ph) {
+            if (ph == 2) {
+                k_long_scan<<<o.count, 1024, 0, st>>>(status, o.tiles_per_inst, o.o, o.orcp);
+                ++t_launches;
+            }
+            if (o.ch == 16) {
+                if (o.wide) k_long_op<true, 16><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp, ph);
+                else k_long_op<false, 16><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp, ph);
+            } else {
+                if (o.wide) k_long_op<true, 4><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp, ph);
+                else k_long_op<false, 4><<<grid, o.nthreads, qs, st>>>(d, status, epoch, cp, ph);
+            }
+            if (ph == 1) ++t_launches;
         }
         ps.done(st);
         ++epoch;
