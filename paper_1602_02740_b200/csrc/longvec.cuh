@@ -31,6 +31,9 @@
 
 namespace tg {
 
+#ifndef TG_LONGOP_MINB
+#define TG_LONGOP_MINB 2   // two tiles per SM (<= 128 registers)
+#endif
 constexpr int LV_MAXT = 40;     // terms per op
 constexpr int LV_NT = 256;      // threads per tile
 constexpr int LV_CH = 16;       // limbs per thread (long vectors; 4 for short ones)
@@ -423,7 +426,7 @@ __device__ __forceinline__ void lv_finish(const Acc (&lin)[CH], const LMod& M, c
 }
 
 template <bool WIDE, int CH>
-__global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ opp, LStatus* __restrict__ status,
+__global__ void __launch_bounds__(LV_NT, TG_LONGOP_MINB) k_long_op(const LOpDev* __restrict__ opp, LStatus* __restrict__ status,
                                                    unsigned epoch, unsigned* __restrict__ tile_ctr, int phase) {
     using Acc = typename std::conditional<WIDE, __int128, long long>::type;
     // the op descriptor (terms included) is cached in shared memory
@@ -483,10 +486,17 @@ __global__ void __launch_bounds__(LV_NT) k_long_op(const LOpDev* __restrict__ op
             {
                 // positions tid + q*NT (all loads issued before the stores)
                 uint32_t xv[CH];
+                if (ilo + 1 >= 0 && ihi < T.len) {   // interior tile: no bounds checks
+                    const uint32_t* sp = src + (long long)(ilo + 1 + tid) * T.limb_stride;
+                    const long long step = (long long)NT * T.limb_stride;
 #pragma unroll
-                for (int q = 0; q < CH; ++q) {
-                    const int idx = ilo + 1 + tid + q * NT;
-                    xv[q] = idx < 0 ? 0u : (idx >= T.len ? fill : __ldg(src + (long long)idx * T.limb_stride));
+                    for (int q = 0; q < CH; ++q) xv[q] = __ldg(sp + q * step);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < CH; ++q) {
+                        const int idx = ilo + 1 + tid + q * NT;
+                        xv[q] = idx < 0 ? 0u : (idx >= T.len ? fill : __ldg(src + (long long)idx * T.limb_stride));
+                    }
                 }
                 if (tid == 0) {
                     const int idx = ilo;      // position tstart - 1
