@@ -627,7 +627,7 @@ struct __align__(16) LMultiDev {
 };
 
 template <bool WIDE, int CH>
-__global__ void __launch_bounds__(LV_NT) k_long_multi(const LMultiDev* __restrict__ dp, LStatus* __restrict__ status,
+__global__ void __launch_bounds__(LV_NT, TG_LONGOP_MINB) k_long_multi(const LMultiDev* __restrict__ dp, LStatus* __restrict__ status,
                                                       unsigned epoch, unsigned* __restrict__ tile_ctr) {
     using Acc = typename std::conditional<WIDE, __int128, long long>::type;
     __shared__ __align__(16) LMultiDev s_d;
