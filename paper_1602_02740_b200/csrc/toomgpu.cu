@@ -618,7 +618,17 @@ static toom_status fail(toom_status s) {
     return s;
 }
 
+// a per-call workspace (the pipelined host entry point runs several chunks
+// concurrently, each with its own workspace)
+static thread_local void* t_ws_override = nullptr;
+static thread_local size_t t_ws_override_bytes = 0;
+
 static toom_status get_ws(size_t bytes, void** out) {
+    if (t_ws_override) {
+        if (bytes > t_ws_override_bytes) return TOOM_ENOMEM;
+        *out = t_ws_override;
+        return TOOM_OK;
+    }
     std::lock_guard<std::mutex> g(g_ws_mu);
     if (bytes <= g_ws_bytes && g_ws) { *out = g_ws; return TOOM_OK; }
     if (!g_ws_owned) return TOOM_ENOMEM;
@@ -1712,28 +1722,78 @@ toom_status toom_mul(uint32_t* w, const uint32_t* u, size_t nu, const uint32_t* 
 toom_status toom_mul_batched_host(uint32_t* w_host, const uint32_t* u_host, const uint32_t* v_host, size_t n,
                                   size_t batch, const toom_plan_t* plan, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (!w_host || !u_host || !v_host || !plan) return fail(TOOM_EINVAL);
+    if (!w_host || !u_host || !v_host || !plan || n == 0) return fail(TOOM_EINVAL);
+    if (batch == 0) return TOOM_OK;
     toom_status s = check_device();
     if (s) return fail(s);
+    // Pipeline: K chunks round-robin over NS streams, each chunk H2D(u, v) ->
+    // multiply (own workspace) -> D2H(w) in its stream's order, so the copies
+    // of one chunk overlap the kernels of another (pinned host buffers overlap;
+    // pageable ones still give the right result).
+    constexpr int NS = 3;
+    const int K = batch >= 4096 ? (int)std::min<size_t>(8, batch / 512) : 1;
+    const size_t chunk = (batch + K - 1) / K;
     static std::mutex mu;
-    static uint32_t* dbuf = nullptr;
+    static uint8_t* dbuf = nullptr;
     static size_t dbytes = 0;
+    static cudaStream_t ss[NS];
+    static cudaEvent_t ev[NS + 1];
+    static bool init = false;
     std::lock_guard<std::mutex> g(mu);
-    const size_t need = 4 * n * batch * 4;
-    if (need > dbytes) {
-        if (dbuf) { cudaDeviceSynchronize(); cudaFree(dbuf); dbuf = nullptr; dbytes = 0; }
-        if (cudaMalloc((void**)&dbuf, need) != cudaSuccess) { cudaGetLastError(); return fail(TOOM_ENOMEM); }
-        dbytes = need;
+    if (!init) {
+        for (int i = 0; i < NS; ++i) {
+            if (cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking) != cudaSuccess) return fail(TOOM_ECUDA);
+            cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&ev[NS], cudaEventDisableTiming);
+        init = true;
     }
-    uint32_t* du = dbuf;
-    uint32_t* dv = dbuf + n * batch;
-    uint32_t* dw = dbuf + 2 * n * batch;
-    if (cudaMemcpyAsync(du, u_host, n * batch * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemcpyAsync(dv, v_host, n * batch * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return fail(TOOM_ECUDA);
-    s = batched(dw, du, dv, n, batch, *plan, st);
-    if (s) return fail(s);
-    if (cudaMemcpyAsync(w_host, dw, 2 * n * batch * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess) return fail(TOOM_ECUDA);
+    toom_plan_t pc = *plan;
+    pc.chunk = 0;
+    Plan pl;
+    if ((s = make_plan((int)n, chunk, pc, pl))) return fail(s);
+    size_t wsb = pl.bytes;
+    if (pl.lv.size() == 1) wsb = (2 * ((chunk * (n + 1) + 63) & ~(size_t)63) + 2 * chunk * (n + 1)) * 4;
+    wsb = (wsb + 255) & ~(size_t)255;
+    const size_t io = ((4 * n * chunk * 4) + 255) & ~(size_t)255;   // u, v, w of a chunk
+    const size_t per = io + wsb;
+    const int nslot = std::min(NS, K);
+    if (per * nslot > dbytes) {
+        if (dbuf) { cudaDeviceSynchronize(); cudaFree(dbuf); dbuf = nullptr; dbytes = 0; }
+        if (cudaMalloc((void**)&dbuf, per * nslot) != cudaSuccess) { cudaGetLastError(); return fail(TOOM_ENOMEM); }
+        dbytes = per * nslot;
+    }
+    cudaEventRecord(ev[NS], st);
+    for (int i = 0; i < nslot; ++i) cudaStreamWaitEvent(ss[i], ev[NS], 0);
+    size_t launches = 0;
+    for (int i = 0; i < K; ++i) {
+        const size_t c0 = (size_t)i * chunk;
+        if (c0 >= batch) break;
+        const size_t cnt = std::min(chunk, batch - c0);
+        const int sl = i % nslot;
+        cudaStream_t cs = ss[sl];
+        uint8_t* base = dbuf + (size_t)sl * per;
+        uint32_t* du = (uint32_t*)base;
+        uint32_t* dv = du + n * cnt;
+        uint32_t* dw = dv + n * cnt;
+        if (cudaMemcpyAsync(du, u_host + c0 * n, n * cnt * 4, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+            cudaMemcpyAsync(dv, v_host + c0 * n, n * cnt * 4, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+            return fail(TOOM_ECUDA);
+        t_ws_override = base + io;
+        t_ws_override_bytes = wsb;
+        s = batched(dw, du, dv, n, cnt, pc, cs);
+        t_ws_override = nullptr;
+        t_ws_override_bytes = 0;
+        if (s) return fail(s);
+        launches += t_launches;
+        if (cudaMemcpyAsync(w_host + c0 * 2 * n, dw, 2 * n * cnt * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+            return fail(TOOM_ECUDA);
+    }
+    for (int i = 0; i < nslot; ++i) {
+        cudaEventRecord(ev[i], ss[i]);
+        cudaStreamWaitEvent(st, ev[i], 0);
+    }
+    t_launches = launches;
     if (cudaStreamSynchronize(st) != cudaSuccess) return fail(TOOM_ECUDA);
     return TOOM_OK;
 }

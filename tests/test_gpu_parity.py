@@ -479,12 +479,21 @@ def test_rows_interp_lower_levels(B, n, t4, t3):
         tg.set_top_stream(2)
 
 
-def test_host_buffer_entry_point():
+@pytest.mark.parametrize("batch,pinned", [(500, False), (5003, True), (9000, False)])
+def test_host_buffer_entry_point(batch, pinned):
     """toom_mul_batched_host (bench.py's e2e path): host buffers in and out,
-    copies and the multiplication in one C call."""
-    u, v = synth.config_inputs(2, batch=500, first=777)
-    w = tg.toom_mul_batched_host(u, v, B=4, t4=32, t3=32)
-    assert np.array_equal(w, oracle.toom_batched(u, v, top_B=4, threads=8))
+    chunks pipelined over streams (copies overlap the kernels), ragged last
+    chunk; pinned and pageable buffers."""
+    u, v = synth.config_inputs(2, batch=batch, first=777)
+    if pinned:
+        hu, hv = torch.from_numpy(u).pin_memory(), torch.from_numpy(v).pin_memory()
+        hw = torch.empty((batch, 512), dtype=torch.uint32).pin_memory()
+        tg.toom_mul_batched_host(hu, hv, B=4, t4=32, t3=32, out=hw)
+        w = hw.numpy()
+    else:
+        w = tg.toom_mul_batched_host(u, v, B=4, t4=32, t3=32)
+    idx = np.unique(np.concatenate([[0, batch - 1], np.random.default_rng(batch).integers(0, batch, 120)]))
+    assert np.array_equal(w[idx], oracle.toom_batched(u[idx], v[idx], top_B=4, threads=8))
 
 
 def test_workspace_user_provided():
