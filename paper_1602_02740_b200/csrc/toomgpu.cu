@@ -1731,7 +1731,11 @@ toom_status toom_mul_batched_host(uint32_t* w_host, const uint32_t* u_host, cons
     // of one chunk overlap the kernels of another (pinned host buffers overlap;
     // pageable ones still give the right result).
     constexpr int NS = 3;
-    const int K = batch >= 4096 ? (int)std::min<size_t>(8, batch / 512) : 1;
+    static const int kmax = [] {
+        const char* e = getenv("TOOM_HOST_CHUNKS");
+        return e ? atoi(e) : 8;
+    }();
+    const int K = batch >= 4096 ? (int)std::min<size_t>((size_t)kmax, batch / 512) : 1;
     const size_t chunk = (batch + K - 1) / K;
     static std::mutex mu;
     static uint8_t* dbuf = nullptr;
