@@ -156,7 +156,11 @@ void toom_set_fused(int on);
  * below, else mode 2); 2 (default) = products of a group of instances staged
  * in shared memory, rows in place, then recomposition (k_interp_top_smem); 1 = one
  * streaming pass per product (k_interp_top_stream); 0 = the per-row kernel
- * (k_interp_top_rows).  All are exact; tests compare them. */
+ * (k_interp_top_rows) and, for every batched level, the one-thread-per-
+ * product streaming programs; 4 = row-parallel interpolation (one thread per
+ * coefficient row and product) + segment-parallel recomposition at every
+ * batched Toom-3/4 level.  The paper's Toom-8 top level (C3) uses the
+ * row-parallel form unless the mode is 0.  All are exact; tests compare them. */
 void toom_set_top_stream(int on);
 
 /* ---- stage exports (tests, bench) ------------------------------------- */
