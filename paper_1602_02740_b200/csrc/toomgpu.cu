@@ -455,6 +455,10 @@ static int choose_B(const toom_plan_t& p, int depth, int n) {
     return B;
 }
 
+static const bool g_its_static = [] {   // TOOM_ITS_STATIC=0: generic top interpolation shapes only
+    const char* e = getenv("TOOM_ITS_STATIC");
+    return e ? atoi(e) != 0 : true;
+}();
 static int g_top_stream = 2;   // 3: one warp per product, 2: smem kernel, 1: one-pass stream, 0: per-row kernel
 // default long-vector rule: levels whose operands exceed this many limbs
 static int g_long_min_n = [] {
@@ -840,14 +844,19 @@ static bool launch_interp_top_smem_t(const Level& Lv, const uint32_t* P1, uint32
     while (G > 4 && interp_top_smem_bytes(B, ywidth, G, nseg) > (size_t)budget_kb * 1024) G -= 4;
     if (interp_top_smem_bytes(B, ywidth, G, nseg) > 220 * 1024 || Lv.Lw >= ywidth || Lv.Lw != 2 * Lv.b + 1) return false;
     const size_t smem = interp_top_smem_bytes(B, ywidth, G, nseg);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_interp_top_smem<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        cudaFuncSetAttribute(k_interp_top_smem<B>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr = true;
+    auto kern = k_interp_top_smem<B>;
+    // the C2 shape (n = 256 limbs, b = 64) with compile-time offsets
+    if constexpr (B == 4)
+        if (ywidth == 130 && G == 28 && Lv.Lw == 129 && Lv.b == 64 && g_its_static) kern = k_interp_top_smem<4, 130, 28, 129, 64>;
+    static bool attr[2] = {false, false};
+    const int ai = kern == k_interp_top_smem<B> ? 0 : 1;
+    if (!attr[ai]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr[ai] = true;
     }
     const unsigned grid = (unsigned)((Lv.count + G - 1) / G);
-    k_interp_top_smem<B><<<grid, 32 * NP, smem, st>>>(P1, w, Lv.count, ywidth, Lv.Lw, Lv.b, 2 * Lv.n, G, nseg);
+    kern<<<grid, 32 * NP, smem, st>>>(P1, w, Lv.count, ywidth, Lv.Lw, Lv.b, 2 * Lv.n, G, nseg);
     return true;
 }
 

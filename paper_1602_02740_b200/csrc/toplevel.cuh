@@ -463,12 +463,18 @@ __device__ __forceinline__ void interp_rows_inplace(uint32_t* Y, int ywidth, int
     }
 }
 
-template <int B>
+// YW_, G_, LW_, B_ != 0 fix ywidth, G, Lw and b at compile time (the C2 shape):
+// every shared-memory offset of the unrolled chunk loops becomes an immediate.
+template <int B, int YW_ = 0, int G_ = 0, int LW_ = 0, int B_ = 0>
 __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint32_t* __restrict__ P1,
                                                                        uint32_t* __restrict__ w, size_t count,
-                                                                       int ywidth, int Lw, int b, int wout, int G,
+                                                                       int ywidth_, int Lw_, int b_, int wout, int G_arg,
                                                                        int nseg) {
     constexpr int NP = 2 * B - 1, CK = 16;
+    const int ywidth = YW_ ? YW_ : ywidth_;
+    const int Lw = LW_ ? LW_ : Lw_;
+    const int b = B_ ? B_ : b_;
+    const int G = G_ ? G_ : G_arg;
     extern __shared__ uint32_t sm[];
     uint32_t* Y = sm;                                   // [NP][ywidth][G]
     uint32_t* CO = Y + (size_t)NP * ywidth * G;         // [nseg][G]

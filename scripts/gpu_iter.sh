@@ -1,8 +1,4 @@
-# iteration: GPU tests, bench, full ncu of kernel regex $1 (tag $2)
+# scratch GPU iteration: parity subset + C2 timing with/without the static-shape top interpolation
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m "gpu" -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-if [ -n "$1" ]; then
-timeout 300 python scripts/prof_c2.py 1 > gpurun_out/prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$1" -c 1 -o gpurun_out/prof_$2 python scripts/prof_c2.py 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_full.log
-fi
+timeout 900 python -m pytest tests -m gpu -x -q -k "c2 or top or smem or stream" > gpurun_out/it_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/it_pytest.log
+for s in 1 0 1 0; do echo "static=$s" >> gpurun_out/it_time.log; TOOM_ITS_STATIC=$s timeout 300 python scripts/time_cfg.py 2 20 >> gpurun_out/it_time.log 2>&1; done
