@@ -350,8 +350,18 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
         const uint32_t* Yl = Y + lane;
         uint32_t* dst = Wb + ((MODE == 0 ? warp - 1 : warp) * Lw) * G + lane;
         if (warp == 0 || warp == NP - 1) {
-            // MODE 0 reads w_0 = y_0 and w_2n = y_inf straight from the products
-            if constexpr (MODE != 0) {
+            // MODE 0 reads w_0 = y_0 and w_2n = y_inf straight from the products;
+            // warp 0 (idle otherwise) writes recomposition segment 0 now: its
+            // limbs are w_0[0..b) = y_0[0..b) alone, with carry-out 0
+            if constexpr (MODE == 0) {
+                if (warp == 0) {
+                    const uint32_t* src = Yl;
+                    const int len = min(b, wout);
+                    for (int r = 0; r < len; ++r) out[(size_t)r * count + c] = src[r * G];
+                    CO[lane] = 0u;
+                    CO[nseg * G + lane] = 0u;
+                }
+            } else {
                 const uint32_t* src = Yl + (warp * 2 * E) * G;
                 for (int t = 0; t < Lw; ++t) dst[t * G] = src[t * G];
             }
@@ -434,7 +444,7 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
         // one pass: every segment is written with carry-in 0; the resolved
         // carry-ins are added afterwards (they rarely ripple past limb 0)
         if (valid) {
-            for (int s = warp; s < nseg; s += NP) {
+            for (int s = warp + 1; s < nseg; s += NP) {   // segment 0 was written in phase B
                 uint32_t l0, ones;
                 const uint64_t cout = seg(s, 0, true, &l0, &ones);
                 CO[s * G + lane] = (uint32_t)cout | ((ones == 0xFFFFFFFFu) ? 0x80000000u : 0u);
@@ -457,7 +467,7 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
         }
         __syncthreads();
         if (valid) {
-            for (int s = warp; s < nseg; s += NP) {
+            for (int s = warp + 1; s < nseg; s += NP) {
                 uint32_t cin = CO[s * G + lane];
                 const int P0 = s * b;
                 const int len = min(b, wout - P0);

@@ -530,6 +530,22 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     }
     __syncthreads();
     const bool act = lane < G;
+    // warp 0 (idle in phase 1) writes recomposition segment 0 first: its limbs
+    // are w_0[0..b) = y_0[0..b) alone, carry-out 0
+    if (warp == 0 && act) {
+        uint32_t* row0 = w + (c0 + lane) * (size_t)wout;
+        const uint32_t* y0 = Y + lane;
+        const int len = min(b, wout);
+        if (lane < nin) {
+            int r = 0;
+            if ((wout & 3) == 0)
+                for (; r + 4 <= len; r += 4)
+                    *reinterpret_cast<uint4*>(row0 + r) =
+                        make_uint4(y0[r * G], y0[(r + 1) * G], y0[(r + 2) * G], y0[(r + 3) * G]);
+            for (; r < len; ++r) row0[r] = y0[r * G];
+        }
+        CO[lane] = 0u;
+    }
     // ---- phase 1: rows 1..NP-2, in place (lock-stepped chunks; the barriers
     // are outside the per-lane work so every thread reaches them)
     {
@@ -582,7 +598,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     uint32_t* row = w + (c0 + lane) * (size_t)wout;
     const bool wr = act && lane < nin;
     if (act) {
-        for (int s = warp; s < nseg; s += NP) {
+        for (int s = warp + 1; s < nseg; s += NP) {   // segment 0 was written before phase 1
             const int len = min(b, wout - s * b);
             const uint32_t* pa = rowA(s);
             const uint32_t* pb = rowB(s);
@@ -633,7 +649,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     }
     __syncthreads();
     if (wr) {
-        for (int s = warp; s < nseg; s += NP) {
+        for (int s = warp + 1; s < nseg; s += NP) {
             uint32_t cin = CI[s * G + lane];
             const int len = min(b, wout - s * b);
             for (int r = 0; r < len && cin; ++r) {
