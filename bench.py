@@ -242,11 +242,11 @@ def main():
     L0, L1 = lv[0], lv[1]
     E = lv[-1]["n"]
     # per-launch algorithmic work of the three kernels of a C2 step:
-    #   eval   (k_eval_top_rows<4>)   : read u, v; write the 7 evaluated pairs
+    #   eval   (k_eval_top_v4<4>)   : read u, v; write the 7 evaluated pairs
     #   fused  (k_fused_bottom<4,18>) : 7 * E^2 limb-products per level-1 parent
     #   interp (k_interp_top_smem<4>) : read the 7 products; write w
     kern = {
-        "eval": dict(name="k_eval_top_rows<4>", bound="hbm",
+        "eval": dict(name="k_eval_top_v4<4>", bound="hbm",
                      units=2 * (L0["count"] * L0["n"] + L0["count"] * L0["npts"] * L0["e"]) * 4),
         "base": dict(name="k_fused_bottom<4,18>", bound="alu", units=L1["count"] * L1["npts"] * E * E,
                      bytes=(2 * L1["count"] * L1["n"] + L1["count"] * 2 * L1["n"]) * 4),

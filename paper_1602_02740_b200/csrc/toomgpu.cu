@@ -455,6 +455,10 @@ static int choose_B(const toom_plan_t& p, int depth, int n) {
     return B;
 }
 
+static const bool g_eval_v4 = [] {      // TOOM_EVAL_V4=0: k_eval_top_rows only
+    const char* e = getenv("TOOM_EVAL_V4");
+    return e ? atoi(e) != 0 : true;
+}();
 static const bool g_its_static = [] {   // TOOM_ITS_STATIC=0: generic top interpolation shapes only
     const char* e = getenv("TOOM_ITS_STATIC");
     return e ? atoi(e) != 0 : true;
@@ -806,7 +810,10 @@ static toom_status launch_eval_top_rows(const Level& Lv, const uint32_t* u, cons
                                         uint32_t* V1, cudaStream_t st) {
     ProfScope ps(CAT_EVAL, st);
     const unsigned grid = (unsigned)((Lv.count + 31) / 32);
-    if (Lv.B == 3) k_eval_top_rows<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
+    const bool v4 = g_eval_v4 && Lv.B <= 4 && (Lv.n & 3) == 0 && (Lv.b & 3) == 0;
+    if (v4 && Lv.B == 3) k_eval_top_v4<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
+    else if (v4) k_eval_top_v4<4><<<grid, 32 * 7, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
+    else if (Lv.B == 3) k_eval_top_rows<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     else if (Lv.B == 4) k_eval_top_rows<4><<<grid, 32 * 7, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     else k_eval_top_rows<8><<<grid, 32 * 15, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     ps.done(st);

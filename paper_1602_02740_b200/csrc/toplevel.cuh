@@ -20,6 +20,11 @@
 namespace tg {
 
 template <int B>
+__host__ __device__ constexpr long long tg_evalc_cx(int k, int j) {
+    return B == 3 ? tg_evalc_cx_T3(k, j) : tg_evalc_cx_T4(k, j);
+}
+
+template <int B>
 __device__ __forceinline__ uint32_t rowstep(int j, const uint32_t (&y)[2 * B - 1], tg_rowstate& st) {
     if constexpr (B == 3) return tg_rowstep_T3(j, y, st);
     else return tg_rowstep_T4(j, y, st);
@@ -104,6 +109,125 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
             }
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------
+// k_eval_top_v4<B>: the top-level evaluation of k_eval_top_rows (B = 3, 4) with
+// 16-byte staging and compile-time points.  CTA = 32 products x NP warps.
+// Chunks of 16 limbs of every block of the 32 products are copied with 16-byte
+// cp.async (zero-filled past a block's end) into S[op][j][i][16], the four
+// 16-byte slots of row i XOR-swizzled by (i >> 1) & 3 so that the per-lane
+// 16-byte reads of one slot are conflict-free; warp k streams U(x_k), V(x_k)
+// with its homogeneous coefficients p^j q^(n-j) as immediates (one
+// mad.wide.u32 per nonzero term); positions past every block (t >= b) carry
+// only the running carry.  Requires n, b multiples of 4.
+// ------------------------------------------------------------------------
+template <int B, int K>
+__device__ __forceinline__ void eval_top_v4_chunk(const uint32_t* __restrict__ Su, const uint32_t* __restrict__ Sv,
+                                                  int lane, int t0, int tend, uint64_t& au, uint64_t& av,
+                                                  uint32_t*& pu, uint32_t*& pv, size_t stride_limb) {
+    constexpr int CH = 16;
+    const int sw = (lane >> 1) & 3;
+#pragma unroll
+    for (int q = 0; q < CH / 4; ++q) {
+        if (t0 + 4 * q >= tend) break;
+        uint4 xu[B], xv[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (tg_evalc_cx<B>(K, j) != 0) {
+                const int off = (j * 32 + lane) * CH + 4 * (q ^ sw);
+                xu[j] = *reinterpret_cast<const uint4*>(Su + off);
+                xv[j] = *reinterpret_cast<const uint4*>(Sv + off);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (t0 + 4 * q + r >= tend) break;
+            uint64_t lu = au, lv = av;
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                const long long cf = tg_evalc_cx<B>(K, j);
+                if (cf == 0) continue;
+                const uint32_t x = r == 0 ? xu[j].x : r == 1 ? xu[j].y : r == 2 ? xu[j].z : xu[j].w;
+                const uint32_t y = r == 0 ? xv[j].x : r == 1 ? xv[j].y : r == 2 ? xv[j].z : xv[j].w;
+                if (cf > 0) { lu = tg_madw((uint32_t)cf, x, lu); lv = tg_madw((uint32_t)cf, y, lv); }
+                else { lu = tg_msubw((uint32_t)(-cf), x, lu); lv = tg_msubw((uint32_t)(-cf), y, lv); }
+            }
+            *pu = (uint32_t)lu;
+            *pv = (uint32_t)lv;
+            pu += stride_limb;
+            pv += stride_limb;
+            au = (uint64_t)((int64_t)lu >> 32);
+            av = (uint64_t)((int64_t)lv >> 32);
+        }
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_v4(
+    const uint32_t* __restrict__ u, const uint32_t* __restrict__ v, uint32_t* __restrict__ U1,
+    uint32_t* __restrict__ V1, size_t count, int n, int b, int e) {
+    constexpr int NP = 2 * B - 1, G = 32, CH = 16, NQ = CH / 4;
+    __shared__ __align__(16) uint32_t S[2][2][B][G][CH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t c0 = (size_t)blockIdx.x * G;
+    const int nin = (int)min((size_t)G, count - c0);
+    const int lentop = n - (B - 1) * b;
+    auto stage = [&](int buf, int t0) {
+        constexpr int NE = 2 * B * G * NQ;
+        for (int idx = threadIdx.x; idx < NE; idx += blockDim.x) {
+            const int q = idx % NQ, i = (idx / NQ) % G, j = (idx / (NQ * G)) % B, op = idx / (NQ * G * B);
+            const int t = t0 + 4 * q;
+            const int len = (j == B - 1) ? lentop : b;
+            const int words = (i < nin) ? min(max(len - t, 0), 4) : 0;
+            const uint32_t* src = words ? (op ? v : u) + (c0 + i) * (size_t)n + (size_t)j * b + t : u;
+            const unsigned d = (unsigned)__cvta_generic_to_shared(&S[buf][op][j][i][4 * (q ^ ((i >> 1) & 3))]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(words * 4));
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    const size_t stride_limb = (size_t)NP * count;
+    uint32_t* pu = U1 + (size_t)warp * count + c0 + lane;
+    uint32_t* pv = V1 + (size_t)warp * count + c0 + lane;
+    uint64_t au = 0, av = 0;
+    const int tb = min(b, e);                 // staged positions; [tb, e) are carries only
+    const int nch = (tb + CH - 1) / CH;
+    stage(0, 0);
+    for (int ci = 0; ci < nch; ++ci) {
+        const int t0 = ci * CH;
+        if (ci + 1 < nch) {
+            stage((ci + 1) & 1, t0 + CH);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (lane < nin) {
+            const uint32_t* Su = &S[ci & 1][0][0][0][0];
+            const uint32_t* Sv = &S[ci & 1][1][0][0][0];
+            const int tend = min(t0 + CH, tb);
+            switch (warp) {
+                case 0: eval_top_v4_chunk<B, 0>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 1: eval_top_v4_chunk<B, 1>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 2: eval_top_v4_chunk<B, 2>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 3: eval_top_v4_chunk<B, 3>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 4: eval_top_v4_chunk<B, 4>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 5: if constexpr (B >= 4) eval_top_v4_chunk<B, 5>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                default: if constexpr (B >= 4) eval_top_v4_chunk<B, 6>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+            }
+        }
+        __syncthreads();
+    }
+    if (lane < nin) {
+        for (int t = tb; t < e; ++t) {
+            *pu = (uint32_t)au;
+            *pv = (uint32_t)av;
+            pu += stride_limb;
+            pv += stride_limb;
+            au = (uint64_t)((int64_t)au >> 32);
+            av = (uint64_t)((int64_t)av >> 32);
+        }
     }
 }
 

@@ -706,6 +706,14 @@ def emit_row_tables(ps: PointSet) -> str:
     for (p, q) in ps.points:
         L.append("  {" + ", ".join(str(p**j * q ** (n - j)) for j in range(ps.B)) + "},")
     L.append("};")
+    # the same coefficients as a constexpr function (compile-time point index)
+    L.append(f"TG_HD constexpr long long tg_evalc_cx_{ps.name}(int k, int j) {{")
+    L.append(f"  return")
+    for k, (p, q) in enumerate(ps.points):
+        for j in range(ps.B):
+            L.append(f"    (k == {k} && j == {j}) ? {p**j * q ** (n - j)}ll :")
+    L.append("    0ll;")
+    L.append("}")
     A, O, INV, S = [], [], [], []
     for j, pr in enumerate(rows):
         coef = [0] * NP

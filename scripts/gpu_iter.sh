@@ -1,4 +1,4 @@
-# scratch GPU iteration: parity + C1-C3 timing
+# scratch GPU iteration: parity + C2 timing with/without the vectorised top evaluation
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/it_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/it_pytest.log
-for c in 1 2 3 2; do timeout 300 python scripts/time_cfg.py $c 20 >> gpurun_out/it_time.log 2>&1; done
+for s in 1 0 1 0; do echo "v4=$s" >> gpurun_out/it_time.log; TOOM_EVAL_V4=$s timeout 300 python scripts/time_cfg.py 2 20 >> gpurun_out/it_time.log 2>&1; done
