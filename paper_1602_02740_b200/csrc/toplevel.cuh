@@ -129,7 +129,9 @@ __device__ __forceinline__ void eval_top_v4_chunk(const uint32_t* __restrict__ S
                                                   uint32_t*& pu, uint32_t*& pv, size_t stride_limb) {
     constexpr int CH = 16;
     const int sw = (lane >> 1) & 3;
-#pragma unroll
+    // (rolled: seven point variants of one unrolled chunk overflow the
+    // instruction cache)
+#pragma unroll 1
     for (int q = 0; q < CH / 4; ++q) {
         if (t0 + 4 * q >= tend) break;
         uint4 xu[B], xv[B];

@@ -1,4 +1,3 @@
-# scratch GPU iteration: parity + C2 timing with/without the vectorised top evaluation
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/it_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/it_pytest.log
-for s in 1 0 1 0; do echo "v4=$s" >> gpurun_out/it_time.log; TOOM_EVAL_V4=$s timeout 300 python scripts/time_cfg.py 2 20 >> gpurun_out/it_time.log 2>&1; done
+timeout 600 python -m pytest tests -m gpu -x -q -k "c2 or top or eval" > gpurun_out/it_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/it_pytest.log
+for s in 1 1; do timeout 300 python scripts/time_cfg.py 2 20 >> gpurun_out/it_time.log 2>&1; done
