@@ -675,7 +675,10 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     // ---- phase 1: rows 1..NP-2, in place (lock-stepped chunks; the barriers
     // are outside the per-lane work so every thread reaches them)
     {
-        constexpr int CK = 16;
+#ifndef TG_ITS_CK
+#define TG_ITS_CK 12   // C2: 277 us (8: 283, 16: 302 -- instruction cache, 4: 291)
+#endif
+        constexpr int CK = TG_ITS_CK;   // limb positions per lock-stepped chunk
         const int j = warp;
         const bool rw = act && j >= 1 && j <= NP - 2;
         tg_rowstate st{0, 0, 0};
