@@ -254,10 +254,18 @@ __device__ int tg_fused_phase_mask = 7;
 //           whose interpolation runs one warp per product).
 // Output products: interleaved [2n][count] for MODE 0, row-major [count][2n]
 // otherwise.
-template <int B, int E, int MODE>
+// N_, BB_ != 0 fix n and b (hence Lw = 2b+1, wout = 2n, nseg) at compile time
+// (the C2 shape): shared-memory offsets and trip counts become immediates.
+template <int B, int E, int MODE, int N_ = 0, int BB_ = 0>
 __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_bottom(
     const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV, uint32_t* __restrict__ out,
-    size_t count, int n, int b, int Lw, int wout, int nseg) {
+    size_t count, int n_, int b_, int Lw_, int wout_, int nseg_) {
+    constexpr bool ST = N_ != 0 && BB_ != 0;
+    const int n = ST ? N_ : n_;
+    const int b = ST ? BB_ : b_;
+    const int Lw = ST ? 2 * BB_ + 1 : Lw_;
+    const int wout = ST ? 2 * N_ : wout_;
+    const int nseg = ST ? (2 * N_ + BB_ - 1) / BB_ : nseg_;
     constexpr int NP = 2 * B - 1;
     constexpr int G = 32;
     extern __shared__ uint32_t sm[];
@@ -366,19 +374,23 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
                 for (int t = 0; t < Lw; ++t) dst[t * G] = src[t * G];
             }
         } else if constexpr (B == 3) {
+            // (the destination row is recomputed per case so that, with a
+            // compile-time shape, its offset from Yl is an immediate)
+#define TG_DST(J) (Wb + ((MODE == 0 ? (J) - 1 : (J)) * Lw) * G + lane)
             switch (warp) {
-                case 1: tg_row_T3_1<2 * E>(Yl, dst, Lw); break;
-                case 2: tg_row_T3_2<2 * E>(Yl, dst, Lw); break;
-                default: tg_row_T3_3<2 * E>(Yl, dst, Lw); break;
+                case 1: tg_row_T3_1<2 * E>(Yl, TG_DST(1), Lw); break;
+                case 2: tg_row_T3_2<2 * E>(Yl, TG_DST(2), Lw); break;
+                default: tg_row_T3_3<2 * E>(Yl, TG_DST(3), Lw); break;
             }
         } else {
             switch (warp) {
-                case 1: tg_row_T4_1<2 * E>(Yl, dst, Lw); break;
-                case 2: tg_row_T4_2<2 * E>(Yl, dst, Lw); break;
-                case 3: tg_row_T4_3<2 * E>(Yl, dst, Lw); break;
-                case 4: tg_row_T4_4<2 * E>(Yl, dst, Lw); break;
-                default: tg_row_T4_5<2 * E>(Yl, dst, Lw); break;
+                case 1: tg_row_T4_1<2 * E>(Yl, TG_DST(1), Lw); break;
+                case 2: tg_row_T4_2<2 * E>(Yl, TG_DST(2), Lw); break;
+                case 3: tg_row_T4_3<2 * E>(Yl, TG_DST(3), Lw); break;
+                case 4: tg_row_T4_4<2 * E>(Yl, TG_DST(4), Lw); break;
+                default: tg_row_T4_5<2 * E>(Yl, TG_DST(5), Lw); break;
             }
+#undef TG_DST
         }
     }
     __syncthreads();

@@ -459,7 +459,7 @@ static const bool g_eval_v4 = [] {      // TOOM_EVAL_V4=0: k_eval_top_rows only
     const char* e = getenv("TOOM_EVAL_V4");
     return e ? atoi(e) != 0 : true;
 }();
-static const bool g_its_static = [] {   // TOOM_ITS_STATIC=0: generic top interpolation shapes only
+static const bool g_its_static = [] {   // TOOM_ITS_STATIC=0: generic shapes only (top interpolation, fused bottom)
     const char* e = getenv("TOOM_ITS_STATIC");
     return e ? atoi(e) != 0 : true;
 }();
@@ -762,19 +762,23 @@ template <int B, int E, int TOP>
 static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out, cudaStream_t st) {
     const int nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
     const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg, Lv.n, TOP);
-    static bool attr_set = false;   // per instantiation
-    if (!attr_set) {
+    auto kern = k_fused_bottom<B, E, TOP>;
+    // the C2 shape (level-1 parents of 65 limbs, b = 17) with compile-time offsets
+    if constexpr (B == 4 && E == 18 && TOP == 0)
+        if (Lv.n == 65 && Lv.b == 17 && Lv.Lw == 35 && g_its_static) kern = k_fused_bottom<4, 18, 0, 65, 17>;
+    static bool attr_set[2] = {false, false};   // per instantiation
+    const int ai = kern == k_fused_bottom<B, E, TOP> ? 0 : 1;
+    if (!attr_set[ai]) {
         if (const char* m = getenv("TOOM_DBG_FUSED_MASK")) {   // diagnostics only
             const int v = atoi(m);
             cudaMemcpyToSymbol(tg_fused_phase_mask, &v, sizeof v);
         }
-        cudaFuncSetAttribute(k_fused_bottom<B, E, TOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        cudaFuncSetAttribute(k_fused_bottom<B, E, TOP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr_set = true;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr_set[ai] = true;
     }
     const unsigned grid = (unsigned)((Lv.count + 31) / 32);
-    k_fused_bottom<B, E, TOP><<<grid, 32 * (2 * B - 1), smem, st>>>(su, sv, out, Lv.count, Lv.n, Lv.b, Lv.Lw,
-                                                                    2 * Lv.n, nseg);
+    kern<<<grid, 32 * (2 * B - 1), smem, st>>>(su, sv, out, Lv.count, Lv.n, Lv.b, Lv.Lw, 2 * Lv.n, nseg);
 }
 
 // mode: 0 interleaved signed parents, 1 row-major unsigned (top), 2 row-major signed
