@@ -766,6 +766,9 @@ static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* 
     // the C2 shape (level-1 parents of 65 limbs, b = 17) with compile-time offsets
     if constexpr (B == 4 && E == 18 && TOP == 0)
         if (Lv.n == 65 && Lv.b == 17 && Lv.Lw == 35 && g_its_static) kern = k_fused_bottom<4, 18, 0, 65, 17>;
+    // the C3 / C4 bottom (parents of 66 limbs, b = 22)
+    if constexpr (B == 3 && E == 23 && TOP == 0)
+        if (Lv.n == 66 && Lv.b == 22 && Lv.Lw == 45 && g_its_static) kern = k_fused_bottom<3, 23, 0, 66, 22>;
     static bool attr_set[2] = {false, false};   // per instantiation
     const int ai = kern == k_fused_bottom<B, E, TOP> ? 0 : 1;
     if (!attr_set[ai]) {
