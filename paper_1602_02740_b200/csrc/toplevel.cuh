@@ -166,8 +166,11 @@ __device__ __forceinline__ void eval_top_v4_chunk(const uint32_t* __restrict__ S
     }
 }
 
+#ifndef TG_EVAL_V4_MINB
+#define TG_EVAL_V4_MINB 4   // 72 registers, four CTAs per SM (1: 122 registers, 91 us on C2; 4: 75 us)
+#endif
 template <int B>
-__global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_v4(
+__global__ void __launch_bounds__(32 * (2 * B - 1), TG_EVAL_V4_MINB) k_eval_top_v4(
     const uint32_t* __restrict__ u, const uint32_t* __restrict__ v, uint32_t* __restrict__ U1,
     uint32_t* __restrict__ V1, size_t count, int n, int b, int e) {
     constexpr int NP = 2 * B - 1, G = 32, CH = 16, NQ = CH / 4;

@@ -1,5 +1,7 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/it_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/it_pytest.log
-for m in 0 24000 200000 0 24000 200000; do echo -n "m=$m " >> gpurun_out/it_time.log; TOOM_EVAL_PTS_MAX_COUNT=$m timeout 300 python scripts/time_cfg.py 4 5 >> gpurun_out/it_time.log 2>&1; done
-for m in 0 24000 200000; do echo -n "m=$m " >> gpurun_out/it_time.log; TOOM_EVAL_PTS_MAX_COUNT=$m timeout 300 python scripts/time_cfg.py 3 10 >> gpurun_out/it_time.log 2>&1; done
-for m in 0 24000; do echo -n "m=$m " >> gpurun_out/it_time.log; TOOM_EVAL_PTS_MAX_COUNT=$m timeout 300 python scripts/time_cfg.py 5 2 >> gpurun_out/it_time.log 2>&1; done
+for r in 1 2; do
+for v in base r72 e3 e4 e5 e6; do
+  if [ $v = base ]; then L=; else L=variants/libtoomgpu_$v.so; fi
+  echo -n "$v " >> gpurun_out/it_time.log
+  TOOM_LIB=$L timeout 300 python scripts/time_cfg.py 2 20 >> gpurun_out/it_time.log 2>&1
+done; done
