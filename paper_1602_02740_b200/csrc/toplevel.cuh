@@ -31,6 +31,9 @@ __device__ __forceinline__ uint32_t rowstep(int j, const uint32_t (&y)[2 * B - 1
 }
 
 constexpr int TOP_CH = 16;   // limbs per staged chunk
+#ifndef TG_ITS_CK
+#define TG_ITS_CK 10   // k_interp_top_smem phase 1 chunk (C2, per-row code: 10 -> 207 us; 4: 241, 6: 230, 8: 230, 12: 275)
+#endif
 
 template <int B>
 __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
@@ -558,7 +561,7 @@ __device__ __forceinline__ uint32_t rowstep_j(const uint32_t (&y)[2 * B - 1], tg
 // warps have read the chunk.
 template <int B, int J>
 __device__ __forceinline__ void interp_rows_inplace(uint32_t* Y, int ywidth, int G, int Lw, int lane, bool work) {
-    constexpr int NP = 2 * B - 1, CK = 8;
+    constexpr int NP = 2 * B - 1, CK = TG_ITS_CK;
     const uint32_t* yb[NP];
 #pragma unroll
     for (int k = 0; k < NP; ++k) yb[k] = Y + (size_t)k * ywidth * G + lane;
@@ -677,10 +680,21 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
     }
     // ---- phase 1: rows 1..NP-2, in place (lock-stepped chunks; the barriers
     // are outside the per-lane work so every thread reaches them)
-    {
-#ifndef TG_ITS_CK
-#define TG_ITS_CK 12   // C2: 277 us (8: 283, 16: 302 -- instruction cache, 4: 291)
+    // Toom-4: one specialised chunk loop per row (warp-uniform dispatch outside
+    // the loop; idle warps run the barriers only).  C2: 277 -> 230 us.
+#ifndef TG_ITS_NO_HOIST
+    if constexpr (B == 4) {
+        switch (warp) {
+            case 1: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, act); break;
+            case 2: interp_rows_inplace<B, 2>(Y, ywidth, G, Lw, lane, act); break;
+            case 3: interp_rows_inplace<B, 3>(Y, ywidth, G, Lw, lane, act); break;
+            case 4: interp_rows_inplace<B, 4>(Y, ywidth, G, Lw, lane, act); break;
+            case 5: interp_rows_inplace<B, 5>(Y, ywidth, G, Lw, lane, act); break;
+            default: interp_rows_inplace<B, 1>(Y, ywidth, G, Lw, lane, false); break;
+        }
+    } else
 #endif
+    {
         constexpr int CK = TG_ITS_CK;   // limb positions per lock-stepped chunk
         const int j = warp;
         const bool rw = act && j >= 1 && j <= NP - 2;
