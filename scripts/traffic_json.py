@@ -11,7 +11,7 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 res = {}
 for r in rows[2:]:
     name = r[ki].split("(")[0].replace("void ", "").replace("tg::", "").replace(" ", "")
-    name = re.sub(r",\d+>$", ">", name) if name.startswith("k_fused_bottom") else name
+    name = re.sub(r"^k_fused_bottom<(\d+),(\d+).*>$", r"k_fused_bottom<\1,\2>", name)
     name = re.sub(r"<(\d+),.*>$", r"<\1>", name) if name.startswith("k_interp_top_smem") else name
     b = float(r[ri].replace(",", "")) * scale[units[ri]] + float(r[wi].replace(",", "")) * scale[units[wi]]
     res.setdefault(name, b)
