@@ -990,6 +990,19 @@ TG_HD TG_INLINE uint64_t tg_msubw(uint32_t m, uint32_t x, uint64_t lin) {
 // one limb of the 2-adic exact division by odd o (ref [4]): q = (t - bor) * o^-1,
 // bor' = hi(q*o) + (t < bor)
 TG_HD TG_INLINE uint32_t tg_divexact_step(uint32_t t, uint32_t& bor, uint32_t oinv, uint32_t o) {
+#if defined(__CUDA_ARCH__) && !defined(TG_DIVEXACT_C)
+  // sub.cc's borrow-out feeds subc (bb = -borrow); bor' = hi(q o) + borrow
+  uint32_t q, nb;
+  asm("{\\n\\t.reg .u32 x, bb;\\n\\t"
+      "sub.cc.u32 x, %2, %3;\\n\\t"
+      "subc.u32 bb, 0, 0;\\n\\t"
+      "mul.lo.u32 %0, x, %4;\\n\\t"
+      "mul.hi.u32 %1, %0, %5;\\n\\t"
+      "sub.u32 %1, %1, bb;\\n\\t}"
+      : "=r"(q), "=r"(nb) : "r"(t), "r"(bor), "r"(oinv), "r"(o));
+  bor = nb;
+  return q;
+#else
   const uint32_t x = t - bor;
   const uint32_t b1 = (t < bor) ? 1u : 0u;
   const uint32_t q = x * oinv;
@@ -999,6 +1012,7 @@ TG_HD TG_INLINE uint32_t tg_divexact_step(uint32_t t, uint32_t& bor, uint32_t oi
   bor = (uint32_t)(((uint64_t)q * o) >> 32) + b1;
 #endif
   return q;
+#endif
 }
 // limb of (x >> r) given consecutive limbs lo = x[i], hi = x[i+1], 0 < r < 32
 TG_HD TG_INLINE uint32_t tg_shr_limb(uint32_t lo, uint32_t hi, int r) {
