@@ -812,20 +812,36 @@ def emit_row_functions(ps: PointSet) -> str:
         L.append("  uint64_t acc = 0; uint32_t qp = 0;")
         if op.odiv != 1:
             L.append("  uint32_t bor = 0;")
-        L.append(f"  TG_ROW_UNROLL_{ps.name}")
-        L.append("  for (int t = 0; t <= Lw; ++t) {")
+        # one position: loads, linear combination, carry, exact division
+        # (Toom-4: position 0 peeled so that the loop stores unconditionally)
+        L.append("  auto step = [&](int t) -> uint32_t {")
         L.append("    const uint32_t* __restrict__ yt = Y + t * 32;")
         for k, m in idx:
             L.append(f"    const uint32_t y{k} = yt[{k} * W2 * 32];")
         L += _lincomb_lines([(f"y{k}", m) for k, m in idx], "acc", "lin", "    ")
         L.append("    acc = (uint64_t)((int64_t)lin >> 32);")
         if op.odiv != 1:
-            L.append(f"    const uint32_t q = tg_divexact_step((uint32_t)lin, bor, 0x{_inv32(op.odiv):08X}u, {op.odiv}u);")
+            L.append(f"    return tg_divexact_step((uint32_t)lin, bor, 0x{_inv32(op.odiv):08X}u, {op.odiv}u);")
         else:
-            L.append("    const uint32_t q = (uint32_t)lin;")
-        L.append(f"    if (t > 0) dst[(t - 1) * 32] = tg_shr_limb_or_delay(qp, q, {op.shr});")
-        L.append("    qp = q;")
-        L.append("  }")
+            L.append("    return (uint32_t)lin;")
+        L.append("  };")
+        if ps.B >= 4:
+            # peeled (C2 fused 426 -> 418 us)
+            L.append("  qp = step(0);")
+            L.append(f"  TG_ROW_UNROLL_{ps.name}")
+            L.append("  for (int t = 1; t <= Lw; ++t) {")
+            L.append("    const uint32_t q = step(t);")
+            L.append(f"    dst[(t - 1) * 32] = tg_shr_limb_or_delay(qp, q, {op.shr});")
+            L.append("    qp = q;")
+            L.append("  }")
+        else:
+            # (peeling measured slower for the unrolled Toom-3 rows: C1, C3)
+            L.append(f"  TG_ROW_UNROLL_{ps.name}")
+            L.append("  for (int t = 0; t <= Lw; ++t) {")
+            L.append("    const uint32_t q = step(t);")
+            L.append(f"    if (t > 0) dst[(t - 1) * 32] = tg_shr_limb_or_delay(qp, q, {op.shr});")
+            L.append("    qp = q;")
+            L.append("  }")
         L.append("}")
     return "\n".join(L)
 
