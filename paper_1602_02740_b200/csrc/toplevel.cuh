@@ -627,7 +627,29 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
         if (v16) {
             const int q4 = G >> 2, rp = 32 / q4;
             const int sub = lane / q4, q = lane - sub * q4;
-            if (sub < rp) {
+            if (sub < rp && nw == NP) {
+                // rows in the source order R = t * NP + k: the stride NP * rp
+                // keeps k fixed per thread and advances t by rp, so both
+                // addresses are plain increments
+                const int R0 = warp * rp + sub;
+                const int k = R0 % NP;
+                int t = R0 / NP;
+                const int g = q * 4;
+                const uint32_t* sr = P1 + (size_t)t * S + (size_t)k * count + c0 + g;
+                uint32_t* dr = Y + (size_t)(k * ywidth + t) * G + g;
+                const size_t sstep = (size_t)rp * S;
+                const int dstep = rp * G;
+                if (g + 3 < nin) {
+                    unsigned d = (unsigned)__cvta_generic_to_shared(dr);
+                    for (; t < ywidth; t += rp, sr += sstep, d += 4u * dstep)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(sr));
+                } else {
+                    for (; t < ywidth; t += rp, sr += sstep, dr += dstep) {
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) dr[x] = (g + x < nin) ? __ldg(sr + x) : 0u;
+                    }
+                }
+            } else if (sub < rp) {
                 // row R = k * ywidth + t, advanced incrementally (no division)
                 const int stride = nw * rp;
                 int R = warp * rp + sub;
