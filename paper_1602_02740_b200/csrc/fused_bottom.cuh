@@ -304,6 +304,36 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
         }
         constexpr int ROWS = B * E, ITER = (ROWS + NP - 1) / NP;
         uint32_t xu[ITER], xv[ITER];
+        if constexpr (MODE == 0 || MODE == 3) {
+            // interleaved parents: row r = warp + q NP is block j limb t; both
+            // advance incrementally and the source pointers by whole limb rows
+            int j = warp / E, t = warp - (warp / E) * E;
+            const uint32_t* pu = srcU + (size_t)(j * b + t) * count + c0 + lane;
+            const uint32_t* pv = srcV + (size_t)(j * b + t) * count + c0 + lane;
+#pragma unroll
+            for (int q = 0; q < ITER; ++q) {
+                const int r = warp + q * NP;
+                const int len = (j == B - 1) ? lentop : b;
+                xu[q] = 0;
+                xv[q] = 0;
+                if (r < ROWS && lane < nin) {
+                    if (t < len) {
+                        xu[q] = __ldg(pu);
+                        xv[q] = __ldg(pv);
+                    } else if (j == B - 1) {
+                        xu[q] = fu;
+                        xv[q] = fv;
+                    }
+                }
+                if (q + 1 < ITER) {
+                    int dl = NP;
+                    t += NP;
+                    while (t >= E) { t -= E; ++j; dl += b - E; }
+                    pu += (long long)dl * (long long)count;
+                    pv += (long long)dl * (long long)count;
+                }
+            }
+        } else {
 #pragma unroll
         for (int q = 0; q < ITER; ++q) {
             const int r = warp + q * NP;
@@ -326,6 +356,7 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
                     xv[q] = fv;
                 }
             }
+        }
         }
 #pragma unroll
         for (int q = 0; q < ITER; ++q) {
