@@ -121,3 +121,30 @@ def test_streaming_interp_matches_convolution(harness, name, half):
                 if half == "_odd" and j % 2 == 0:
                     continue
                 assert got[j] == conv[j], (name, half, b, j)
+
+
+def test_constexpr_eval_coefficients_match_table(tmp_path):
+    """k_eval_top_v4 takes its point coefficients from the generated constexpr
+    function tg_evalc_cx_*; they must equal the tg_evalc_* table (the fused
+    kernel's) and the homogeneous-point definition p^j q^(n-j) (§2)."""
+    from paper_1602_02740_b200.build import generate
+    generate()
+    src = tmp_path / "cx.cpp"
+    src.write_text('#include "toom_programs.cuh"\n#include <cstdio>\n'
+                   'int main() {\n'
+                   '  for (int k = 0; k < 5; ++k) for (int j = 0; j < 3; ++j)\n'
+                   '    std::printf("T3 %d %d %lld %lld\\n", k, j, tg_evalc_cx_T3(k, j), tg_evalc_T3[k][j]);\n'
+                   '  for (int k = 0; k < 7; ++k) for (int j = 0; j < 4; ++j)\n'
+                   '    std::printf("T4 %d %d %lld %lld\\n", k, j, tg_evalc_cx_T4(k, j), tg_evalc_T4[k][j]);\n'
+                   '  static_assert(tg_evalc_cx_T4(3, 3) == 8, "compile-time");\n'
+                   '  return 0;\n}\n')
+    exe = tmp_path / "cx"
+    subprocess.check_call(["g++", "-std=c++17", "-I", GEN, "-o", str(exe), str(src)])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    rows = [l.split() for l in out if l]
+    assert len(rows) == 15 + 28
+    for name, k, j, cx, tab in rows:
+        ps = SETS[name]
+        p, q = ps.points[int(k)]
+        want = p ** int(j) * q ** (ps.n - int(j))
+        assert int(cx) == int(tab) == want, (name, k, j, cx, tab, want)
