@@ -39,7 +39,7 @@ extern "C" {
 typedef enum {
     TOOM_OK = 0,
     TOOM_EINVAL = 1,       /* bad argument (null pointer, aliasing, unsupported B, size) */
-    TOOM_EVERIFY = 2,      /* reserved: verification failure reported by a checker */
+    TOOM_EVERIFY = 2,      /* result verification failed (residue check, toom_set_verify) */
     TOOM_EINEXACT = 3,     /* an exact division was not exact (exit code 3) */
     TOOM_ENOMEM = 4,       /* device workspace allocation failed */
     TOOM_ECUDA = 5,        /* a CUDA runtime error (no device, launch failure, ...) */
@@ -97,16 +97,48 @@ toom_status toom_mul(uint32_t *w, const uint32_t *u, size_t nu, const uint32_t *
 toom_status toom_mul_batched_host(uint32_t *w_host, const uint32_t *u_host, const uint32_t *v_host,
                                   size_t n, size_t batch, const toom_plan_t *plan, void *stream);
 
-/* Device workspace the batched call needs for this shape (bytes). */
+/* Device workspace (bytes) that toom_mul_batched_plan needs for this shape:
+ * the breadth-first recursion keeps every level's child operands and products
+ * (2B-1 per parent, Eq. 2.1) plus the long levels' scan state
+ * (SURVEY.md §5(g), H5).  0 on an invalid plan.  Covers every plan, including
+ * the schoolbook-only one (n <= 64).                                       */
 size_t toom_workspace_bytes(size_t n, size_t batch, const toom_plan_t *plan);
 
 /* Provide a caller-owned device workspace (NULL, 0 = let the library
- * allocate and cache its own).  The library uses it until replaced.        */
+ * allocate and cache its own).  Ownership stays with the caller; the library
+ * uses it until replaced and never frees it.  Without one, the library keeps
+ * one buffer PER STREAM (calls on different streams never share scratch).
+ * A caller buffer is shared by all streams: a call on another stream than the
+ * previous user's waits (stream-ordered) for that user's work first.  A call
+ * whose shape needs more than `bytes` fails with TOOM_ENOMEM.  Blocks until
+ * work using the previous buffers has finished.                            */
 toom_status toom_set_workspace(void *dev_ptr, size_t bytes);
 
-/* Sticky status of the last failed call on this host thread (TOOM_OK if none);
- * reading it clears it.                                                     */
+/* Status of the last failed call on this host thread (TOOM_OK if none);
+ * reading it clears it.  When toom_set_check / toom_set_verify are on, it
+ * first synchronizes the device and reports a device-detected failure of any
+ * call since the last read: TOOM_EINEXACT (an "exact" division left a
+ * remainder, §3; SPEC.md:462 exit code 3) or TOOM_EVERIFY (the
+ * result's residue mod 2^61-1 differs from the residues' product).         */
 toom_status toom_last_error(void);
+
+/* Debug exact-division check: every
+ * interpolation kernel of the batched path whose dividends have a known end
+ * (fused bottom rows, top-level rows, row-parallel levels) checks that the
+ * 2-adic division left no remainder (final borrow) and that the power-of-two
+ * shift dropped only zero bits.  on = 0 (default): no checks.             */
+void toom_set_check(int on);
+
+/* Result verification: after every unsigned product (toom_mul,
+ * toom_mul_batched*), a kernel checks w mod p == (u mod p)(v mod p) mod p
+ * for p = 2^61 - 1 (one warp per product, O(n) reads).  Catches any wrong
+ * limb of w with probability 1 - 2^-61 per random error.  on = 0: off.   */
+void toom_set_verify(int on);
+
+/* Fault injection for tests: kind 1 flips one bit of one
+ * base-case product inside the fused bottom kernel, so that the next exact
+ * division is inexact; 0 = off.  Never set in production.                 */
+void toom_debug_fault(int kind);
 
 /* Human-readable name of a status code (static string). */
 const char *toom_status_string(toom_status s);

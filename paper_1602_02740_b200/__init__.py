@@ -69,6 +69,9 @@ SIGNATURES = {
     "toom_interp_recompose": (_I, [_P, _P, _SZ, _SZ, _I, _P]),
     "toom_mul_signed_batched": (_I, [_P, _P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
     "toom_product_width_point": (_SZ, [_SZ, _I]),
+    "toom_set_check": (None, [_I]),
+    "toom_set_verify": (None, [_I]),
+    "toom_debug_fault": (None, [_I]),
 }
 
 
@@ -101,6 +104,15 @@ def _dev(t: torch.Tensor, name: str) -> int:
     return t.data_ptr()
 
 
+def _out(t: torch.Tensor, name: str, shape, like: torch.Tensor) -> int:
+    """A caller-supplied output must have exactly the result's shape, dtype
+    and device (the library writes every limb of it and nothing beyond)."""
+    if tuple(t.shape) != tuple(shape) or t.dtype != like.dtype or t.device != like.device:
+        raise ValueError(f"{name} must be a {like.dtype} tensor of shape {tuple(shape)} on {like.device}, "
+                         f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+    return _dev(t, name)
+
+
 def _stream(stream=None) -> int:
     s = torch.cuda.current_stream() if stream is None else stream
     return s.cuda_stream
@@ -115,7 +127,8 @@ def toom_mul_batched(u: torch.Tensor, v: torch.Tensor, B: int = 4, t4: int = 256
     if out is None:
         out = torch.empty((batch, 2 * n), dtype=u.dtype, device=u.device)
     p = plan(B, t4, t3, chunk, long_count)
-    st = lib().toom_mul_batched_plan(_dev(out, "out"), _dev(u, "u"), _dev(v, "v"), n, batch, ctypes.byref(p),
+    st = lib().toom_mul_batched_plan(_out(out, "out", (batch, 2 * n), u), _dev(u, "u"), _dev(v, "v"), n, batch,
+                                     ctypes.byref(p),
                                      _stream(stream))
     _check(st, "toom_mul_batched")
     return out
@@ -126,7 +139,9 @@ def toom_mul(u: torch.Tensor, v: torch.Tensor, B: int = 4, out: torch.Tensor | N
     nu, nv = u.numel(), v.numel()
     if out is None:
         out = torch.empty(nu + nv, dtype=u.dtype, device=u.device)
-    st = lib().toom_mul(_dev(out, "out"), _dev(u, "u") if nu else None, nu, _dev(v, "v") if nv else None, nv, B,
+    if u.dim() != 1 or v.dim() != 1 or u.dtype != v.dtype:
+        raise ValueError("u and v must be 1-D tensors of one dtype")
+    st = lib().toom_mul(_out(out, "out", (nu + nv,), u), _dev(u, "u") if nu else None, nu, _dev(v, "v") if nv else None, nv, B,
                         _stream(stream))
     _check(st, "toom_mul")
     return out
@@ -145,8 +160,12 @@ def toom_mul_batched_host(u, v, B: int = 4, t4: int = 256, t3: int = 64, chunk: 
         return x.ctypes.data
 
     batch, n = u.shape
+    if tuple(v.shape) != (batch, n):
+        raise ValueError("u and v must both be [batch][n]")
     if out is None:
         out = np.empty((batch, 2 * n), dtype=np.uint32)
+    if tuple(out.shape) != (batch, 2 * n):
+        raise ValueError(f"out must have shape {(batch, 2 * n)}")
     p = plan(B, t4, t3, chunk)
     st = lib().toom_mul_batched_host(ptr(out), ptr(u), ptr(v), n, batch, ctypes.byref(p), _stream(stream))
     _check(st, "toom_mul_batched_host")
@@ -188,9 +207,12 @@ def eval_points(a: torch.Tensor, B: int, signed: bool = False, stream=None) -> t
 def interp_recompose(y: torch.Tensor, n: int, B: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Long-path stages a4+a5: y [2B-1][batch][2e] products -> w [batch][2n]."""
     npts, batch, w2 = y.shape
+    if npts != lib().toom_npoints(B) or w2 != lib().toom_product_width_point(n, B):
+        raise ValueError(f"y must be [{lib().toom_npoints(B)}][batch][{lib().toom_product_width_point(n, B)}]")
     if out is None:
         out = torch.empty((batch, 2 * n), dtype=y.dtype, device=y.device)
-    _check(lib().toom_interp_recompose(_dev(out, "out"), _dev(y, "y"), n, batch, B, _stream(stream)),
+    _check(lib().toom_interp_recompose(_out(out, "out", (batch, 2 * n), y), _dev(y, "y"), n, batch, B,
+                                       _stream(stream)),
            "toom_interp_recompose")
     return out
 
@@ -198,11 +220,13 @@ def interp_recompose(y: torch.Tensor, n: int, B: int, out: torch.Tensor | None =
 def mul_signed_batched(u: torch.Tensor, v: torch.Tensor, B: int = 4, t4: int = 256, t3: int = 64,
                        long_count: int = 0, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Two's-complement products w[i] = u[i]*v[i] ([batch][n] -> [batch][2n])."""
+    if u.shape != v.shape or u.dim() != 2:
+        raise ValueError("u and v must both be [batch][n]")
     batch, n = u.shape
     if out is None:
         out = torch.empty((batch, 2 * n), dtype=u.dtype, device=u.device)
     p = plan(B, t4, t3, 0, long_count)
-    _check(lib().toom_mul_signed_batched(_dev(out, "out"), _dev(u, "u"), _dev(v, "v"), n, batch, ctypes.byref(p),
+    _check(lib().toom_mul_signed_batched(_out(out, "out", (batch, 2 * n), u), _dev(u, "u"), _dev(v, "v"), n, batch, ctypes.byref(p),
                                          _stream(stream)), "toom_mul_signed_batched")
     return out
 
@@ -271,3 +295,28 @@ def probe_carry_chain(stream=None) -> tuple:
     if r < 0:
         raise RuntimeError("probe failed")
     return r, ms.value
+
+
+def set_check(on: bool = True):
+    """Device-side exact-division checks (a failure reads back as
+    TOOM_EINEXACT from last_error())."""
+    lib().toom_set_check(1 if on else 0)
+
+
+def set_verify(on: bool = True):
+    """Verify every unsigned result by its residue mod 2^61-1 on the device
+    (a mismatch reads back as TOOM_EVERIFY from last_error())."""
+    lib().toom_set_verify(1 if on else 0)
+
+
+def debug_fault(kind: int = 0):
+    """Fault injection for tests: 1 = flip one bit of one base-case product in
+    the fused bottom kernel; 0 = off."""
+    lib().toom_debug_fault(int(kind))
+
+
+def last_error() -> int:
+    """toom_last_error(): the sticky host status of this thread's last failed
+    call, or a device-detected failure (TOOM_EINEXACT / TOOM_EVERIFY) when
+    set_check / set_verify are on (synchronizes the device).  Clears it."""
+    return lib().toom_last_error()

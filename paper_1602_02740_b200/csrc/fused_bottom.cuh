@@ -381,6 +381,9 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
 #pragma unroll
         for (int t = 0; t < E; ++t) { a[t] = slot[t * G]; bb[t] = slot[(E + t) * G]; }
         if (pmask & 1) mul_twos_to_smem<E>(a, bb, slot);
+        // fault injection (tests): one flipped bit of y_1 of the
+        // CTA's first instance makes the rows' exact divisions inexact
+        if (tg_fault && blockIdx.x == 0 && lane == 0 && warp == 1) slot[3 * G] ^= 1u;
     }
     __syncthreads();
 

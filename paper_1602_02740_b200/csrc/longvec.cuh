@@ -124,7 +124,10 @@ __device__ __forceinline__ LAgg lv_compose(const LAgg& A, const LAgg& B, const L
         const int q = lv_piece(B, c1);
         C.cout[p] = lv_sel(B.cout, q);
         if (o > 1) {
-            const unsigned long long x = (unsigned long long)A.g[p] * B.m + (unsigned long long)lv_negmod(c1, M) * B.m + lv_sel(B.g, q);
+            // (g + (-c) mod o) reduced before the multiply: (o-1) m + g < o^2 + o < 2^64
+            uint32_t t = A.g[p] + lv_negmod(c1, M);
+            if (t < A.g[p] || t >= o) t -= o;
+            const unsigned long long x = (unsigned long long)t * B.m + lv_sel(B.g, q);
             C.g[p] = lv_mod(x, M);
         } else {
             C.g[p] = 0;
@@ -136,7 +139,9 @@ __device__ __forceinline__ LAgg lv_compose(const LAgg& A, const LAgg& B, const L
 __device__ __forceinline__ void lv_apply(const LAgg& A, long long& c, uint32_t& beta, const LMod& M) {
     const int p = lv_piece(A, c);
     if (M.o > 1) {
-        const unsigned long long x = (unsigned long long)beta * A.m + (unsigned long long)lv_negmod(c, M) * A.m + lv_sel(A.g, p);
+        uint32_t t = beta + lv_negmod(c, M);   // both < o < 2^32: reduce before the multiply
+        if (t < beta || t >= M.o) t -= M.o;
+        const unsigned long long x = (unsigned long long)t * A.m + lv_sel(A.g, p);
         beta = lv_mod(x, M);
     }
     c = lv_sel(A.cout, p);

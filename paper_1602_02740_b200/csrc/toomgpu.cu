@@ -23,6 +23,7 @@
 #include <type_traits>
 
 #include "../../include/toomgpu.h"
+#include "check.cuh"
 #include "generated/toom_programs.cuh"
 
 namespace tg {
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(128) k_eval(const uint32_t* __restrict__ srcU,
                                               uint32_t* __restrict__ outU, uint32_t* __restrict__ outV,
                                               size_t count, int n, int b, int e) {
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= 2 * count) return;
+    if (gid >= (srcV ? 2 : 1) * count) return;   // srcV = nullptr: one operand only
     const int which = gid >= count;
     const size_t c = which ? gid - count : gid;
     const uint32_t* src = which ? srcV : srcU;
@@ -593,10 +594,21 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
 // ------------------------------------------------------------------------
 // workspace + error state
 // ------------------------------------------------------------------------
+// Workspace.  Library-owned buffers are kept PER STREAM (calls on different
+// streams never share scratch memory; a buffer grows only after its own
+// stream has drained).  A caller-provided buffer (toom_set_workspace) is
+// shared by every stream: a call holds it from the first use to the end of
+// its enqueue and records an event; a call on another stream first waits for
+// that event (stream-ordered, no host sync).
 static std::mutex g_ws_mu;
-static void* g_ws = nullptr;
-static size_t g_ws_bytes = 0;
-static bool g_ws_owned = true;
+struct WsEntry { cudaStream_t st; void* p; size_t bytes; };
+static std::vector<WsEntry> g_ws_list;   // library-owned, one per stream
+static void* g_user_ws = nullptr;        // caller-owned (toom_set_workspace)
+static size_t g_user_bytes = 0;
+static std::mutex g_user_mu;             // held by the call using g_user_ws
+static cudaEvent_t g_user_ev = nullptr;
+static cudaStream_t g_user_last = nullptr;
+static bool g_user_used = false;
 static thread_local toom_status t_last = TOOM_OK;
 static thread_local size_t t_launches = 0;
 
@@ -631,27 +643,82 @@ static toom_status fail(toom_status s) {
 static thread_local void* t_ws_override = nullptr;
 static thread_local size_t t_ws_override_bytes = 0;
 
-static toom_status get_ws(size_t bytes, void** out) {
+// A workspace lease: ws_acquire(bytes, stream) gives the scratch for one call
+// on `stream`; ws_release() ends it (records the caller-buffer event).
+struct WsLease {
+    bool user = false;
+    cudaStream_t st = nullptr;
+};
+static thread_local WsLease t_lease;
+static thread_local int t_lease_depth = 0;
+
+static toom_status get_ws(size_t bytes, void** out, cudaStream_t st) {
     if (t_ws_override) {
         if (bytes > t_ws_override_bytes) return TOOM_ENOMEM;
         *out = t_ws_override;
         return TOOM_OK;
     }
-    std::lock_guard<std::mutex> g(g_ws_mu);
-    if (bytes <= g_ws_bytes && g_ws) { *out = g_ws; return TOOM_OK; }
-    if (!g_ws_owned) return TOOM_ENOMEM;
-    if (g_ws) { cudaDeviceSynchronize(); cudaFree(g_ws); g_ws = nullptr; g_ws_bytes = 0; }
-    if (cudaMalloc(&g_ws, bytes) != cudaSuccess) { cudaGetLastError(); g_ws = nullptr; return TOOM_ENOMEM; }
-    g_ws_bytes = bytes;
-    *out = g_ws;
+    if (t_lease_depth > 0) return TOOM_EINVAL;   // one lease per call
+    {
+        std::lock_guard<std::mutex> g(g_ws_mu);
+        if (!g_user_ws) {
+            for (auto& e : g_ws_list) {
+                if (e.st != st) continue;
+                if (bytes <= e.bytes) { *out = e.p; ++t_lease_depth; t_lease = WsLease{false, st}; return TOOM_OK; }
+                // grow: only this stream uses the buffer, so draining it suffices
+                cudaStreamSynchronize(st);
+                cudaFree(e.p);
+                e.p = nullptr;
+                e.bytes = 0;
+                if (cudaMalloc(&e.p, bytes) != cudaSuccess) { cudaGetLastError(); return TOOM_ENOMEM; }
+                e.bytes = bytes;
+                *out = e.p;
+                ++t_lease_depth;
+                t_lease = WsLease{false, st};
+                return TOOM_OK;
+            }
+            WsEntry e{st, nullptr, 0};
+            if (cudaMalloc(&e.p, bytes) != cudaSuccess) { cudaGetLastError(); return TOOM_ENOMEM; }
+            e.bytes = bytes;
+            g_ws_list.push_back(e);
+            *out = e.p;
+            ++t_lease_depth;
+            t_lease = WsLease{false, st};
+            return TOOM_OK;
+        }
+    }
+    // caller-owned buffer: exclusive until ws_release
+    g_user_mu.lock();
+    if (!g_user_ws || bytes > g_user_bytes) { g_user_mu.unlock(); return TOOM_ENOMEM; }
+    if (!g_user_ev) cudaEventCreateWithFlags(&g_user_ev, cudaEventDisableTiming);
+    if (g_user_used && g_user_last != st) cudaStreamWaitEvent(st, g_user_ev, 0);
+    *out = g_user_ws;
+    ++t_lease_depth;
+    t_lease = WsLease{true, st};
     return TOOM_OK;
 }
+
+static void ws_release() {
+    if (t_lease_depth == 0) return;
+    --t_lease_depth;
+    if (t_lease.user) {
+        cudaEventRecord(g_user_ev, t_lease.st);
+        g_user_last = t_lease.st;
+        g_user_used = true;
+        g_user_mu.unlock();
+    }
+    t_lease = WsLease{};
+}
+struct WsGuard {
+    bool on = false;
+    ~WsGuard() { if (on) ws_release(); }
+};
 
 static inline unsigned nblk(size_t threads, int bs = 128) { return (unsigned)((threads + bs - 1) / bs); }
 
 static toom_status launch_eval(int B, bool top, const uint32_t* su, const uint32_t* sv, uint32_t* ou, uint32_t* ov,
                                size_t count, int n, int b, int e, cudaStream_t st) {
-    const unsigned g = nblk(2 * count);
+    const unsigned g = nblk((sv ? 2 : 1) * count);
     if (g == 0) return TOOM_OK;
     ProfScope ps(CAT_EVAL, st);
 #define TG_EV(BB)                                                                          \
@@ -817,7 +884,9 @@ static toom_status launch_eval_top_rows(const Level& Lv, const uint32_t* u, cons
                                         uint32_t* V1, cudaStream_t st) {
     ProfScope ps(CAT_EVAL, st);
     const unsigned grid = (unsigned)((Lv.count + 31) / 32);
-    const bool v4 = g_eval_v4 && Lv.B <= 4 && (Lv.n & 3) == 0 && (Lv.b & 3) == 0;
+    // 16-byte cp.async staging needs 16-byte aligned operand rows
+    const bool v4 = g_eval_v4 && Lv.B <= 4 && (Lv.n & 3) == 0 && (Lv.b & 3) == 0 &&
+                    ((((uintptr_t)u) | ((uintptr_t)v)) & 15) == 0;
     if (v4 && Lv.B == 3) k_eval_top_v4<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     else if (v4) k_eval_top_v4<4><<<grid, 32 * 7, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     else if (Lv.B == 3) k_eval_top_rows<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
@@ -1490,6 +1559,13 @@ static int g_split_streams = [] {
     return e ? atoi(e) : 1;   // off: two streams measured 1.072 vs 1.075 ms on C2 (no gain), three slower
 }();
 
+// device workspace of one call with this plan (the schoolbook-only plan
+// needs transposed operand / product buffers instead of level buffers)
+static size_t ws_need(const Plan& plan, size_t chunk, size_t n) {
+    if (plan.lv.size() == 1) return (2 * ((chunk * (n + 1) + 63) & ~(size_t)63) + 2 * chunk * (n + 1)) * 4;
+    return plan.bytes;
+}
+
 static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
                            const toom_plan_t& p, cudaStream_t st, bool sgn = false);
 
@@ -1519,7 +1595,9 @@ static toom_status batched_split(uint32_t* w, const uint32_t* u, const uint32_t*
     if ((s = make_plan((int)n, part, p, plan, sgn))) return s;
     const size_t per = (plan.bytes + 255) & ~(size_t)255;
     void* ws = nullptr;
-    if ((s = get_ws(per * S, &ws))) return s;
+    WsGuard wg;
+    if ((s = get_ws(per * S, &ws, st))) return s;
+    wg.on = true;
     cudaEvent_t start = evs[S];
     cudaEventRecord(start, st);
     size_t launches = 0;
@@ -1543,8 +1621,31 @@ static toom_status batched_split(uint32_t* w, const uint32_t* u, const uint32_t*
     return cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA;
 }
 
+static bool g_verify = false;   // toom_set_verify: residue check of every unsigned result
+static bool g_check = false;    // toom_set_check: device exact-division checks
+
+static toom_status batched_core(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
+                                const toom_plan_t& p, cudaStream_t st, bool sgn);
+
+static void launch_verify(const uint32_t* u, size_t nu, const uint32_t* v, size_t nv, const uint32_t* w, size_t batch,
+                          cudaStream_t st) {
+    if (!batch) return;
+    k_verify_m61<<<nblk(batch * 32, 256), 256, 0, st>>>(u, nu, v, nv, w, batch);
+    ++t_launches;
+}
+
 static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
                            const toom_plan_t& p, cudaStream_t st, bool sgn) {
+    toom_status s = batched_core(w, u, v, n, batch, p, st, sgn);
+    if (s == TOOM_OK && g_verify && !sgn && batch) {
+        launch_verify(u, n, v, n, w, batch, st);
+        if (cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+    }
+    return s;
+}
+
+static toom_status batched_core(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
+                                const toom_plan_t& p, cudaStream_t st, bool sgn) {
     t_launches = 0;
     if (n == 0 || n > (1u << 30)) return TOOM_EINVAL;
     if (batch == 0) return TOOM_OK;
@@ -1564,10 +1665,11 @@ static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, si
     // shapes) share the SMs with those of the other
     if (!p.chunk && g_split_streams > 1 && batch >= 8192 && !plan.lv[0].lng && !t_prof && plan.lv.size() > 1)
         return batched_split(w, u, v, n, batch, p, st, sgn);
-    size_t need = plan.bytes;
-    if (plan.lv.size() == 1) need = (2 * ((chunk * (n + 1) + 63) & ~(size_t)63) + 2 * chunk * (n + 1)) * 4;
+    const size_t need = ws_need(plan, chunk, n);
     void* ws = nullptr;
-    if ((s = get_ws(need, &ws))) return s;
+    WsGuard wg;
+    if ((s = get_ws(need, &ws, st))) return s;
+    wg.on = true;
     for (size_t c0 = 0; c0 < batch; c0 += chunk) {
         const size_t cnt = (batch - c0 < chunk) ? batch - c0 : chunk;
         if (cnt != chunk) {
@@ -1616,7 +1718,9 @@ static toom_status run_long_standalone(size_t slot_limbs, size_t tiles, size_t n
                  bD = rnd(nops * sizeof(LOpDev));
     void* ws = nullptr;
     toom_status s;
-    if ((s = get_ws(bS + bT + bC + bD, &ws))) return s;
+    WsGuard wg;
+    if ((s = get_ws(bS + bT + bC + bD, &ws, st))) return s;
+    wg.on = true;
     uint8_t* base = (uint8_t*)ws;
     LStatus* status = (LStatus*)(base + bS);
     unsigned* ctr = (unsigned*)(base + bS + bT);
@@ -1723,21 +1827,35 @@ toom_status toom_mul(uint32_t* w, const uint32_t* u, size_t nu, const uint32_t* 
     }
     const size_t n = nu > nv ? nu : nv;
     toom_plan_t p = toom_default_plan(B);
-    // padded operands and a 2n-limb product buffer (separate allocation)
-    uint32_t *pu = nullptr, *pv = nullptr, *pw = nullptr;
-    if (cudaMallocAsync((void**)&pu, n * 4, st) != cudaSuccess || cudaMallocAsync((void**)&pv, n * 4, st) != cudaSuccess ||
-        cudaMallocAsync((void**)&pw, 2 * n * 4, st) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(TOOM_ENOMEM);
+    if (nu == nv) return fail(batched(w, u, v, n, 1, p, st));   // w has exactly 2n limbs: no copies
+    // unbalanced: the shorter operand zero-padded to n limbs in
+    // the call's workspace, behind the plan's own scratch; w has nu+nv < 2n
+    // limbs, so the 2n-limb product also lives in the workspace and its low
+    // nu+nv limbs (the high ones are zero) are copied out
+    Plan pl;
+    if ((s = make_plan((int)n, 1, p, pl))) return fail(s);
+    const size_t wsb = (ws_need(pl, 1, n) + 255) & ~(size_t)255;
+    const size_t pad = ((4 * n * 4) + 255) & ~(size_t)255;
+    void* ws = nullptr;
+    WsGuard wg;
+    if ((s = get_ws(wsb + pad, &ws, st))) return fail(s);
+    wg.on = true;
+    uint32_t* pu = (uint32_t*)((uint8_t*)ws + wsb);
+    uint32_t* pv = pu + n;
+    uint32_t* pw = pv + n;
+    const uint32_t* su = u;
+    const uint32_t* sv = v;
+    if (nu < n) { k_pad_copy<<<nblk(n, 256), 256, 0, st>>>(u, nu, pu, n); su = pu; }
+    if (nv < n) { k_pad_copy<<<nblk(n, 256), 256, 0, st>>>(v, nv, pv, n); sv = pv; }
+    t_ws_override = ws;
+    t_ws_override_bytes = wsb;
+    s = batched(pw, su, sv, n, 1, p, st);
+    t_ws_override = nullptr;
+    t_ws_override_bytes = 0;
+    if (s == TOOM_OK) {
+        k_pad_copy<<<nblk(nu + nv, 256), 256, 0, st>>>(pw, nu + nv, w, nu + nv);
+        t_launches += 2;
     }
-    k_pad_copy<<<nblk(n, 256), 256, 0, st>>>(u, nu, pu, n);
-    k_pad_copy<<<nblk(n, 256), 256, 0, st>>>(v, nv, pv, n);
-    s = batched(pw, pu, pv, n, 1, p, st);
-    if (s == TOOM_OK) k_pad_copy<<<nblk(nu + nv, 256), 256, 0, st>>>(pw, nu + nv, w, nu + nv);
-    t_launches += 3;
-    cudaFreeAsync(pu, st);
-    cudaFreeAsync(pv, st);
-    cudaFreeAsync(pw, st);
     if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
     return fail(s);
 }
@@ -1779,8 +1897,7 @@ toom_status toom_mul_batched_host(uint32_t* w_host, const uint32_t* u_host, cons
     pc.chunk = 0;
     Plan pl;
     if ((s = make_plan((int)n, chunk, pc, pl))) return fail(s);
-    size_t wsb = pl.bytes;
-    if (pl.lv.size() == 1) wsb = (2 * ((chunk * (n + 1) + 63) & ~(size_t)63) + 2 * chunk * (n + 1)) * 4;
+    size_t wsb = ws_need(pl, chunk, n);
     wsb = (wsb + 255) & ~(size_t)255;
     const size_t io = ((4 * n * chunk * 4) + 255) & ~(size_t)255;   // u, v, w of a chunk
     const size_t per = io + wsb;
@@ -1832,21 +1949,56 @@ size_t toom_workspace_bytes(size_t n, size_t batch, const toom_plan_t* plan) {
     if (chunk > batch) chunk = batch;
     Plan pl;
     if (make_plan((int)n, chunk, p, pl) != TOOM_OK) return 0;
-    return pl.bytes;
+    return ws_need(pl, chunk, n);
 }
 
 toom_status toom_set_workspace(void* dev_ptr, size_t bytes) {
     std::lock_guard<std::mutex> g(g_ws_mu);
-    if (g_ws_owned && g_ws) { cudaDeviceSynchronize(); cudaFree(g_ws); }
-    if (dev_ptr) { g_ws = dev_ptr; g_ws_bytes = bytes; g_ws_owned = false; }
-    else { g_ws = nullptr; g_ws_bytes = 0; g_ws_owned = true; }
+    std::lock_guard<std::mutex> gu(g_user_mu);   // no call is using the caller buffer
+    // the library's own buffers are released (after the device drained)
+    if (!g_ws_list.empty()) cudaDeviceSynchronize();
+    for (auto& e : g_ws_list) cudaFree(e.p);
+    g_ws_list.clear();
+    if (g_user_ws && g_user_used) cudaEventSynchronize(g_user_ev);   // the previous caller buffer is idle
+    g_user_ws = dev_ptr;
+    g_user_bytes = dev_ptr ? bytes : 0;
+    g_user_used = false;
+    g_user_last = nullptr;
     return TOOM_OK;
 }
 
 toom_status toom_last_error(void) {
     toom_status s = t_last;
     t_last = TOOM_OK;
+    if (g_check || g_verify) {
+        // device-detected failures: read back and clear
+        unsigned f = 0;
+        if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpyFromSymbol(&f, tg_err_flags, sizeof f) != cudaSuccess) {
+            cudaGetLastError();
+            return s == TOOM_OK ? TOOM_ECUDA : s;
+        }
+        if (f) {
+            const unsigned z = 0;
+            cudaMemcpyToSymbol(tg_err_flags, &z, sizeof z);
+            if (s == TOOM_OK) s = (f & 1u) ? TOOM_EINEXACT : TOOM_EVERIFY;
+        }
+    }
     return s;
+}
+
+void toom_set_check(int on) {
+    g_check = on != 0;
+    const int v = g_check ? 1 : 0;
+    cudaMemcpyToSymbol(tg_check_on, &v, sizeof v);
+    cudaGetLastError();
+}
+
+void toom_set_verify(int on) { g_verify = on != 0; }
+
+void toom_debug_fault(int kind) {
+    const int v = kind;
+    cudaMemcpyToSymbol(tg_fault, &v, sizeof v);
+    cudaGetLastError();
 }
 
 const char* toom_status_string(toom_status s) {
@@ -1948,9 +2100,9 @@ toom_status toom_eval_top(uint32_t* out, const uint32_t* a, size_t n, size_t bat
     toom_status s = check_device();
     if (s) return fail(s);
     const int e = (int)toom_eval_width(n, B);
-    // reuse the two-operand kernel with the same source twice: out gets both copies
-    // of the evaluation; only the first half (operand "u") is the requested output.
-    s = launch_eval(B, true, a, a, out, out, batch, (int)n, b, e, (cudaStream_t)stream);
+    // the two-operand kernel with no second operand (srcV = nullptr: one
+    // thread per instance, every output limb stored once)
+    s = launch_eval(B, true, a, nullptr, out, nullptr, batch, (int)n, b, e, (cudaStream_t)stream);
     if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
     return fail(s);
 }

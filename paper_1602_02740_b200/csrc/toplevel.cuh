@@ -540,6 +540,17 @@ __device__ __forceinline__ void cp_async4(uint32_t* dst_smem, const uint32_t* sr
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
 }
 
+// exactness check of row j (csrc/check.cuh): the products are read modulo
+// 2^(32 ywidth), so a negative y_k adds -A_jk 2^(32 ywidth) to the dividend
+template <int B>
+__device__ __forceinline__ uint64_t row_sign_corr(int j, const uint32_t* Y, int ywidth, int G, int lane) {
+    uint64_t corr = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * B - 1; ++k)
+        corr += (uint64_t)rowA<B>(j, k) * (Y[((size_t)k * ywidth + ywidth - 1) * G + lane] >> 31);
+    return corr;
+}
+
 template <int B, int J>
 __device__ __forceinline__ uint32_t rowstep_j(const uint32_t (&y)[2 * B - 1], tg_rowstate& st) {
     if constexpr (B == 3) {
@@ -580,6 +591,7 @@ __device__ __forceinline__ void interp_rows_inplace(uint32_t* Y, int ywidth, int
 #pragma unroll
                     for (int k = 0; k < NP; ++k) y[k] = yb[k][off];
                     ob[tt] = rowstep_j<B, J>(y, st);
+                    if (t == 0) TG_CHECK_LOW(st.qp, rowS<B>(J));
                 }
             }
         }
@@ -593,6 +605,7 @@ __device__ __forceinline__ void interp_rows_inplace(uint32_t* Y, int ywidth, int
         }
         __syncthreads();
     }
+    if (work && TG_CHECK_ENABLED) TG_CHECK_END(st.acc - row_sign_corr<B>(J, Y, ywidth, G, lane), st.bor, rowO<B>(J));
 }
 
 // YW_, G_, LW_, B_ != 0 fix ywidth, G, Lw and b at compile time (the C2 shape):
@@ -692,7 +705,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
         const int len = min(b, wout);
         if (lane < nin) {
             int r = 0;
-            if ((wout & 3) == 0)
+            if ((wout & 3) == 0 && (((uintptr_t)w) & 15) == 0)
                 for (; r + 4 <= len; r += 4)
                     *reinterpret_cast<uint4*>(row0 + r) =
                         make_uint4(y0[r * G], y0[(r + 1) * G], y0[(r + 2) * G], y0[(r + 3) * G]);
@@ -733,6 +746,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
 #pragma unroll
                         for (int k = 0; k < NP; ++k) y[k] = Y[(k * ywidth + t) * G + lane];
                         ob[tt] = rowstep<B>(j, y, st);
+                        if (t == 0) TG_CHECK_LOW(st.qp, rowS<B>(j));
                     }
                 }
             }
@@ -746,6 +760,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
             }
             __syncthreads();
         }
+        if (rw && TG_CHECK_ENABLED) TG_CHECK_END(st.acc - row_sign_corr<B>(j, Y, ywidth, G, lane), st.bor, rowO<B>(j));
     }
     // ---- phase 2: recomposition (every w_j >= 0 at the top level).  Segment
     // s limb r = w_s[r] + w_{s-1}[b + r] (+ w_{s-2}[2b] at r = 0); absent rows
@@ -776,7 +791,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_interp_top_smem(const uint
             uint64_t carry = extraC(s);
             uint32_t ones = 0xFFFFFFFFu, l0 = 0;
             int r = 0;
-            if (((s * b) & 3) == 0 && (wout & 3) == 0) {
+            if (((s * b) & 3) == 0 && (wout & 3) == 0 && (((uintptr_t)w) & 15) == 0) {
                 for (; r + 4 <= len; r += 4) {
                     uint32_t o[4];
 #pragma unroll
@@ -1049,8 +1064,11 @@ __global__ void __launch_bounds__(128) k_interp_rows_p8(const uint32_t* __restri
     uint32_t y0[NP], y1[NP];
     ld(0, y0);
     ld(1, y1);
+    // with the exactness check on, the chains run 3 limbs further so that the
+    // whole dividend (up to o1 o2 < 2^64 times the quotient) is inside the window
+    const int tlast = tend + (tg_check_on ? 3 : 0);
 #pragma unroll 1
-    for (int t = 0; t < tend; ++t) {
+    for (int t = 0; t < tlast; ++t) {
         uint32_t y[NP];
 #pragma unroll
         for (int k = 0; k < NP; ++k) { y[k] = y0[k]; y0[k] = y1[k]; }
@@ -1064,7 +1082,19 @@ __global__ void __launch_bounds__(128) k_interp_rows_p8(const uint32_t* __restri
         // quotient limb t; output limb u = t - a (r = 0) or t - a - 1 (r > 0)
         const int u = t - a - (r ? 1 : 0);
         if (u >= 0 && u < Lw) dst[(size_t)u * count] = r ? __funnelshift_r(qp, q, r) : q;
+        if (t <= a && tg_check_on) tg_check_low(t < a ? (q ? 1u : 0u) : q, t < a ? 1 : r);   // exact 2^sh
         qp = q;
+    }
+    if (tg_check_on) {
+        // the dividend ended (tend >= its length): carry 0 / -1, borrows 0 / o-1
+        // the tlast-limb window holds y_k mod 2^(32 tlast): negative y_k add
+        // -m_k 2^(32 tlast) (csrc/check.cuh); the first quotient's own carry
+        // past the window is then (acc - b1) / o1
+        long long ac = acc;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) ac -= m[k] * (long long)(fill[k] & 1u);
+        tg_check_end((uint64_t)ac, b1, o1);
+        if (o2 > 1) tg_check_end((uint64_t)((ac - (long long)b1) / (long long)o1), b2, o2);
     }
 }
 
@@ -1215,6 +1245,15 @@ __global__ void __launch_bounds__(128) k_interp_rows_w(const uint32_t* __restric
         ld(t + 2, y1);
         const uint32_t r = rowstep<B>(j, y, st);
         if (t >= 1) dst[(size_t)(t - 1) * count] = r;
+        else TG_CHECK_LOW(st.qp, rowS<B>(j));
+    }
+    if (TG_CHECK_ENABLED) {
+        // the window of Lw+1 limbs holds y_k mod 2^(32 (Lw+1)): a negative y_k
+        // adds -A_jk 2^(32 (Lw+1)) to the dividend (csrc/check.cuh)
+        uint64_t corr = 0;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) corr += (uint64_t)rowA<B>(j, k) * (fill[k] & 1u);
+        TG_CHECK_END(st.acc - corr, st.bor, rowO<B>(j));
     }
 }
 

@@ -825,9 +825,11 @@ def emit_row_functions(ps: PointSet) -> str:
         else:
             L.append("    return (uint32_t)lin;")
         L.append("  };")
+        bor = "bor" if op.odiv != 1 else "0u"
         if ps.B >= 4:
             # peeled (C2 fused 426 -> 418 us)
             L.append("  qp = step(0);")
+            L.append(f"  TG_CHECK_LOW(qp, {op.shr});")
             L.append(f"  TG_ROW_UNROLL_{ps.name}")
             L.append("  for (int t = 1; t <= Lw; ++t) {")
             L.append("    const uint32_t q = step(t);")
@@ -840,8 +842,20 @@ def emit_row_functions(ps: PointSet) -> str:
             L.append("  for (int t = 0; t <= Lw; ++t) {")
             L.append("    const uint32_t q = step(t);")
             L.append(f"    if (t > 0) dst[(t - 1) * 32] = tg_shr_limb_or_delay(qp, q, {op.shr});")
+            L.append(f"    else TG_CHECK_LOW(q, {op.shr});")
             L.append("    qp = q;")
             L.append("  }")
+        # debug exactness check: after the last position the
+        # value D_j w_j is fully sign-extended, so the carry is 0 / -1 and the
+        # 2-adic borrow 0 / o-1 exactly when the division was exact
+        # (the y_k are read mod 2^(32 W2): a negative y_k adds -A_k 2^(32 W2)
+        # to the true dividend, so the carry is corrected by its sign)
+        L.append("  if (TG_CHECK_ENABLED) {")
+        L.append("    uint64_t corr = 0;")
+        for k, m in idx:
+            L.append(f"    corr += (uint64_t)({m}ll) * (Y[({k} * W2 + W2 - 1) * 32] >> 31);")
+        L.append(f"    TG_CHECK_END(acc - corr, {bor}, {op.odiv}u);")
+        L.append("  }")
         L.append("}")
     return "\n".join(L)
 
@@ -972,6 +986,17 @@ HEADER = """// AUTO-GENERATED by paper_1602_02740_b200/gen/toomgen.py -- do not 
 #  else
 #    define TG_CONST static const
 #  endif
+#endif
+// optional exact-division checks (defined by the CUDA library, csrc/check.cuh;
+// no-ops elsewhere)
+#ifndef TG_CHECK_LOW
+#  define TG_CHECK_LOW(q0, s) ((void)0)
+#endif
+#ifndef TG_CHECK_END
+#  define TG_CHECK_END(acc, bor, o) ((void)0)
+#endif
+#ifndef TG_CHECK_ENABLED
+#  define TG_CHECK_ENABLED 0
 #endif
 #ifndef TG_HELPERS_DEFINED
 #define TG_HELPERS_DEFINED

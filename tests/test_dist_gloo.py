@@ -144,3 +144,65 @@ def test_single_rank_path_int_ops():
     v = torch.from_numpy(synth.uniform_limbs(seed, 4, 1, 1, n)[0])
     w = tgdist.sharded_mul(u, v, n, IntOps())
     assert synth.to_int(w.numpy()) == synth.to_int(u.numpy()) * synth.to_int(v.numpy())
+
+
+# ---------------------------------------------------------------- C2 slices
+# bench.py splits the ONE C2 batch into contiguous slices of 65536/P products
+# (strong scaling); each rank generates its own slice from
+# the counter-based stream.  Check with gloo ranks that the slices partition
+# the batch and that the per-rank inputs are exactly the full batch's rows.
+
+def _c2_worker(rank, world, port, total, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = bench.c2_slice(rank, world, total)
+        u, v = bench.c2_inputs(lo, hi, 16)
+        # exact products of this slice (Python integers; the compute is not under test)
+        w = np.stack([to_limbs(synth.to_int(a) * synth.to_int(b), 32) for a, b in zip(u, v)])
+        m = -(-total // world)
+        pad = np.zeros((m, 32), np.uint32)
+        pad[: hi - lo] = w
+        gl = [torch.zeros((m, 32), dtype=torch.int32) for _ in range(world)]
+        cnt = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(gl, torch.from_numpy(pad.view(np.int32)))
+        dist.all_gather(cnt, torch.tensor([hi - lo]))
+        if rank == 0:
+            rows = np.concatenate([g.numpy().view(np.uint32)[: int(c)] for g, c in zip(gl, cnt)])
+            uf, vf = bench.c2_inputs(0, total, 16)
+            want = np.stack([to_limbs(synth.to_int(a) * synth.to_int(b), 32) for a, b in zip(uf, vf)])
+            q.put(rows.shape[0] == total and np.array_equal(rows, want))
+        else:
+            q.put(True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_c2_strong_scaling_slices_gloo(world):
+    total = 101
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_c2_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(res) and len(res) == world
+
+
+def test_c2_slices_partition_the_batch():
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    for world in (1, 2, 3, 4, 8):
+        s = [bench.c2_slice(r, world) for r in range(world)]
+        assert s[0][0] == 0 and s[-1][1] == 65536
+        assert all(s[i][1] == s[i + 1][0] for i in range(world - 1))
+        assert max(h - l for l, h in s) - min(h - l for l, h in s) <= 1

@@ -128,15 +128,18 @@ def test_c2_slice_bit_exact():
     assert np.array_equal(w, want)
 
 
-def test_c2_full_batch_sampled_and_residues():
-    # the bench launch configuration: all 65536 products in one call
+def test_c2_full_batch_bit_exact():
+    """The bench launch configuration: all 65536 products of BASELINE configs[1]
+    in one call, every product compared with the oracle O2 (w = uv
+    is unique), plus residues on a sample."""
+    import os
     u, v = synth.config_inputs(2)
     w = run_batched(u, v, 4, **C2_PLAN)
+    want = oracle.toom_batched(u, v, top_B=4, threads=os.cpu_count() or 8)
+    bad = np.nonzero((w != want).any(axis=1))[0]
+    assert bad.size == 0, f"{bad.size} of 65536 products differ, first {bad[:8]}"
     rng = np.random.default_rng(2)
-    idx = np.unique(np.concatenate([[0, 65535], rng.integers(0, 65536, 254)]))
-    want = oracle.toom_batched(u[idx], v[idx], top_B=4, threads=8)
-    assert np.array_equal(w[idx], want)
-    for i in rng.integers(0, 65536, 64):
+    for i in rng.integers(0, 65536, 16):
         check_residues(u[i], v[i], w[i])
 
 
@@ -147,25 +150,35 @@ def test_c2_chunked_equals_unchunked():
     assert np.array_equal(a, b)
 
 
-def test_c3_classes_closed_forms_and_oracle():
+def test_c3_every_product_closed_forms_and_oracle():
+    """BASELINE configs[2] in full (4096 products, one call): every product of
+    the three structured quarters against its closed form,
+    every uniform product against the oracle O2."""
+    import os
     u, v = synth.config_inputs(3)
     w = run_batched(u, v, 8)
     n, N = 2048, 65536
-    ones = (1 << (2 * N)) - (1 << (N + 1)) + 1
-    for i in range(0, 1024, 97):
-        assert I(w[i]) == ones
+    # all-ones quarter: (2^N - 1)^2 = 2^2N - 2^(N+1) + 1
+    ones = synth.from_int((1 << (2 * N)) - (1 << (N + 1)) + 1, 2 * n)
+    assert (w[0:1024] == ones[None, :]).all()
+    # alternating quarter: u = v, (2^32 + 1)^2 w = 2^64 (2^N - 1)^2
     alt_u = I(u[1024])
-    for i in range(1024, 2048, 101):
-        assert (2**32 + 1) ** 2 * I(w[i]) == 2**64 * (2**N - 1) ** 2
-        assert I(w[i]) == alt_u * alt_u
-    for i in range(2048, 3072, 37):
+    alt = synth.from_int(alt_u * alt_u, 2 * n)
+    assert (2**32 + 1) ** 2 * I(alt) == 2**64 * (2**N - 1) ** 2
+    assert (u[1024:2048] == u[1024][None, :]).all() and (v[1024:2048] == u[1024][None, :]).all()
+    assert (w[1024:2048] == alt[None, :]).all()
+    # single-bit quarter: 2^(a+c), one nonzero limb
+    for i in range(2048, 3072):
         a, c = synth.c3_bits(synth.seed_for(3), i)
-        assert I(w[i]) == 1 << (a + c)
-    sample = list(range(3072, 4096, 64)) + [4095]
-    want = oracle.toom_batched(u[sample], v[sample], top_B=8, threads=8)
-    assert np.array_equal(w[sample], want)
-    # every product: residues mod 8 seeded 61-bit primes
-    for i in range(0, 4096, 7):
+        e = a + c
+        row = w[i]
+        nz = np.flatnonzero(row)
+        assert nz.tolist() == [e // 32] and int(row[e // 32]) == 1 << (e % 32), i
+    # uniform quarter: the oracle on every product
+    want = oracle.toom_batched(u[3072:], v[3072:], top_B=8, threads=os.cpu_count() or 8)
+    bad = np.nonzero((w[3072:] != want).any(axis=1))[0]
+    assert bad.size == 0, f"{bad.size} uniform products differ"
+    for i in range(0, 4096, 257):
         check_residues(u[i], v[i], w[i])
 
 
@@ -205,8 +218,12 @@ def test_empty_batch_and_errors():
     with pytest.raises(tg.ToomError) as ei:
         tg.toom_mul_batched(x, x, B=5)
     assert ei.value.status == tg.TOOM_EINVAL
-    with pytest.raises(tg.ToomError):
-        tg.toom_mul_batched(x, x, B=3, out=x.view(2, 192))   # aliasing
+    big = torch.zeros(4 * 192 + 96, dtype=torch.uint32, device="cuda")
+    with pytest.raises(tg.ToomError) as ei:                  # aliasing: w overlaps u
+        tg.toom_mul_batched(big[96:96 + 384].view(4, 96), x, B=3, out=big[:768].view(4, 192))
+    assert ei.value.status == tg.TOOM_EINVAL
+    with pytest.raises(ValueError):                         # wrong output shape
+        tg.toom_mul_batched(x, x, B=3, out=x.view(2, 192))
     with pytest.raises(TypeError):
         tg.toom_mul_batched(x.cpu(), x.cpu(), B=3)            # no CPU fallback
 
@@ -348,9 +365,10 @@ def test_c5_full():
     assert I(w[:2]) == (I(u[:2]) * I(v[:2])) % (1 << 64)
 
 
-@pytest.mark.slow
-@pytest.mark.skipif(not __import__("os").environ.get("TOOM_SLOW"), reason="minutes of CPU oracle; set TOOM_SLOW=1")
 def test_c5_full_oracle():
+    """configs[4] at full size, bit-exact against the oracle's recursive Toom
+    (the paper's points 0, +-2^j at the top; about 50 s on the
+    box's host cores)."""
     import os
     u, v = synth.config_inputs(5)
     w = host(tg.toom_mul(dev(u), dev(v), B=16))
