@@ -370,6 +370,8 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 }  // namespace tg
 #include "fused_bottom.cuh"
 #include "longvec.cuh"
+#include "longvec2.cuh"
+#include "level34.cuh"
 #include "toplevel.cuh"
 namespace tg {
 
@@ -384,7 +386,8 @@ struct Level {
     int e = 0;          // child operand width
     int Lw = 0;         // interpolation output width per coefficient
     int npts = 0;
-    bool lng = false;   // long-vector (limb-parallel) level
+    bool lng = false;   // long-vector (limb-parallel) level: row-major child layouts
+    bool res = false;   // ... run instance-resident (one CTA per instance, level34.cuh)
     size_t offU = 0, offV = 0, offP = 0, offW = 0;   // child operands/products, this level's scratch
 };
 
@@ -477,6 +480,22 @@ static int g_long_max_count = [] {
     return e ? atoi(e) : 8000;   // C5: 220 -> 150 ms (levels 4, 5 instance-parallel); C4 unchanged
 }();
 
+// instance-resident levels (level34.cuh): operands of at most this many limbs
+static int g_res_max_n = [] {
+    const char* e = getenv("TOOM_RES_MAX_N");
+    return e ? atoi(e) : 4200;
+}();
+// ... and at least this many (below: one thread per instance has parallelism
+// enough and no scan overhead; measured on C4's 1026- and 258-limb levels)
+static int g_res_min_n = [] {
+    const char* e = getenv("TOOM_RES_MIN_N");
+    return e ? atoi(e) : 2000;
+}();
+static bool g_res_on = [] {
+    const char* e = getenv("TOOM_RES");
+    return e ? atoi(e) != 0 : true;
+}();
+
 // one warp per product (k_interp_top_warp) needs the products row-major; CH
 // positions per lane, CH = ceil((2n+1)/32) rounded up to an instantiated size
 static int top_warp_ch(const Level& Lv) {
@@ -518,15 +537,34 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         // default (long_count = 0): operands longer than 2048 limbs (few,
         // long vectors: one thread per instance would stream too long);
         // long_count = 1: never; otherwise: levels with < long_count instances
+        // Default plans also run the levels below a long level (and a top
+        // level of few instances) with operands of at most g_res_max_n limbs
+        // instance-resident (level34.cuh) down to the fused bottom level, so
+        // that the whole recursion keeps row-major layouts.
         LongTables T;
-        for (size_t l = 0; l + 1 < plan.lv.size(); ++l) {
+        const size_t NL = plan.lv.size() - 1;   // Toom levels
+        const Level& Bt = plan.lv[NL - (NL ? 1 : 0)];
+        const bool fusable = NL >= 1 && !g_disable_fused && (Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) &&
+                             Bt.e == Bt.b + 1 && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
+                             2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e;
+        for (size_t l = 0; l < NL; ++l) {
             Level& L = plan.lv[l];
             const bool want = L.B == 16 || (top_long && l == 0) ||   // T16: no instance-parallel program
                               (p.long_count == 0 ? (L.n > g_long_min_n && L.count < (size_t)g_long_max_count)
-                                                 : (p.long_count > 1 && L.count < p.long_count));
-            if (want && long_tables(L.B, T)) L.lng = true;
+                                                 : (p.long_count > 1 && L.count < p.long_count)) ||
+                              // below a long level, operands too long to be resident stay long
+                              (p.long_count == 0 && g_res_on && l > 0 && plan.lv[l - 1].lng && L.n > g_res_max_n &&
+                               L.count < (size_t)g_long_max_count);
+            const bool resok = p.long_count == 0 && g_res_on && (L.B == 3 || L.B == 4) && L.n <= g_res_max_n &&
+                               L.n >= g_res_min_n &&
+                               l + 1 < NL && L.count < (size_t)g_long_max_count &&   // many instances: one thread each (C5: 125 vs 158 ms)
+                               res_interp_smem(L.B, 2 * L.e, L.Lw, res_threads(L.Lw + 1)) <= 200 * 1024;
+            if (resok && (l > 0 || want)) { L.lng = true; L.res = true; }
+            else if (want && long_tables(L.B, T)) L.lng = true;
+            else if (l > 0 && plan.lv[l - 1].lng && resok) { L.lng = true; L.res = true; }
             else break;
         }
+
         for (size_t l = 0; l + 1 < plan.lv.size(); ++l)
             if (plan.lv[l].B == 16 && !plan.lv[l].lng) return TOOM_EUNSUPPORTED;   // T16 runs long only
     }
@@ -557,7 +595,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
     size_t slot_limbs = 0, tiles = 0, nops = 0;
     for (size_t l = 0; l < nstaged; ++l) {
         const Level& L = plan.lv[l];
-        if (!L.lng) continue;
+        if (!L.lng || L.res) continue;
         LongTables T;
         long_tables(L.B, T);
         const int Wt = long_Wt(L);
@@ -1327,11 +1365,67 @@ static toom_status long_prepare(const std::vector<LOpDev>& ops, const std::vecto
     return TOOM_OK;
 }
 
+// single-pass decoupled look-back executor (longvec.cuh) instead of the
+// two-pass one (longvec2.cuh): TOOM_LONG_LOOKBACK=1, for comparison only
+static const bool g_long_lookback = [] {
+    const char* e = getenv("TOOM_LONG_LOOKBACK");
+    return e ? atoi(e) != 0 : false;
+}();
+
+// one two-pass op: summaries, scan, finish (longvec2.cuh)
+static void launch_scan2(LTile* tiles, int count, int tpi, int no, int nthreads, const uint32_t* o,
+                         const unsigned long long* orcp, const uint32_t* mch, const uint32_t* mi, cudaStream_t st) {
+    L2ScanArgs A;
+    memset(&A, 0, sizeof A);
+    A.tiles = tiles;
+    A.count = count;
+    A.tpi = tpi;
+    A.no = no;
+    A.nthreads = nthreads;
+    for (int i = 0; i < no; ++i) { A.o[i] = o[i]; A.orcp[i] = orcp[i]; A.mch[i] = mch[i]; A.mi[i] = mi[i]; }
+    const size_t warps = (size_t)count * no;
+    if (tpi >= 128) k_lscan2_blk<<<(unsigned)warps, 1024, 0, st>>>(A);   // one CTA per vector
+    else k_lscan2<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(A);
+    ++t_launches;
+}
+
 static toom_status launch_long_multi(const LMultiDev& d, const LMultiDev* dd, LStatus* status, unsigned* ctr,
                                      unsigned& epoch, int cat, cudaStream_t st) {
     const unsigned grid = (unsigned)((size_t)d.count * d.tiles_per_inst);
     if (grid == 0) return TOOM_OK;
     ProfScope ps(cat, st);
+    if (!g_long_lookback) {
+        const size_t sm = lmulti2_smem(d.nthreads, d.ch, d.ns);
+        LTile* tiles = reinterpret_cast<LTile*>(status);
+        const bool one = d.tiles_per_inst == 1;   // the tile is the whole vector: one pass
+#define TG_LM2(W, C)                                                                                      \
+        {                                                                                                 \
+            static bool attr = false;                                                                     \
+            if (!attr) {                                                                                  \
+                cudaFuncSetAttribute(k_lmulti2<W, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+                attr = true;                                                                              \
+            }                                                                                             \
+            if (one) {                                                                                    \
+                k_lmulti2<W, C><<<grid, d.nthreads, sm, st>>>(dd, tiles, 3);                              \
+            } else {                                                                                      \
+                k_lmulti2<W, C><<<grid, d.nthreads, sm, st>>>(dd, tiles, 1);                              \
+                launch_scan2(tiles, d.count, d.tiles_per_inst, d.no, d.nthreads, o, orcp, mch, mi, st);   \
+                k_lmulti2<W, C><<<grid, d.nthreads, sm, st>>>(dd, tiles, 2);                              \
+            }                                                                                             \
+        }
+        uint32_t o[LM_MAXO], mch[LM_MAXO], mi[LM_MAXO];
+        unsigned long long orcp[LM_MAXO];
+        for (int i = 0; i < d.no; ++i) { o[i] = d.out[i].o; orcp[i] = d.out[i].orcp; mch[i] = d.out[i].Mch; mi[i] = d.out[i].mi; }
+        if (d.ch == 16) {
+            if (d.wide) TG_LM2(true, 16) else TG_LM2(false, 16)
+        } else {
+            if (d.wide) TG_LM2(true, 4) else TG_LM2(false, 4)
+        }
+#undef TG_LM2
+        ps.done(st);
+        t_launches += one ? 0 : 2;
+        return TOOM_OK;
+    }
     const size_t sm = long_multi_smem(d.nthreads, d.ch, d.ns);
 #define TG_LM(W, C)                                                                                        \
     {                                                                                                      \
@@ -1370,6 +1464,35 @@ static toom_status launch_long_ops(const std::vector<LOpDev>& ops, size_t first,
         const LOpDev* d = ddesc + first + i;
         unsigned* cp = ctr + first + i;
         const size_t qs = ((size_t)o.nthreads * o.ch + LV_MAXHALO + 1 + (size_t)(o.ch + 1) * (o.nthreads + 1)) * 4;
+        if (!g_long_lookback) {
+            LTile* tiles = reinterpret_cast<LTile*>(status);
+            static bool attr2 = false;
+            if (!attr2) {
+                cudaFuncSetAttribute(k_lop2<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+                cudaFuncSetAttribute(k_lop2<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+                cudaFuncSetAttribute(k_lop2<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+                cudaFuncSetAttribute(k_lop2<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+                attr2 = true;
+            }
+            const size_t qs2 = lop2_smem(o.nthreads, o.ch);
+            const bool one = o.tiles_per_inst == 1;   // the tile is the whole vector: one pass
+            for (int ph = one ? 3 : 1; ph <= (one ? 3 : 2); ++ph) {
+                if (ph == 2) {
+                    const unsigned long long orcp = o.orcp;
+                    launch_scan2(tiles, o.count, o.tiles_per_inst, 1, o.nthreads, &o.o, &orcp, &o.Mch, &o.mi, st);
+                }
+                if (o.ch == 16) {
+                    if (o.wide) k_lop2<true, 16><<<grid, o.nthreads, qs2, st>>>(d, tiles, ph);
+                    else k_lop2<false, 16><<<grid, o.nthreads, qs2, st>>>(d, tiles, ph);
+                } else {
+                    if (o.wide) k_lop2<true, 4><<<grid, o.nthreads, qs2, st>>>(d, tiles, ph);
+                    else k_lop2<false, 4><<<grid, o.nthreads, qs2, st>>>(d, tiles, ph);
+                }
+            }
+            ps.done(st);
+            t_launches += one ? 0 : 2;
+            continue;
+        }
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_long_op<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
@@ -1402,6 +1525,59 @@ static toom_status launch_long_ops(const std::vector<LOpDev>& ops, size_t first,
     return TOOM_OK;
 }
 
+// one instance-resident level (level34.cuh): evaluation (down) or
+// interpolation + recomposition (up), one CTA per instance, row-major layouts
+static toom_status launch_res(const Plan& plan, size_t l, bool down, uint32_t* w, const uint32_t* u, const uint32_t* v,
+                              uint8_t* ws, cudaStream_t st) {
+    const Level& L = plan.lv[l];
+    if (L.count == 0) return TOOM_OK;
+    if (L.count > 0x7FFFFFFFull) return TOOM_EUNSUPPORTED;
+    ProfScope ps(down ? CAT_EVAL : CAT_INTERP, st);
+    const int cnt = (int)L.count;
+    // children and child products: row-major families (child_vec: the
+    // level's own buffers, or the staging transposed to the instance-parallel
+    // level below)
+    const LVec cu = child_vec(plan, l, ws, L.offU, L.e, 0), cv = child_vec(plan, l, ws, L.offV, L.e, 0);
+    const LVec cy = child_vec(plan, l, ws, L.offP, 2 * L.e, 0);
+    if (cu.ls != 1 || cv.ls != 1 || cy.ls != 1) return TOOM_EUNSUPPORTED;
+    if (down) {
+        const uint32_t* su = l == 0 ? u : (const uint32_t*)(ws + plan.lv[l - 1].offU);
+        const uint32_t* sv = l == 0 ? v : (const uint32_t*)(ws + plan.lv[l - 1].offV);
+        const int sgn = (l > 0 || plan.signed_in) ? 1 : 0;
+        const int nt = res_threads(L.e);
+        const size_t sm = res_eval_smem(L.n);
+        dim3 grid((unsigned)cnt, 2);
+        uint32_t* du = (uint32_t*)cu.base;
+        uint32_t* dv = (uint32_t*)cv.base;
+        if (L.B == 3) {
+            static bool a = false;
+            if (!a) { cudaFuncSetAttribute(k_res_eval<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); a = true; }
+            k_res_eval<3><<<grid, nt, sm, st>>>(su, sv, du, dv, cnt, L.n, L.b, L.e, sgn);
+        } else {
+            static bool a = false;
+            if (!a) { cudaFuncSetAttribute(k_res_eval<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); a = true; }
+            k_res_eval<4><<<grid, nt, sm, st>>>(su, sv, du, dv, cnt, L.n, L.b, L.e, sgn);
+        }
+    } else {
+        uint32_t* dst = l == 0 ? w : (uint32_t*)(ws + plan.lv[l - 1].offP);
+        const int nt = res_threads(L.Lw + 1);   // one round per coefficient row when it fits
+        const size_t sm = res_interp_smem(L.B, 2 * L.e, L.Lw, nt);
+        const uint32_t* Y = cy.base;
+        if (L.B == 3) {
+            static bool a = false;
+            if (!a) { cudaFuncSetAttribute(k_res_interp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); a = true; }
+            k_res_interp<3><<<cnt, nt, sm, st>>>(Y, dst, 2ll * L.n, cnt, L.n, L.b, 2 * L.e, L.Lw);
+        } else {
+            static bool a = false;
+            if (!a) { cudaFuncSetAttribute(k_res_interp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); a = true; }
+            k_res_interp<4><<<cnt, nt, sm, st>>>(Y, dst, 2ll * L.n, cnt, L.n, L.b, 2 * L.e, L.Lw);
+        }
+    }
+    ps.done(st);
+    ++t_launches;
+    return TOOM_OK;
+}
+
 static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, const uint32_t* v, int n, size_t batch,
                             uint8_t* ws, cudaStream_t st) {
     const size_t L = plan.lv.size() - 1;   // number of Toom levels
@@ -1423,7 +1599,9 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         const size_t nops = ops.size();
         for (const auto& stp : steps) {
             toom_status r;
-            if (stp.first == 0) {
+            if (stp.first == 2) {
+                r = launch_res(plan, (size_t)stp.second, cat == CAT_EVAL, w, u, v, ws, st);
+            } else if (stp.first == 0) {
                 std::vector<LOpDev> one(1, ops[stp.second]);
                 r = launch_long_ops(one, (size_t)stp.second, ddesc, status, ctr, epoch, cat, st);
             } else {
@@ -1437,6 +1615,11 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
     if (Tl) {
         std::vector<std::vector<std::pair<int, int>>> ups(Tl);
         for (size_t l = 0; l < Tl; ++l) {
+            if (plan.lv[l].res) {   // instance-resident level: kind 2 steps
+                sdown.push_back({2, (int)l});
+                ups[l].push_back({2, (int)l});
+                continue;
+            }
             LongCall one;
             build_long_level(plan, l, w, u, v, ws, one);
             const int od = (int)ops.size();
@@ -2066,8 +2249,9 @@ size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t* plan, char*
         const Level& L = pl.lv[l];
         char tmp[512];
         snprintf(tmp, sizeof tmp,
-                 "%s{\"B\": %d, \"count\": %zu, \"n\": %d, \"b\": %d, \"lentop\": %d, \"e\": %d, \"Lw\": %d, \"npts\": %d, \"long\": %s}",
-                 l ? ", " : "", L.B, L.count, L.n, L.b, L.lentop, L.e, L.Lw, L.npts, L.lng ? "true" : "false");
+                 "%s{\"B\": %d, \"count\": %zu, \"n\": %d, \"b\": %d, \"lentop\": %d, \"e\": %d, \"Lw\": %d, \"npts\": %d, \"long\": %s, \"res\": %s}",
+                 l ? ", " : "", L.B, L.count, L.n, L.b, L.lentop, L.e, L.Lw, L.npts, L.lng ? "true" : "false",
+                 L.res ? "true" : "false");
         js += tmp;
     }
     char tail[128];

@@ -738,6 +738,16 @@ def emit_row_tables(ps: PointSet) -> str:
     L.append(f"TG_CONST unsigned tg_rowO_{ps.name}[{NP}] = {{" + ", ".join(f"{x}u" for x in O) + "};")
     L.append(f"TG_CONST unsigned tg_rowInv_{ps.name}[{NP}] = {{" + ", ".join(f"0x{x:08X}u" for x in INV) + "};")
     L.append(f"TG_CONST int tg_rowS_{ps.name}[{NP}] = {{" + ", ".join(str(x) for x in S) + "};")
+    # scan constants of the instance-resident level kernels (csrc/level34.cuh,
+    # RES_CH = 9 positions per thread): 2^32 mod o, Mch = 2^(32*9) mod o and
+    # its inverse (all o here are odd, > 1 or the no-division marker 1)
+    RES_CH = 9
+    P32 = [(1 << 32) % o if o > 1 else 0 for o in O]
+    MCH = [pow(2, 32 * RES_CH, o) if o > 1 else 0 for o in O]
+    MI = [pow(m, -1, o) if o > 1 else 0 for m, o in zip(MCH, O)]
+    L.append(f"TG_CONST unsigned tg_rowP32_{ps.name}[{NP}] = {{" + ", ".join(f"{x}u" for x in P32) + "};")
+    L.append(f"TG_CONST unsigned tg_rowMch9_{ps.name}[{NP}] = {{" + ", ".join(f"{x}u" for x in MCH) + "};")
+    L.append(f"TG_CONST unsigned tg_rowMi9_{ps.name}[{NP}] = {{" + ", ".join(f"{x}u" for x in MI) + "};")
     # combined form over a common denominator Dc = lcm_j D_j (PAPER.md:162
     # matrix form + Eq. 1.3): Dc w = sum_j 2^(32 b j) sum_k (Dc/D_j) A[j][k] y_k
     Ds = [O[j] << S[j] for j in range(NP)]
