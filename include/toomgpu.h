@@ -195,6 +195,14 @@ void toom_set_fused(int on);
  * row-parallel form unless the mode is 0.  All are exact; tests compare them. */
 void toom_set_top_stream(int on);
 
+/* Toom-16 top-level interpolation: 1 (default) = the matrix form (even-odd
+ * split, then one dense pass per half with the symbolic inverse's wide
+ * multipliers and exact divisions by the rows' word-factored denominators,
+ * PAPER.md:162); 0 = the staged Newton program (the
+ * paper's listings, one long op per step).  Both
+ * are exact; tests compare them.  Affects later calls only.                */
+void toom_set_t16_matrix(int on);
+
 /* ---- stage exports (tests, bench) ------------------------------------- */
 
 /* Base case alone (step a3): batched schoolbook of signed two's-complement

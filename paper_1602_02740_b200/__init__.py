@@ -70,6 +70,7 @@ SIGNATURES = {
     "toom_mul_signed_batched": (_I, [_P, _P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
     "toom_product_width_point": (_SZ, [_SZ, _I]),
     "toom_set_check": (None, [_I]),
+    "toom_set_t16_matrix": (None, [_I]),
     "toom_set_verify": (None, [_I]),
     "toom_debug_fault": (None, [_I]),
 }
@@ -320,3 +321,9 @@ def last_error() -> int:
     call, or a device-detected failure (TOOM_EINEXACT / TOOM_EVERIFY) when
     set_check / set_verify are on (synchronizes the device).  Clears it."""
     return lib().toom_last_error()
+
+
+def set_t16_matrix(on: bool = True):
+    """Toom-16 top-level interpolation: matrix form (default) or the staged
+    Newton program."""
+    lib().toom_set_t16_matrix(1 if on else 0)

@@ -597,3 +597,100 @@ __global__ void __launch_bounds__(256) k_lscan2(L2ScanArgs A) {
 }
 
 }  // namespace tg
+
+namespace tg {
+// ------------------------------------------------------------------------
+// Multi-output op with WIDE multipliers (the matrix-form Toom-16
+// interpolation): out_o = ((sum_s m_os src_s) / o_o) >> shr_o
+// with m_os = sum_d a_osd 2^(32 d) given as balanced 32-bit digits, so a
+// position p of the linear combination is sum_s sum_d a_osd src_s[p - d]
+// (int64 products, int128 accumulation).  Sources are staged once per tile
+// with LB_PRE limbs before the tile; the scans are those of k_lmulti2.
+// ------------------------------------------------------------------------
+constexpr int LB_MAXS = 17, LB_MAXO = 15, LB_ND = 4, LB_PRE = LB_ND - 1, LB_CH = 8;
+
+struct __align__(16) LBigDev {
+    int ns, no, W, tiles_per_inst, nthreads, ch, count, pad;
+    long long dst_is, dst_ls;
+    LMSrc src[LB_MAXS];
+    LMOut out[LB_MAXO];
+    int nd[LB_MAXO][LB_MAXS];          // digits in use (0: the source is not a term)
+    int a[LB_MAXO][LB_MAXS][LB_ND];
+};
+
+__host__ __device__ inline int lbig2_np1(int nthreads) { return nthreads + (LB_PRE + LM_HALO + LB_CH - 1) / LB_CH + 1; }
+inline size_t lbig2_smem(int nthreads, int ns) {
+    return 4 * ((size_t)lv2_qwords(nthreads * LB_CH, LB_CH) + (size_t)ns * LB_CH * lbig2_np1(nthreads));
+}
+
+__global__ void __launch_bounds__(128, 3) k_lbig2(const LBigDev* __restrict__ dp, LTile* __restrict__ tiles, int phase) {
+    constexpr int CH = LB_CH;
+    using Acc = __int128;
+    __shared__ __align__(16) LBigDev s_d;
+    {
+        const int4* srcd = reinterpret_cast<const int4*>(dp);
+        int4* dstd = reinterpret_cast<int4*>(&s_d);
+        constexpr int NQ = (int)(sizeof(LBigDev) / 16);
+        for (int i = threadIdx.x; i < NQ; i += blockDim.x) dstd[i] = __ldg(srcd + i);
+    }
+    __shared__ L2Smem s_sh;
+    extern __shared__ uint32_t dsm[];
+    __syncthreads();
+    const int tid = threadIdx.x, NT = blockDim.x, TL = NT * CH, NP1 = lbig2_np1(NT);
+    uint32_t* Q = dsm;
+    uint32_t* Sb = dsm + lv2_qwords(TL, CH);   // [ns][CH][NP1]: relative position i = pos - tstart + LB_PRE
+    const LBigDev& d = s_d;
+    const unsigned tile = blockIdx.x;
+    const long long inst = tile / d.tiles_per_inst;
+    const int kt = (int)(tile - inst * d.tiles_per_inst);
+    const int tstart = kt * TL;
+    const int NI = TL + LB_PRE + LM_HALO;
+    for (int sI = 0; sI < d.ns; ++sI) {
+        const LMSrc& S = d.src[sI];
+        const uint32_t* sp = S.base + inst * S.is;
+        uint32_t fill = 0;
+        if (S.sign && S.len > 0) fill = (__ldg(sp + (S.len - 1)) >> 31) ? 0xFFFFFFFFu : 0u;
+        uint32_t* sj = Sb + (size_t)sI * CH * NP1;
+        for (int i = tid; i < NI; i += NT) {
+            const int t = tstart - LB_PRE + i;
+            sj[(i % CH) * NP1 + i / CH] = t < 0 ? 0u : (t < S.len ? __ldg(sp + t) : fill);
+        }
+    }
+    __syncthreads();
+    auto staged = [&](int sI, int i) -> uint32_t { return Sb[(size_t)sI * CH * NP1 + (i % CH) * NP1 + i / CH]; };
+    for (int o = 0; o < d.no; ++o) {
+        const LMOut& O = d.out[o];
+        Acc lin[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) lin[q] = 0;
+        for (int sI = 0; sI < d.ns; ++sI) {
+            const int nd = d.nd[o][sI];
+            for (int dd = 0; dd < nd; ++dd) {
+                const long long a = d.a[o][sI][dd];
+                if (a == 0) continue;
+                // position p0 + q - dd  ->  relative index tid*CH + q - dd + LB_PRE
+                const int i0 = tid * CH - dd + LB_PRE;
+#pragma unroll
+                for (int q = 0; q < CH; ++q) lin[q] += (Acc)(a * (long long)staged(sI, i0 + q));
+            }
+        }
+        const LMod M{O.o, O.orcp};
+        lv2_tile<Acc, CH>(lin, M,
+                          LFinish{O.oinv, O.p32, O.Mch, O.mi, O.sa, O.sr, d.W,
+                                  reinterpret_cast<LStatus*>(tiles + o), d.no, O.dst + inst * d.dst_is, d.dst_ls},
+                          tile, tstart, s_sh, Q,
+                          [&](Acc (&hl)[LV_MAXHALO]) {
+#pragma unroll
+                              for (int h = 0; h < LV_MAXHALO; ++h) {
+                                  Acc v = 0;
+                                  for (int s2 = 0; s2 < d.ns; ++s2)
+                                      for (int dd = 0; dd < d.nd[o][s2]; ++dd)
+                                          v += (Acc)((long long)d.a[o][s2][dd] * (long long)staged(s2, TL + h - dd + LB_PRE));
+                                  hl[h] = v;
+                              }
+                          },
+                          phase);
+        __syncthreads();
+    }
+}
+}  // namespace tg

@@ -405,6 +405,7 @@ struct Plan {
     int bnd = -1;
     size_t offT = 0;
     size_t offEDesc = 0;     // multi-output evaluation descriptors
+    size_t offBDesc = 0;     // wide-multiplier multi-output descriptors (matrix-form T16)
     bool top_warp = false;   // top interpolation one warp per product (fused level writes row-major)
 };
 
@@ -495,6 +496,15 @@ static bool g_res_on = [] {
     const char* e = getenv("TOOM_RES");
     return e ? atoi(e) != 0 : true;
 }();
+
+// the matrix-form Toom-16 interpolation (f1) instead of the 459-op staged
+// Newton program: TOOM_T16_MATRIX=0 restores the latter (tests compare both)
+static bool g_t16_matrix = [] {
+    const char* e = getenv("TOOM_T16_MATRIX");
+    return e ? atoi(e) != 0 : true;
+}();
+constexpr int F1_SLOTS = 61;   // E, O, R, T (15 each) + y'
+static int long_nslots(int B, int nslots) { return (B == 16 && g_t16_matrix) ? std::max(nslots, F1_SLOTS) : nslots; }
 
 // one warp per product (k_interp_top_warp) needs the products row-major; CH
 // positions per lane, CH = ceil((2n+1)/32) rounded up to an instantiated size
@@ -599,7 +609,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         LongTables T;
         long_tables(L.B, T);
         const int Wt = long_Wt(L);
-        slot_limbs = std::max(slot_limbs, (size_t)T.nslots * L.count * Wt);
+        slot_limbs = std::max(slot_limbs, (size_t)long_nslots(L.B, T.nslots) * L.count * Wt);
         tiles = std::max(tiles, long_tiles(L.count, std::max(std::max(Wt, L.e), 2 * L.n)));
         tiles = std::max(tiles, long_tiles(L.count, std::max(L.e, L.Lw)) * (size_t)L.npts);   // multi-output ops
         nops += 2 * (size_t)T.neo + T.nio + 1 + 2;
@@ -624,6 +634,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         plan.nDesc = nops;
         plan.offDesc = take((nops * sizeof(LOpDev) + 3) / 4);
         plan.offEDesc = take((nops * sizeof(LMultiDev) + 3) / 4);
+        plan.offBDesc = take((nops * sizeof(LBigDev) + 3) / 4);
     }
     plan.bytes = off;
     return TOOM_OK;
@@ -1086,9 +1097,11 @@ static void launch_transpose(const uint32_t* in, uint32_t* out, size_t R, size_t
 struct LongCall {
     std::vector<LOpDev> down, up;        // single-output ops (per level, in launch order)
     std::vector<LMultiDev> mdown, mup;   // multi-output ops
-    // launch order of a level: (kind 0 = op, 1 = multi, index into the level's vectors)
+    std::vector<LBigDev> bup;            // wide-multiplier multi-output ops (matrix-form T16)
+    // launch order of a level: (kind 0 = op, 1 = multi, 3 = big, index into the level's vectors)
     std::vector<std::pair<int, int>> sdown, sup;
 };
+
 
 // layout of level l's child operand / product families
 static LVec child_vec(const Plan& plan, size_t l, const uint8_t* ws, size_t off, int width, int k) {
@@ -1280,6 +1293,169 @@ static bool long_multi_rows(const Level& L, YF yv, uint32_t* slots, LMultiDev& d
     return true;
 }
 
+// ---- matrix-form Toom-16 interpolation: the
+// even-odd split (Eqs. 4.5-4.6), one dense pass per half with wide
+// multipliers (the symbolic inverse, gen/toomgen.py t16_matrix_form), the
+// exact divisions by the remaining coprime word factors of each row's
+// denominator, and the recomposition (Eq. 1.3).
+static void big_out(LBigDev& d) {
+    d.ch = LB_CH;
+    d.nthreads = 128;
+    d.tiles_per_inst = (d.W + d.nthreads * LB_CH - 1) / (d.nthreads * LB_CH);
+}
+
+template <class YF>
+static void long_t16_matrix(const Level& L, YF yv, uint32_t* slots, uint32_t* dst, LongCall& lc) {
+    const int cnt = (int)L.count, Wt = long_Wt(L), W2 = 2 * L.e, Lw = L.Lw;
+    auto slot = [&](int g, int i) { return slots + (size_t)(g * 15 + i) * cnt * Wt; };   // groups E=0 O=1 R=2 T=3, y' = 60
+    uint32_t* Y = slots + (size_t)60 * cnt * Wt;
+    constexpr int NPR = tg_f1_npairs;
+    auto msrc = [&](const uint32_t* base, int len) { return LMSrc{base, (long long)Wt, len, 1}; };
+    auto ysrc = [&](int k) {
+        const LVec y = yv(k);
+        return LMSrc{y.base, y.is, 2 * L.e, 1};
+    };
+    // 1. E_i = y+ + y-, O_i = y+ - y- (two multi ops of 7 pairs)
+    for (int h = 0; h < 2; ++h) {
+        LMultiDev d;
+        memset(&d, 0, sizeof d);
+        const int p0 = h * 7, np = std::min(7, NPR - p0);
+        d.ns = 2 * np;
+        d.no = 2 * np;
+        d.W = W2 + 1;
+        d.count = cnt;
+        for (int i = 0; i < np; ++i) {
+            d.src[2 * i] = ysrc(tg_f1_pair[p0 + i][0]);
+            d.src[2 * i + 1] = ysrc(tg_f1_pair[p0 + i][1]);
+            d.m[2 * i][2 * i] = 1;
+            d.m[2 * i][2 * i + 1] = 1;
+            d.m[2 * i + 1][2 * i] = 1;
+            d.m[2 * i + 1][2 * i + 1] = -1;
+        }
+        multi_shape(d);
+        for (int i = 0; i < np; ++i) {
+            multi_out(d.out[2 * i], slot(0, p0 + i), 1, 0, d.ch);
+            multi_out(d.out[2 * i + 1], slot(1, p0 + i), 1, 0, d.ch);
+        }
+        d.dst_is = Wt;
+        d.dst_ls = 1;
+        lc.sup.push_back({1, (int)lc.mup.size()});
+        lc.mup.push_back(d);
+    }
+    // exact division of rows `nr` in group gs by their word factor f, into group gd
+    auto div_pass = [&](int nr, int gs, int gd, const unsigned (*o)[3], int f) {
+        LMultiDev d;
+        memset(&d, 0, sizeof d);
+        d.ns = d.no = nr;
+        d.W = Lw;
+        d.count = cnt;
+        for (int r = 0; r < nr; ++r) {
+            d.src[r] = msrc(slot(gs, r), Lw);
+            d.m[r][r] = 1;
+        }
+        multi_shape(d);
+        for (int r = 0; r < nr; ++r) multi_out(d.out[r], slot(gd, r), o[r][f], 0, d.ch);
+        d.dst_is = Wt;
+        d.dst_ls = 1;
+        lc.sup.push_back({1, (int)lc.mup.size()});
+        lc.mup.push_back(d);
+    };
+    auto big_rows = [&](int nr, int ns, const LMSrc* src, const int (*a)[17][4], int astride, const unsigned (*o)[3],
+                        const int* sh, int gd) {
+        (void)astride;
+        LBigDev d;
+        memset(&d, 0, sizeof d);
+        d.ns = ns;
+        d.no = nr;
+        d.W = Lw;
+        d.count = cnt;
+        for (int sI = 0; sI < ns; ++sI) d.src[sI] = src[sI];
+        for (int r = 0; r < nr; ++r)
+            for (int sI = 0; sI < ns; ++sI) {
+                int nd = 0;
+                for (int k = 0; k < LB_ND; ++k) {
+                    d.a[r][sI][k] = a[r][sI][k];
+                    if (a[r][sI][k]) nd = k + 1;
+                }
+                d.nd[r][sI] = nd;
+            }
+        big_out(d);
+        for (int r = 0; r < nr; ++r) multi_out(d.out[r], slot(gd, r), o[r][0], sh[r], LB_CH);
+        d.dst_is = Wt;
+        d.dst_ls = 1;
+        lc.sup.push_back({3, (int)lc.bup.size()});
+        lc.bup.push_back(d);
+    };
+    // 2. even rows (sources E_0..13, y_0, y_inf), then the remaining word factors
+    {
+        static int ae[tg_f1_even_n][17][4];
+        for (int r = 0; r < tg_f1_even_n; ++r)
+            for (int sI = 0; sI < 17; ++sI)
+                for (int k = 0; k < 4; ++k) ae[r][sI][k] = sI < NPR + 2 ? tg_f1_even_a[r][sI][k] : 0;
+        LMSrc src[LB_MAXS];
+        for (int i = 0; i < NPR; ++i) src[i] = msrc(slot(0, i), W2 + 1);
+        src[NPR] = ysrc(tg_f1_i0);
+        src[NPR + 1] = ysrc(tg_f1_iinf);
+        big_rows(tg_f1_even_n, NPR + 2, src, ae, 17, tg_f1_even_o, tg_f1_even_s, 2);
+        div_pass(tg_f1_even_n, 2, 3, tg_f1_even_o, 1);
+        div_pass(tg_f1_even_n, 3, 2, tg_f1_even_o, 2);   // even w_2..w_28 in group R
+    }
+    // 3. y' = y(2:5) - sum_{j even} w_j 2^j 5^(30-j)
+    {
+        LBigDev d;
+        memset(&d, 0, sizeof d);
+        d.ns = 2 + tg_f1_even_n + 1;
+        d.no = 1;
+        d.W = W2 + 1;
+        d.count = cnt;
+        d.src[0] = ysrc(tg_f1_iu);
+        d.a[0][0][0] = 1;
+        d.nd[0][0] = 1;
+        for (int jj = 0; jj <= tg_f1_even_n + 1; ++jj) {   // w_0, w_2 .. w_28, w_30
+            LMSrc sI = jj == 0 ? ysrc(tg_f1_i0) : (jj == tg_f1_even_n + 1 ? ysrc(tg_f1_iinf) : msrc(slot(2, jj - 1), Lw));
+            d.src[1 + jj] = sI;
+            int nd = 0;
+            for (int k = 0; k < LB_ND; ++k) {
+                d.a[0][1 + jj][k] = -tg_f1_ymul[jj][k];
+                if (tg_f1_ymul[jj][k]) nd = k + 1;
+            }
+            d.nd[0][1 + jj] = nd;
+        }
+        big_out(d);
+        multi_out(d.out[0], Y, 1, 0, LB_CH);
+        d.dst_is = Wt;
+        d.dst_ls = 1;
+        lc.sup.push_back({3, (int)lc.bup.size()});
+        lc.bup.push_back(d);
+    }
+    // 4. odd rows (sources O_0..13, y'), then the remaining word factors
+    {
+        static int ao[tg_f1_odd_n][17][4];
+        for (int r = 0; r < tg_f1_odd_n; ++r)
+            for (int sI = 0; sI < 17; ++sI)
+                for (int k = 0; k < 4; ++k) ao[r][sI][k] = sI < NPR + 1 ? tg_f1_odd_a[r][sI][k] : 0;
+        LMSrc src[LB_MAXS];
+        for (int i = 0; i < NPR; ++i) src[i] = msrc(slot(1, i), W2 + 1);
+        src[NPR] = msrc(Y, W2 + 1);
+        big_rows(tg_f1_odd_n, NPR + 1, src, ao, 17, tg_f1_odd_o, tg_f1_odd_s, 3);
+        div_pass(tg_f1_odd_n, 3, 0, tg_f1_odd_o, 1);
+        div_pass(tg_f1_odd_n, 0, 3, tg_f1_odd_o, 2);     // odd w_1..w_29 in group T
+    }
+    // 5. w = sum_j w_j 2^(32 b j)
+    LOpBuilder b(dst, 2 * L.n, 1, 2 * L.n, cnt);
+    for (int j = 0; j <= 30; ++j) {
+        if (j == 0) b.add(yv(tg_f1_i0), 1, 0);
+        else if (j == 30) b.add(yv(tg_f1_iinf), 1, 32ll * L.b * j);
+        else {
+            const int g = (j & 1) ? 3 : 2, r = (j & 1) ? (j - 1) / 2 : (j - 2) / 2;
+            b.add(LVec{slot(g, r), Wt, 1, Wt, 0}, 1, 32ll * L.b * j, 0, Lw, 1);
+        }
+    }
+    b.op.wide = 0;
+    lc.sup.push_back({0, (int)lc.up.size()});
+    lc.up.push_back(b.op);
+}
+
 static void build_long_level(const Plan& plan, size_t l, uint32_t* w, const uint32_t* u, const uint32_t* v, uint8_t* ws,
                              LongCall& lc) {
     const Level& L = plan.lv[l];
@@ -1317,6 +1493,10 @@ static void build_long_level(const Plan& plan, size_t l, uint32_t* w, const uint
         lc.up.push_back(b.op);
         return;
     }
+    if (L.B == 16 && g_t16_matrix) {
+        long_t16_matrix(L, yv, slots, dst, lc);
+        return;
+    }
     const size_t a = lc.up.size();
     long_interp_ops(L, yv, slots, dst, lc.up);
     for (size_t i = a; i < lc.up.size(); ++i) lc.sup.push_back({0, (int)i});
@@ -1331,9 +1511,9 @@ static cudaEvent_t g_desc_ev = nullptr;
 // reset the scan status / tile counters, all stream-ordered
 static toom_status long_prepare(const std::vector<LOpDev>& ops, const std::vector<LMultiDev>& mops, LOpDev* ddesc,
                                 LMultiDev* mdesc, LStatus* status, size_t nStatus, unsigned* ctr, size_t nCtr,
-                                cudaStream_t st) {
-    const size_t nd = ops.size(), ne = mops.size();
-    const size_t bytes = nd * sizeof(LOpDev) + ne * sizeof(LMultiDev);
+                                cudaStream_t st, const std::vector<LBigDev>* bops = nullptr, LBigDev* bdesc = nullptr) {
+    const size_t nd = ops.size(), ne = mops.size(), nb = bops ? bops->size() : 0;
+    const size_t bytes = nd * sizeof(LOpDev) + ne * sizeof(LMultiDev) + nb * sizeof(LBigDev);
     std::lock_guard<std::mutex> g(g_desc_mu);
     if (g_desc_ev) cudaEventSynchronize(g_desc_ev);   // previous upload finished reading the staging
     if (bytes > g_desc_cap * sizeof(LOpDev)) {
@@ -1356,6 +1536,12 @@ static toom_status long_prepare(const std::vector<LOpDev>& ops, const std::vecto
         uint8_t* hb = (uint8_t*)(g_desc_host + nd);
         memcpy(hb, mops.data(), ne * sizeof(LMultiDev));
         if (cudaMemcpyAsync(mdesc, hb, ne * sizeof(LMultiDev), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return TOOM_ECUDA;
+    }
+    if (nb) {
+        uint8_t* hb = (uint8_t*)(g_desc_host + nd) + ne * sizeof(LMultiDev);
+        memcpy(hb, bops->data(), nb * sizeof(LBigDev));
+        if (cudaMemcpyAsync(bdesc, hb, nb * sizeof(LBigDev), cudaMemcpyHostToDevice, st) != cudaSuccess)
             return TOOM_ECUDA;
     }
     if (!g_desc_ev) cudaEventCreateWithFlags(&g_desc_ev, cudaEventDisableTiming);
@@ -1444,6 +1630,35 @@ static toom_status launch_long_multi(const LMultiDev& d, const LMultiDev* dd, LS
 #undef TG_LM
     ps.done(st);
     ++epoch;
+    ++t_launches;
+    return TOOM_OK;
+}
+
+// wide-multiplier multi-output op (matrix-form T16): two passes + scan, or
+// one pass when a tile holds the whole vector
+static toom_status launch_long_big(const LBigDev& d, const LBigDev* dd, LStatus* status, int cat, cudaStream_t st) {
+    const unsigned grid = (unsigned)((size_t)d.count * d.tiles_per_inst);
+    if (grid == 0) return TOOM_OK;
+    ProfScope ps(cat, st);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_lbig2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    const size_t sm = lbig2_smem(d.nthreads, d.ns);
+    LTile* tiles = reinterpret_cast<LTile*>(status);
+    if (d.tiles_per_inst == 1) {
+        k_lbig2<<<grid, d.nthreads, sm, st>>>(dd, tiles, 3);
+    } else {
+        uint32_t o[LM_MAXO], mch[LM_MAXO], mi[LM_MAXO];
+        unsigned long long orcp[LM_MAXO];
+        for (int i = 0; i < d.no; ++i) { o[i] = d.out[i].o; orcp[i] = d.out[i].orcp; mch[i] = d.out[i].Mch; mi[i] = d.out[i].mi; }
+        k_lbig2<<<grid, d.nthreads, sm, st>>>(dd, tiles, 1);
+        launch_scan2(tiles, d.count, d.tiles_per_inst, d.no, d.nthreads, o, orcp, mch, mi, st);
+        k_lbig2<<<grid, d.nthreads, sm, st>>>(dd, tiles, 2);
+        t_launches += 2;
+    }
+    ps.done(st);
     ++t_launches;
     return TOOM_OK;
 }
@@ -1589,9 +1804,11 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
     // launch steps (kind, global index): down in level order, up deepest first
     std::vector<LOpDev> ops;
     std::vector<LMultiDev> mops;
+    std::vector<LBigDev> bops;
     std::vector<std::pair<int, int>> sdown, sup;
     LOpDev* ddesc = (LOpDev*)(ws + plan.offDesc);
     LMultiDev* mdesc = (LMultiDev*)(ws + plan.offEDesc);
+    LBigDev* bdesc = (LBigDev*)(ws + plan.offBDesc);
     LStatus* status = (LStatus*)(ws + plan.offStatus);
     unsigned* ctr = (unsigned*)(ws + plan.offCtr);
     unsigned epoch = 1;
@@ -1601,6 +1818,8 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             toom_status r;
             if (stp.first == 2) {
                 r = launch_res(plan, (size_t)stp.second, cat == CAT_EVAL, w, u, v, ws, st);
+            } else if (stp.first == 3) {
+                r = launch_long_big(bops[stp.second], bdesc + stp.second, status, cat, st);
             } else if (stp.first == 0) {
                 std::vector<LOpDev> one(1, ops[stp.second]);
                 r = launch_long_ops(one, (size_t)stp.second, ddesc, status, ctr, epoch, cat, st);
@@ -1630,13 +1849,16 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             mops.insert(mops.end(), one.mdown.begin(), one.mdown.end());
             const int mu = (int)mops.size();
             mops.insert(mops.end(), one.mup.begin(), one.mup.end());
+            const int bu = (int)bops.size();
+            bops.insert(bops.end(), one.bup.begin(), one.bup.end());
             for (auto x : one.sdown) sdown.push_back({x.first, x.second + (x.first ? md : od)});
-            for (auto x : one.sup) ups[l].push_back({x.first, x.second + (x.first ? mu : ou)});
+            for (auto x : one.sup) ups[l].push_back({x.first, x.second + (x.first == 3 ? bu : (x.first ? mu : ou))});
         }
         for (size_t l = Tl; l-- > 0;) sup.insert(sup.end(), ups[l].begin(), ups[l].end());
-        if (ops.size() > plan.nDesc || mops.size() > plan.nDesc || ops.size() + mops.size() > plan.nCtr)
+        if (ops.size() > plan.nDesc || mops.size() > plan.nDesc || bops.size() > plan.nDesc ||
+            ops.size() + mops.size() > plan.nCtr)
             return TOOM_EINVAL;
-        if ((s = long_prepare(ops, mops, ddesc, mdesc, status, plan.nStatus, ctr, plan.nCtr, st))) return s;
+        if ((s = long_prepare(ops, mops, ddesc, mdesc, status, plan.nStatus, ctr, plan.nCtr, st, &bops, bdesc))) return s;
         if ((s = run_steps(sdown, CAT_EVAL))) return s;
         if (plan.bnd >= 0) {   // row-major children -> interleaved [e][npts*count]
             const Level& Lb = plan.lv[plan.bnd];
@@ -1917,6 +2139,43 @@ static toom_status run_long_standalone(size_t slot_limbs, size_t tiles, size_t n
     return launch_long_ops(ops, 0, ddesc, status, ctr, epoch, CAT_OTHER, st);
 }
 
+// as run_long_standalone for a whole LongCall (single, multi-output and
+// wide-multiplier ops in the call's `sup` order): the stage export of the
+// matrix-form Toom-16 interpolation
+template <class BuildF>
+static toom_status run_long_call_standalone(size_t slot_limbs, size_t tiles, size_t nops, BuildF build, cudaStream_t st) {
+    auto rnd = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t bS = rnd(slot_limbs * 4), bT = rnd(tiles * sizeof(LStatus)), bC = rnd(nops * 4),
+                 bD = rnd(nops * sizeof(LOpDev)), bM = rnd(nops * sizeof(LMultiDev)), bB = rnd(nops * sizeof(LBigDev));
+    void* ws = nullptr;
+    toom_status s;
+    WsGuard wg;
+    if ((s = get_ws(bS + bT + bC + bD + bM + bB, &ws, st))) return s;
+    wg.on = true;
+    uint8_t* base = (uint8_t*)ws;
+    LStatus* status = (LStatus*)(base + bS);
+    unsigned* ctr = (unsigned*)(base + bS + bT);
+    LOpDev* ddesc = (LOpDev*)(base + bS + bT + bC);
+    LMultiDev* mdesc = (LMultiDev*)(base + bS + bT + bC + bD);
+    LBigDev* bdesc = (LBigDev*)(base + bS + bT + bC + bD + bM);
+    LongCall lc;
+    build((uint32_t*)base, lc);
+    if (lc.up.size() > nops || lc.mup.size() > nops || lc.bup.size() > nops) return TOOM_EINVAL;
+    if ((s = long_prepare(lc.up, lc.mup, ddesc, mdesc, status, tiles, ctr, nops, st, &lc.bup, bdesc))) return s;
+    unsigned epoch = 1;
+    for (const auto& stp : lc.sup) {
+        toom_status r;
+        if (stp.first == 3) r = launch_long_big(lc.bup[stp.second], bdesc + stp.second, status, CAT_OTHER, st);
+        else if (stp.first == 1) r = launch_long_multi(lc.mup[stp.second], mdesc + stp.second, status, ctr, epoch, CAT_OTHER, st);
+        else {
+            std::vector<LOpDev> one(1, lc.up[stp.second]);
+            r = launch_long_ops(one, (size_t)stp.second, ddesc, status, ctr, epoch, CAT_OTHER, st);
+        }
+        if (r) return r;
+    }
+    return TOOM_OK;
+}
+
 }  // namespace tg
 
 using namespace tg;
@@ -1961,7 +2220,17 @@ toom_status toom_interp_recompose(uint32_t* w, const uint32_t* y, size_t n, size
     LongTables T;
     long_tables(B, T);
     const int Wt = long_Wt(L);
-    const size_t slot_limbs = (size_t)T.nslots * batch * Wt;
+    const size_t slot_limbs = (size_t)long_nslots(B, T.nslots) * batch * Wt;
+    if (B == 16 && g_t16_matrix) {   // the matrix form (f1)
+        s = run_long_call_standalone(slot_limbs, long_tiles(batch, std::max(Wt, 2 * L.n)) * (size_t)L.npts, 64,
+                                     [&](uint32_t* slots, LongCall& lc) {
+                                         long_t16_matrix(L, [&](int k) { return LVec{y + (size_t)k * batch * 2 * L.e, 2 * L.e, 1, 2 * L.e, 1}; },
+                                                         slots, w, lc);
+                                     },
+                                     (cudaStream_t)stream);
+        if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+        return fail(s);
+    }
     s = run_long_standalone(slot_limbs, long_tiles(batch, std::max(Wt, 2 * L.n)), (size_t)T.nio + 1,
                             [&](uint32_t* slots, std::vector<LOpDev>& ops) {
                                 long_interp_ops(L, [&](int k) { return LVec{y + (size_t)k * batch * 2 * L.e, 2 * L.e, 1, 2 * L.e, 1}; },
@@ -2213,6 +2482,8 @@ toom_status toom_base_interleaved(uint32_t* w, const uint32_t* u, const uint32_t
 int toom_npoints(int B) { return ps_desc(B).npts; }
 
 void toom_set_top_stream(int on) { g_top_stream = on; }
+
+void toom_set_t16_matrix(int on) { g_t16_matrix = on != 0; }
 
 void toom_set_fused(int on) {
     // 0: every level staged (k_eval / k_base / k_interp); 1: fused bottom level

@@ -1345,6 +1345,181 @@ struct tg_lop { int dst; int t0; int nt; unsigned odiv; unsigned oinv; int shr; 
 """
 
 
+
+# ------------------------------------------- matrix-form Toom-16 interpolation
+#
+# SURVEY §8(f)1 / PAPER.md:162 ("inverting this matrix ... for specific n this
+# may be faster"): after the even-odd split (Eqs. 4.5-4.6) the 31-point
+# interpolation is two dense solves, done here once symbolically:
+#   E_i = y(+p_i/q_i) + y(-p_i/q_i) = 2 sum_{j even} w_j p_i^j q_i^(30-j)
+#   O_i = y(+p_i/q_i) - y(-p_i/q_i) = 2 sum_{j odd}  w_j p_i^j q_i^(30-j)
+#   w_0 = y_0, w_30 = y_inf;  even rows w_j = (sum_i a_ji E_i + b_j y_0 + c_j y_inf) / D_j
+#   y' = y(2:5) - sum_{j even} w_j 2^j 5^(30-j)   (the unpaired point)
+#   odd rows  w_j = (sum_i a'_ji O_i + d_j y') / D'_j
+# Every D_j = 2^s o_1 o_2 o_3 with coprime odd word factors (primes <= 29);
+# every numerator exactly divisible (the selfcheck below runs the pipeline).
+# Multipliers (<= 120 bits) are balanced 32-bit digits m = sum_d a_d 2^(32 d).
+
+F1_ND = 4
+
+
+def _solve_rows(M):
+    N = len(M)
+    A = [list(map(Fraction, row)) + [Fraction(int(i == r)) for i in range(N)] for r, row in enumerate(M)]
+    for c in range(N):
+        piv = next(r for r in range(c, N) if A[r][c] != 0)
+        A[c], A[piv] = A[piv], A[c]
+        inv = 1 / A[c][c]
+        A[c] = [x * inv for x in A[c]]
+        for r in range(N):
+            if r != c and A[r][c] != 0:
+                f = A[r][c]
+                A[r] = [x - f * y for x, y in zip(A[r], A[c])]
+    return [row[N:] for row in A]
+
+
+def _digits(m, nd=F1_ND):
+    """balanced base-2^32 digits, |a_d| <= 2^31"""
+    out = []
+    for _ in range(nd):
+        d = m & 0xFFFFFFFF
+        if d >= 1 << 31:
+            d -= 1 << 32
+        out.append(d)
+        m = (m - d) >> 32
+    assert m == 0, "multiplier too wide"
+    return out
+
+
+def _word_factor_coprime(o):
+    """odd o -> coprime word factors (prime powers packed greedily below 2^32)"""
+    f = {}
+    p = 3
+    while o > 1:
+        while o % p == 0:
+            f[p] = f.get(p, 0) + 1
+            o //= p
+        p += 2
+    words = []
+    for x in sorted([p**e for p, e in f.items()], reverse=True):
+        assert x < (1 << 32)
+        for i in range(len(words)):
+            if words[i] * x < (1 << 32):
+                words[i] *= x
+                break
+        else:
+            words.append(x)
+    return words
+
+
+def t16_matrix_form(ps=None):
+    ps = ps or pointset_T16_31()
+    pts, d = ps.points, 2 * ps.n
+    pairs, used = [], set()
+    for i, (p, q) in enumerate(pts):
+        if p > 0 and q > 0 and (-p, q) in pts:
+            j = pts.index((-p, q))
+            pairs.append((i, j, p, q))
+            used |= {i, j}
+    i0, iinf = pts.index((0, 1)), pts.index((1, 0))
+    unp = [i for i in range(len(pts)) if i not in used and i not in (i0, iinf)]
+    assert len(unp) == 1
+    iu = unp[0]
+    pu, qu = pts[iu]
+    lcm = lambda xs: reduce(_lcm, xs, 1)
+    ev = list(range(2, d - 1, 2))
+    Ie = _solve_rows([[2 * p**j * q**(d - j) for j in ev] for (_, _, p, q) in pairs])
+    even = []
+    for r, j in enumerate(ev):
+        coef = list(Ie[r]) + [Fraction(0), Fraction(0)]
+        for i, (_, _, p, q) in enumerate(pairs):
+            coef[len(pairs)] -= Ie[r][i] * 2 * q**d
+            coef[len(pairs) + 1] -= Ie[r][i] * 2 * p**d
+        D = lcm([c.denominator for c in coef])
+        even.append((j, [int(c * D) for c in coef], D))
+    od = list(range(1, d, 2))
+    Io = _solve_rows([[2 * p**j * q**(d - j) for j in od] for (_, _, p, q) in pairs] + [[pu**j * qu**(d - j) for j in od]])
+    odd = []
+    for r, j in enumerate(od):
+        coef = list(Io[r])
+        D = lcm([c.denominator for c in coef])
+        odd.append((j, [int(c * D) for c in coef], D))
+    ymul = [pu**j * qu**(d - j) for j in range(0, d + 1, 2)]
+    return dict(pairs=pairs, i0=i0, iinf=iinf, iu=iu, even=even, odd=odd, ymul=ymul, d=d, pts=pts)
+
+
+def t16_matrix_selfcheck(F, trials=12, bits=400, seed=7):
+    rnd = random.Random(seed)
+    d, pts = F["d"], F["pts"]
+    for _ in range(trials):
+        w = [rnd.getrandbits(bits) - (rnd.getrandbits(1) << (bits - 1)) for _ in range(d + 1)]
+        y = [sum(w[j] * p**j * q**(d - j) for j in range(d + 1)) for (p, q) in pts]
+        E = [y[a] + y[b] for a, b, _, _ in F["pairs"]]
+        O = [y[a] - y[b] for a, b, _, _ in F["pairs"]]
+        wr = [None] * (d + 1)
+        wr[0], wr[d] = y[F["i0"]], y[F["iinf"]]
+        for j, cf, D in F["even"]:
+            X = sum(c * x for c, x in zip(cf, E + [y[F["i0"]], y[F["iinf"]]]))
+            # the executor's order: / o1 >> s, then / o2, / o3 -- each exact
+            s = (D & -D).bit_length() - 1
+            words = _word_factor_coprime(D >> s) or [1]
+            assert X % words[0] == 0 and (X // words[0]) % (1 << s) == 0
+            X = (X // words[0]) >> s
+            for o in words[1:]:
+                assert X % o == 0
+                X //= o
+            wr[j] = X
+        yp = y[F["iu"]] - sum(wr[j] * m for j, m in zip(range(0, d + 1, 2), F["ymul"]))
+        for j, cf, D in F["odd"]:
+            X = sum(c * x for c, x in zip(cf, O + [yp]))
+            s = (D & -D).bit_length() - 1
+            words = _word_factor_coprime(D >> s) or [1]
+            X = (X // words[0]) >> s
+            for o in words[1:]:
+                assert X % o == 0
+                X //= o
+            wr[j] = X
+        assert wr == w, "matrix-form T16 interpolation is not exact"
+    return True
+
+
+def emit_t16_matrix_tables() -> str:
+    F = t16_matrix_form()
+    t16_matrix_selfcheck(F)
+    L = ["// ---- matrix-form Toom-16 interpolation (f1; PAPER.md:162, Eqs. 4.5-4.6), generated and",
+         "// checked by toomgen.t16_matrix_form / t16_matrix_selfcheck"]
+    NPR = len(F["pairs"])
+    L.append(f"constexpr int tg_f1_npairs = {NPR};")
+    L.append(f"constexpr int tg_f1_nd = {F1_ND};")
+    L.append("constexpr int tg_f1_pair[%d][2] = {%s};" % (NPR, ", ".join("{%d, %d}" % (a, b) for a, b, _, _ in F["pairs"])))
+    L.append(f"constexpr int tg_f1_i0 = {F['i0']}, tg_f1_iinf = {F['iinf']}, tg_f1_iu = {F['iu']};")
+
+    def rows(name, R, nsrc):
+        NW = 3
+        L.append(f"constexpr int tg_f1_{name}_n = {len(R)};")
+        L.append(f"constexpr int tg_f1_{name}_j[{len(R)}] = {{" + ", ".join(str(j) for j, _, _ in R) + "};")
+        L.append(f"constexpr int tg_f1_{name}_a[{len(R)}][{nsrc}][{F1_ND}] = {{")
+        for _, cf, _ in R:
+            assert len(cf) == nsrc
+            L.append("  {" + ", ".join("{" + ", ".join(str(x) for x in _digits(c)) + "}" for c in cf) + "},")
+        L.append("};")
+        sh, ws = [], []
+        for _, _, D in R:
+            s = (D & -D).bit_length() - 1
+            words = _word_factor_coprime(D >> s)
+            assert len(words) <= NW
+            sh.append(s)
+            ws.append(words + [1] * (NW - len(words)))
+        L.append(f"constexpr int tg_f1_{name}_s[{len(R)}] = {{" + ", ".join(str(x) for x in sh) + "};")
+        L.append(f"constexpr unsigned tg_f1_{name}_o[{len(R)}][{NW}] = {{" +
+                 ", ".join("{" + ", ".join(f"{x}u" for x in w) + "}" for w in ws) + "};")
+
+    rows("even", F["even"], NPR + 2)
+    rows("odd", F["odd"], NPR + 1)
+    L.append(f"constexpr int tg_f1_ymul[{len(F['ymul'])}][{F1_ND}] = {{" +
+             ", ".join("{" + ", ".join(str(x) for x in _digits(m)) + "}" for m in F["ymul"]) + "};")
+    return "\n".join(L)
+
 def generate_all():
     # T16 (31 points, C5's top level) runs through the long-vector path, not
     # the streaming emitter (its multipliers exceed one word).
@@ -1379,6 +1554,7 @@ def generate_all():
     parts.append(LONG_HEADER)
     for ps in [pointset_T3(), pointset_T4(), pointset_paper(8), pointset_T16_31()]:
         parts.append(emit_long_tables(ps))
+    parts.append(emit_t16_matrix_tables())
     return "\n\n".join(parts) + "\n", meta
 
 

@@ -544,3 +544,27 @@ def test_streams_and_repeat_determinism():
     s.synchronize()
     assert np.array_equal(a, host(w))
     assert np.array_equal(a, run_batched(u, v, 8))
+
+
+@pytest.mark.parametrize("n", [1 << 13, 20011, 1 << 16])
+def test_t16_matrix_form_equals_newton_program(n):
+    """The matrix-form Toom-16 interpolation (f1) against the
+    staged Newton program and the oracle, through
+    toom_mul and through the stage export (the sharded C5 top level)."""
+    seed = synth.seed_for(5)
+    u = synth.uniform_limbs(seed, 21, 1, 0, n)[0]
+    v = synth.uniform_limbs(seed, 21, 1, 1, n)[0]
+    u[: n // 3] = 0xFFFFFFFF          # long carry runs
+    got = {}
+    try:
+        for mode in (True, False):
+            tg.set_t16_matrix(mode)
+            got[mode] = host(tg.toom_mul(dev(u), dev(v), B=16))
+            U, V = tg.eval_points(dev(u[None]), 16), tg.eval_points(dev(v[None]), 16)
+            Y = tg.mul_signed_batched(U[:, 0].contiguous(), V[:, 0].contiguous(), B=4)
+            got[(mode, "stage")] = host(tg.interp_recompose(Y.view(31, 1, -1).contiguous(), n, 16))[0]
+    finally:
+        tg.set_t16_matrix(True)
+    want = oracle.schoolbook(u, v) if n <= 20011 else oracle.toom(u, v, top_B=16)
+    for k, w in got.items():
+        assert np.array_equal(w, want), k
