@@ -50,7 +50,10 @@ typedef enum {
  * top_B: B of the top level: 3 (points 0,1,-1,2,inf), 4 (0,+-1,+-2,1/2,inf),
  *        8 (the paper's points 0,+-1,+-2,...,+-64) or
  *        16 (31 points: 0, inf and the 29 smallest-height +-p/q, homogeneous;
- *        BASELINE configs[4]);
+ *        BASELINE configs[4]) or 32 (the paper's points 0, +-2^j, j < 31: B = 32
+ *        as the paper's 64-bit code allows; divisors up to 2^60
+ *        run as exact divisions by their 32-bit word factors); 16 and 32 run
+ *        on the limb-parallel long-vector kernels only;
  * lower levels: Toom-4 while the operand has more than t4 limbs, Toom-3
  *        while more than t3 limbs, schoolbook base case otherwise (<= 64 limbs);
  * chunk: products per scheduling chunk (0 = automatic);
@@ -74,7 +77,7 @@ toom_plan_t toom_default_plan(int B);
 
 /* w[i] = u[i] * v[i] for i < batch.
  * u, v: [batch][n] uint32 (row-major, device); w: [batch][2n] (device).
- * B: top-level B in {3, 4, 8, 16} (see toom_plan_t).  n >= 1, batch >= 0
+ * B: top-level B in {3, 4, 8, 16, 32} (see toom_plan_t).  n >= 1, batch >= 0
  * (batch 0: no-op).
  * Errors: TOOM_EINVAL (null/aliasing/B), TOOM_ENOMEM, TOOM_ECUDA.           */
 toom_status toom_mul_batched(uint32_t *w, const uint32_t *u, const uint32_t *v,
@@ -84,6 +87,15 @@ toom_status toom_mul_batched(uint32_t *w, const uint32_t *u, const uint32_t *v,
 toom_status toom_mul_batched_plan(uint32_t *w, const uint32_t *u, const uint32_t *v,
                                   size_t n, size_t batch, const toom_plan_t *plan,
                                   void *stream);
+
+/* Squaring specialisation: w[i] = u[i]^2 for i < batch,
+ * layouts as toom_mul_batched (u: [batch][n], w: [batch][2n], device).  The
+ * evaluation runs once (V = U at every level, Eq. 1.1-1.2 for one operand) and
+ * the base case squares: sum_{i<j} 2 a_i a_j + a_i^2, E(E+1)/2 instead of E^2
+ * limb-products.  Errors as toom_mul_batched.  toom_mul with u == v and
+ * nu == nv takes the same path.                                            */
+toom_status toom_sqr_batched(uint32_t *w, const uint32_t *u, size_t n, size_t batch, const toom_plan_t *plan,
+                             void *stream);
 
 /* w[0 .. nu+nv) = u[0..nu) * v[0..nv) (device pointers).  nu, nv >= 0;
  * zero-length operands are zero (w is zeroed).  The shorter operand is

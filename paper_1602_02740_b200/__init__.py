@@ -70,6 +70,7 @@ SIGNATURES = {
     "toom_mul_signed_batched": (_I, [_P, _P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
     "toom_product_width_point": (_SZ, [_SZ, _I]),
     "toom_set_check": (None, [_I]),
+    "toom_sqr_batched": (_I, [_P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
     "toom_set_t16_matrix": (None, [_I]),
     "toom_set_verify": (None, [_I]),
     "toom_debug_fault": (None, [_I]),
@@ -132,6 +133,21 @@ def toom_mul_batched(u: torch.Tensor, v: torch.Tensor, B: int = 4, t4: int = 256
                                      ctypes.byref(p),
                                      _stream(stream))
     _check(st, "toom_mul_batched")
+    return out
+
+
+def toom_sqr_batched(u: torch.Tensor, B: int = 4, t4: int = 256, t3: int = 64, chunk: int = 0,
+                     out: torch.Tensor | None = None, stream=None, long_count: int = 0) -> torch.Tensor:
+    """w[i] = u[i]^2 (squaring specialisation); u: [batch][n] uint32 CUDA tensor."""
+    if u.dim() != 2:
+        raise ValueError("u must be [batch][n]")
+    batch, n = u.shape
+    if out is None:
+        out = torch.empty((batch, 2 * n), dtype=u.dtype, device=u.device)
+    p = plan(B, t4, t3, chunk, long_count)
+    st = lib().toom_sqr_batched(_out(out, "out", (batch, 2 * n), u), _dev(u, "u"), n, batch, ctypes.byref(p),
+                                _stream(stream))
+    _check(st, "toom_sqr_batched")
     return out
 
 

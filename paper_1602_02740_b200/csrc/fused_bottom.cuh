@@ -196,6 +196,45 @@ __device__ __forceinline__ void mul_twos_to_smem(const uint32_t (&a)[E], const u
     }
 }
 
+// squaring specialisation: a^2 = |a|^2 of an E-limb two's-
+// complement value, 2E limbs to dst[t*32]: the cross products
+// sum_{i<j} a_i a_j 2^(32(i+j)) by product scanning (E(E-1)/2 limb-products
+// instead of E^2), then doubled and the diagonal squares a_i^2 2^(64 i) added
+// in one carry pass over the limbs.
+template <int E>
+__device__ __forceinline__ void sqr_twos_to_smem(uint32_t (&a)[E], uint32_t* dst) {
+    {
+        const uint32_t sa = a[E - 1] >> 31, m = 0u - sa;
+        uint32_t cy = sa;
+#pragma unroll
+        for (int i = 0; i < E; ++i) { const uint32_t x = (a[i] ^ m) + cy; cy = (x < cy) ? 1u : 0u; a[i] = x; }
+    }
+    uint32_t c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+    for (int k = 1; k < 2 * E - 2; ++k) {
+#pragma unroll
+        for (int i = (k < E ? 0 : k - E + 1); 2 * i < k; ++i) TG_MADD(c0, c1, c2, a[i], a[k - i]);
+        dst[k * 32] = c0;
+        c0 = c1; c1 = c2; c2 = 0;
+    }
+    dst[(2 * E - 2) * 32] = c0;
+    dst[(2 * E - 1) * 32] = c1;
+    // w = 2 C + sum_i a_i^2 2^(64 i): limb k gets (C_k << 1 | C_{k-1} >> 31) and
+    // the low (k even) or high (k odd) word of a_{k/2}^2
+    uint64_t acc = 0;
+    uint32_t prev = 0;   // C_{k-1}
+#pragma unroll
+    for (int k = 0; k < 2 * E; ++k) {
+        const uint32_t ck = k >= 1 ? dst[k * 32] : 0u;
+        const uint32_t dbl = (ck << 1) | (prev >> 31);
+        prev = ck;
+        const uint64_t sq = (uint64_t)a[k >> 1] * a[k >> 1];
+        acc += (uint64_t)dbl + ((k & 1) ? (uint32_t)(sq >> 32) : (uint32_t)sq);
+        dst[k * 32] = (uint32_t)acc;
+        acc >>= 32;
+    }
+}
+
 // |a| * |b| with the product sign applied, 2E limbs streamed to dst[t*32]
 template <int E>
 __device__ __forceinline__ void mul_signed_to_smem(uint32_t (&a)[E], uint32_t (&b)[E], uint32_t* dst) {
@@ -256,7 +295,7 @@ __device__ int tg_fused_phase_mask = 7;
 // otherwise.
 // N_, BB_ != 0 fix n and b (hence Lw = 2b+1, wout = 2n, nseg) at compile time
 // (the C2 shape): shared-memory offsets and trip counts become immediates.
-template <int B, int E, int MODE, int N_ = 0, int BB_ = 0>
+template <int B, int E, int MODE, int N_ = 0, int BB_ = 0, bool SQ = false>
 __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_bottom(
     const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV, uint32_t* __restrict__ out,
     size_t count, int n_, int b_, int Lw_, int wout_, int nseg_) {
@@ -380,7 +419,10 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
         uint32_t a[E], bb[E];
 #pragma unroll
         for (int t = 0; t < E; ++t) { a[t] = slot[t * G]; bb[t] = slot[(E + t) * G]; }
-        if (pmask & 1) mul_twos_to_smem<E>(a, bb, slot);
+        if (pmask & 1) {
+            if constexpr (SQ) sqr_twos_to_smem<E>(a, slot);   // V = U: the square
+            else mul_twos_to_smem<E>(a, bb, slot);
+        }
         // fault injection (tests): one flipped bit of y_1 of the
         // CTA's first instance makes the rows' exact divisions inexact
         if (tg_fault && blockIdx.x == 0 && lane == 0 && warp == 1) slot[3 * G] ^= 1u;

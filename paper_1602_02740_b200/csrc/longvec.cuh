@@ -34,11 +34,11 @@ namespace tg {
 #ifndef TG_LONGOP_MINB
 #define TG_LONGOP_MINB 2   // two tiles per SM (<= 128 registers)
 #endif
-constexpr int LV_MAXT = 40;     // terms per op
+constexpr int LV_MAXT = 64;     // terms per op (the P32 recomposition has 63)
 constexpr int LV_NT = 256;      // threads per tile
 constexpr int LV_CH = 16;       // limbs per thread (long vectors; 4 for short ones)
 constexpr int LV_TL = LV_NT * LV_CH;
-constexpr int LV_MAXHALO = 8;   // look-ahead limbs of the final right shift (shr < 32*7)
+constexpr int LV_MAXHALO = 10;  // look-ahead limbs of the final right shift (shr < 32*9: P32 shifts up to 271 bits)
 
 struct LTermDev {
     const uint32_t* base;       // limb `start` of instance 0
@@ -738,6 +738,12 @@ static uint32_t host_invmod(uint32_t a, uint32_t o) {   // o odd, gcd(a, o) = 1
     return (uint32_t)t;
 }
 
+// set when an op needed more than LV_MAXT terms; the call that built it fails
+inline bool& lv_build_overflow() {
+    static thread_local bool f = false;
+    return f;
+}
+
 struct LOpBuilder {
     LOpDev op;
     LOpBuilder(uint32_t* dst, long long is, long long ls, int W, int count, uint32_t o = 1, int shr = 0) {
@@ -774,7 +780,8 @@ struct LOpBuilder {
     }
     // term m * (slice << s), slice = limbs [start, start+len) of v (len clipped to v.len)
     bool add(const LVec& v, long long m, long long s, int start = 0, int len = -1, int sign = -1) {
-        if (op.nt >= LV_MAXT || m == 0) return m == 0;
+        if (m == 0) return true;
+        if (op.nt >= LV_MAXT) { lv_build_overflow() = true; return false; }   // the call fails (EUNSUPPORTED)
         LTermDev& T = op.t[op.nt++];
         T.base = v.base + (long long)start * v.ls;
         T.inst_stride = v.is;

@@ -644,16 +644,38 @@ __global__ void __launch_bounds__(128, 3) k_lbig2(const LBigDev* __restrict__ dp
     const long long inst = tile / d.tiles_per_inst;
     const int kt = (int)(tile - inst * d.tiles_per_inst);
     const int tstart = kt * TL;
-    const int NI = TL + LB_PRE + LM_HALO;
-    for (int sI = 0; sI < d.ns; ++sI) {
-        const LMSrc& S = d.src[sI];
-        const uint32_t* sp = S.base + inst * S.is;
-        uint32_t fill = 0;
-        if (S.sign && S.len > 0) fill = (__ldg(sp + (S.len - 1)) >> 31) ? 0xFFFFFFFFu : 0u;
-        uint32_t* sj = Sb + (size_t)sI * CH * NP1;
-        for (int i = tid; i < NI; i += NT) {
-            const int t = tstart - LB_PRE + i;
-            sj[(i % CH) * NP1 + i / CH] = t < 0 ? 0u : (t < S.len ? __ldg(sp + t) : fill);
+    // staging: every thread issues the loads of two sources before storing
+    // (a load-store loop per element was latency-bound: 11 long-scoreboard
+    // stalls per issue, profiles/r02_lbig2_ncu.csv)
+    constexpr int EX = (LB_PRE + LM_HALO + 31) / 32;   // extra elements past TL, per warp lane
+    for (int s0 = 0; s0 < d.ns; s0 += 2) {
+        uint32_t xv[2][CH + EX];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int sI = s0 + h;
+            if (sI >= d.ns) break;
+            const LMSrc& S = d.src[sI];
+            const uint32_t* sp = S.base + inst * S.is;
+            uint32_t fill = 0;
+            if (S.sign && S.len > 0) fill = (__ldg(sp + (S.len - 1)) >> 31) ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+            for (int q = 0; q < CH + EX; ++q) {
+                const int i = tid + q * NT;   // relative index; q >= CH: the tail past TL
+                const int t = tstart - LB_PRE + i;
+                xv[h][q] = (q >= CH && i >= TL + LB_PRE + LM_HALO) ? 0u
+                           : (t < 0 ? 0u : (t < S.len ? __ldg(sp + t) : fill));
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int sI = s0 + h;
+            if (sI >= d.ns) break;
+            uint32_t* sj = Sb + (size_t)sI * CH * NP1;
+#pragma unroll
+            for (int q = 0; q < CH + EX; ++q) {
+                const int i = tid + q * NT;
+                if (q < CH || i < TL + LB_PRE + LM_HALO) sj[(i % CH) * NP1 + i / CH] = xv[h][q];
+            }
         }
     }
     __syncthreads();

@@ -36,23 +36,28 @@ struct PSDesc {
     int B;
     int npts;
     uint64_t S;   // max over points of sum_k |p^k q^(n-k)| (value growth factor)
+    int grow;     // limbs an evaluated operand grows by: e = b + grow
 };
 
+static int bitlen(uint64_t x) { int b = 0; while (x) { ++b; x >>= 1; } return b; }
+
 static PSDesc ps_desc(int B) {
+    auto g = [](uint64_t S) { return (bitlen(S) + 1 + 31) / 32; };
     switch (B) {
-        case 3: return {3, 5, 7};          // points 0,1,-1,2,inf: S = 1+2+4
-        case 4: return {4, 7, 15};         // 0,+-1,+-2,1/2,inf: S = 1+2+4+8
-        case 8: {                          // 0,+-1,...,+-64: S = sum 64^k, k<8
+        case 3: return {3, 5, 7, g(7)};            // points 0,1,-1,2,inf: S = 1+2+4
+        case 4: return {4, 7, 15, g(15)};          // 0,+-1,+-2,1/2,inf: S = 1+2+4+8
+        case 8: {                                  // 0,+-1,...,+-64: S = sum 64^k, k<8
             uint64_t s = 0, p = 1;
             for (int k = 0; k < 8; ++k) { s += p; p *= 64; }
-            return {8, 15, s};
+            return {8, 15, s, g(s)};
         }
-        case 16: return {16, 31, tg_growthS_T16};   // 31-point set (configs[4])
-        default: return {0, 0, 0};
+        case 16: return {16, 31, tg_growthS_T16, g(tg_growthS_T16)};   // 31-point set (configs[4])
+        // the paper's points 0, +-2^j (j < 31) at B = 32:
+        // S = sum 2^(30 k) does not fit 64 bits; its limb count is generated
+        case 32: return {32, 63, 0, tg_growthLimbs_P32};
+        default: return {0, 0, 0, 0};
     }
 }
-
-static int bitlen(uint64_t x) { int b = 0; while (x) { ++b; x >>= 1; } return b; }
 
 // ------------------------------------------------------------------------
 // accessors for the generated streaming programs
@@ -396,6 +401,7 @@ struct Plan {
     size_t bytes = 0;
     bool fused = false;      // bottom Toom level runs as k_fused_bottom
     bool signed_in = false;  // user operands are two's complement (stage export)
+    bool square = false;     // v = u: V children alias U children, squaring base case
     // long-vector levels: slot pool, scan status, tile counters, op descriptors
     size_t offSlots = 0, offStatus = 0, offCtr = 0, offDesc = 0;
     size_t nStatus = 0, nCtr = 0, nDesc = 0;
@@ -425,6 +431,7 @@ static bool long_tables(int B, LongTables& T) {
         case 4: TG_LT(T4)
         case 8: TG_LT(P8)
         case 16: TG_LT(T16)
+        case 32: TG_LT(P32)
         default: return false;
     }
 #undef TG_LT
@@ -516,7 +523,9 @@ static int top_warp_ch(const Level& Lv) {
     return 0;
 }
 
-static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& plan, bool top_long = false) {
+static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& plan, bool top_long = false,
+                             bool square = false) {
+    plan.square = square;
     plan.lv.clear();
     size_t count = batch;
     int width = n;
@@ -535,7 +544,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         L.npts = d.npts;
         L.b = (width + L.B - 1) / L.B;
         L.lentop = width - (L.B - 1) * L.b;
-        L.e = L.b + (bitlen(d.S) + 1 + 31) / 32;
+        L.e = L.b + d.grow;
         L.Lw = 2 * L.b + 1;
         plan.lv.push_back(L);
         count *= (size_t)d.npts;
@@ -559,7 +568,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
                              2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e;
         for (size_t l = 0; l < NL; ++l) {
             Level& L = plan.lv[l];
-            const bool want = L.B == 16 || (top_long && l == 0) ||   // T16: no instance-parallel program
+            const bool want = L.B == 16 || L.B == 32 || (top_long && l == 0) ||   // T16/P32: no instance-parallel program
                               (p.long_count == 0 ? (L.n > g_long_min_n && L.count < (size_t)g_long_max_count)
                                                  : (p.long_count > 1 && L.count < p.long_count)) ||
                               // below a long level, operands too long to be resident stay long
@@ -576,7 +585,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         }
 
         for (size_t l = 0; l + 1 < plan.lv.size(); ++l)
-            if (plan.lv[l].B == 16 && !plan.lv[l].lng) return TOOM_EUNSUPPORTED;   // T16 runs long only
+            if ((plan.lv[l].B == 16 || plan.lv[l].B == 32) && !plan.lv[l].lng) return TOOM_EUNSUPPORTED;   // long only
     }
     // fused bottom level?
     plan.fused = false;
@@ -598,7 +607,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         Level& L = plan.lv[l];
         const size_t cc = L.count * (size_t)L.npts;
         L.offU = take((size_t)L.e * cc);
-        L.offV = take((size_t)L.e * cc);
+        L.offV = square ? L.offU : take((size_t)L.e * cc);   // squaring: V = U
         L.offP = take((size_t)2 * L.e * cc);
         L.offW = L.lng ? 0 : take((size_t)L.npts * L.Lw * L.count);
     }
@@ -875,7 +884,8 @@ static toom_status launch_base(int E, const uint32_t* U, const uint32_t* V, uint
 }
 
 template <int B, int E, int TOP>
-static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out, cudaStream_t st) {
+static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out, cudaStream_t st,
+                           bool sq = false) {
     const int nseg = (2 * Lv.n + Lv.b - 1) / Lv.b;
     const size_t smem = fused_smem_bytes(B, E, Lv.Lw, nseg, Lv.n, TOP);
     auto kern = k_fused_bottom<B, E, TOP>;
@@ -885,8 +895,13 @@ static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* 
     // the C3 / C4 bottom (parents of 66 limbs, b = 22)
     if constexpr (B == 3 && E == 23 && TOP == 0)
         if (Lv.n == 66 && Lv.b == 22 && Lv.Lw == 45 && g_its_static) kern = k_fused_bottom<3, 23, 0, 66, 22>;
-    static bool attr_set[2] = {false, false};   // per instantiation
-    const int ai = kern == k_fused_bottom<B, E, TOP> ? 0 : 1;
+    // squaring (v = u): the generic-shape kernel with the squaring base case
+    // (instantiated for the base widths of C1-C5; others multiply u by u)
+    bool sqk = false;
+    if constexpr ((E == 18 || E == 23 || E == 33) && TOP != 3)
+        if (sq) { kern = k_fused_bottom<B, E, TOP, 0, 0, true>; sqk = true; }
+    static bool attr_set[3] = {false, false, false};   // per instantiation
+    const int ai = sqk ? 2 : (kern == k_fused_bottom<B, E, TOP> ? 0 : 1);
     if (!attr_set[ai]) {
         if (const char* m = getenv("TOOM_DBG_FUSED_MASK")) {   // diagnostics only
             const int v = atoi(m);
@@ -902,15 +917,15 @@ static void launch_fused_t(const Level& Lv, const uint32_t* su, const uint32_t* 
 
 // mode: 0 interleaved signed parents, 1 row-major unsigned (top), 2 row-major signed
 static toom_status launch_fused(const Level& Lv, int mode, const uint32_t* su, const uint32_t* sv, uint32_t* out,
-                                cudaStream_t st) {
+                                cudaStream_t st, bool sq = false) {
     if (Lv.count == 0) return TOOM_OK;
     ProfScope ps(CAT_BASE, st);
 #define TG_F(BB, EE)                                                      \
     if (Lv.B == BB && Lv.e == EE) {                                       \
-        if (mode == 1) launch_fused_t<BB, EE, 1>(Lv, su, sv, out, st);    \
-        else if (mode == 2) launch_fused_t<BB, EE, 2>(Lv, su, sv, out, st); \
-        else if (mode == 3) launch_fused_t<BB, EE, 3>(Lv, su, sv, out, st); \
-        else launch_fused_t<BB, EE, 0>(Lv, su, sv, out, st);              \
+        if (mode == 1) launch_fused_t<BB, EE, 1>(Lv, su, sv, out, st, sq);    \
+        else if (mode == 2) launch_fused_t<BB, EE, 2>(Lv, su, sv, out, st, sq); \
+        else if (mode == 3) launch_fused_t<BB, EE, 3>(Lv, su, sv, out, st, sq); \
+        else launch_fused_t<BB, EE, 0>(Lv, su, sv, out, st, sq);              \
         ps.done(st);                                                      \
         ++t_launches;                                                     \
         return TOOM_OK;                                                   \
@@ -930,13 +945,17 @@ static bool top_rows_ok(const Level& Lv) {
 }
 
 static toom_status launch_eval_top_rows(const Level& Lv, const uint32_t* u, const uint32_t* v, uint32_t* U1,
-                                        uint32_t* V1, cudaStream_t st) {
-    ProfScope ps(CAT_EVAL, st);
-    const unsigned grid = (unsigned)((Lv.count + 31) / 32);
+                                        uint32_t* V1, cudaStream_t st, bool sq = false) {
     // 16-byte cp.async staging needs 16-byte aligned operand rows
     const bool v4 = g_eval_v4 && Lv.B <= 4 && (Lv.n & 3) == 0 && (Lv.b & 3) == 0 &&
                     ((((uintptr_t)u) | ((uintptr_t)v)) & 15) == 0;
-    if (v4 && Lv.B == 3) k_eval_top_v4<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
+    // squaring without the vectorised kernel: one thread per operand, u only
+    if (sq && !v4) return launch_eval(Lv.B, true, u, nullptr, U1, nullptr, Lv.count, Lv.n, Lv.b, Lv.e, st);
+    ProfScope ps(CAT_EVAL, st);
+    const unsigned grid = (unsigned)((Lv.count + 31) / 32);
+    if (v4 && sq && Lv.B == 3) k_eval_top_v4<3, true><<<grid, 32 * 5, 0, st>>>(u, u, U1, U1, Lv.count, Lv.n, Lv.b, Lv.e);
+    else if (v4 && sq) k_eval_top_v4<4, true><<<grid, 32 * 7, 0, st>>>(u, u, U1, U1, Lv.count, Lv.n, Lv.b, Lv.e);
+    else if (v4 && Lv.B == 3) k_eval_top_v4<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     else if (v4) k_eval_top_v4<4><<<grid, 32 * 7, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     else if (Lv.B == 3) k_eval_top_rows<3><<<grid, 32 * 5, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
     else if (Lv.B == 4) k_eval_top_rows<4><<<grid, 32 * 7, 0, st>>>(u, v, U1, V1, Lv.count, Lv.n, Lv.b, Lv.e);
@@ -1108,7 +1127,7 @@ static LVec child_vec(const Plan& plan, size_t l, const uint8_t* ws, size_t off,
     const Level& L = plan.lv[l];
     if ((int)l == plan.bnd) {   // row-major staging, transposed to/from the level below
         size_t o = plan.offT;
-        if (off == L.offV) o += (size_t)L.e * L.count * L.npts * 4;
+        if (off == L.offV && L.offV != L.offU) o += (size_t)L.e * L.count * L.npts * 4;
         const uint32_t* base = (const uint32_t*)(ws + o);
         return LVec{base + (size_t)k * L.count * width, width, 1, width, 1};
     }
@@ -1190,8 +1209,15 @@ static void long_interp_ops(const Level& L, YF yv, uint32_t* slots, uint32_t* ds
 
 // tile shape of a multi-output op: the largest tile within the shared-memory
 // budget that pads the vector by at most 1/8
+// multi-output ops staging at least this many sources use 4 limbs per thread
+// (off by default: C5 106.0 ms at 16 limbs vs 107.6 ms with 4 from 8 sources)
+static int g_multi_ch4_ns = [] {
+    const char* e = getenv("TOOM_MULTI_CH4_NS");
+    return e ? atoi(e) : 1 << 20;
+}();
+
 static bool multi_shape(LMultiDev& d) {
-    d.ch = 16;   // the per-output scan costs ~1k instructions per thread: amortise over 16 limbs
+    d.ch = d.ns >= g_multi_ch4_ns ? 4 : 16;   // 16: the per-output scan amortised over 16 limbs
     int best = 0;
     long long bestw = -1;
     for (int nt = LV_NT; nt >= 32; nt -= 32) {
@@ -1459,7 +1485,7 @@ static void long_t16_matrix(const Level& L, YF yv, uint32_t* slots, uint32_t* ds
 static void build_long_level(const Plan& plan, size_t l, uint32_t* w, const uint32_t* u, const uint32_t* v, uint8_t* ws,
                              LongCall& lc) {
     const Level& L = plan.lv[l];
-    for (int opd = 0; opd < 2; ++opd) {
+    for (int opd = 0; opd < (plan.square ? 1 : 2); ++opd) {   // squaring: V = U
         LVec par;
         if (l == 0) par = LVec{opd ? v : u, L.n, 1, L.n, plan.signed_in ? 1 : 0};   // user operands, row-major
         else par = LVec{(const uint32_t*)(ws + (opd ? plan.lv[l - 1].offV : plan.lv[l - 1].offU)), L.n, 1, L.n, 1};
@@ -1493,7 +1519,9 @@ static void build_long_level(const Plan& plan, size_t l, uint32_t* w, const uint
         lc.up.push_back(b.op);
         return;
     }
-    if (L.B == 16 && g_t16_matrix) {
+    // (the matrix form stages its sources row-major: products of a schoolbook
+    // level directly below, interleaved, take the Newton program)
+    if (L.B == 16 && g_t16_matrix && yv(0).ls == 1) {
         long_t16_matrix(L, yv, slots, dst, lc);
         return;
     }
@@ -1761,7 +1789,7 @@ static toom_status launch_res(const Plan& plan, size_t l, bool down, uint32_t* w
         const int sgn = (l > 0 || plan.signed_in) ? 1 : 0;
         const int nt = res_threads(L.e);
         const size_t sm = res_eval_smem(L.n);
-        dim3 grid((unsigned)cnt, 2);
+        dim3 grid((unsigned)cnt, plan.square ? 1 : 2);   // squaring: u only
         uint32_t* du = (uint32_t*)cu.base;
         uint32_t* dv = (uint32_t*)cv.base;
         if (L.B == 3) {
@@ -1855,6 +1883,7 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             for (auto x : one.sup) ups[l].push_back({x.first, x.second + (x.first == 3 ? bu : (x.first ? mu : ou))});
         }
         for (size_t l = Tl; l-- > 0;) sup.insert(sup.end(), ups[l].begin(), ups[l].end());
+        if (lv_build_overflow()) { lv_build_overflow() = false; return TOOM_EUNSUPPORTED; }
         if (ops.size() > plan.nDesc || mops.size() > plan.nDesc || bops.size() > plan.nDesc ||
             ops.size() + mops.size() > plan.nCtr)
             return TOOM_EINVAL;
@@ -1865,7 +1894,8 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             const size_t cc = Lb.count * Lb.npts;
             ProfScope ps(CAT_OTHER, st);
             launch_transpose((const uint32_t*)(ws + plan.offT), (uint32_t*)(ws + Lb.offU), cc, Lb.e, st);
-            launch_transpose((const uint32_t*)(ws + plan.offT) + cc * Lb.e, (uint32_t*)(ws + Lb.offV), cc, Lb.e, st);
+            if (Lb.offV != Lb.offU)   // (squaring: V = U)
+                launch_transpose((const uint32_t*)(ws + plan.offT) + cc * Lb.e, (uint32_t*)(ws + Lb.offV), cc, Lb.e, st);
             ps.done(st);
         }
     }
@@ -1890,11 +1920,12 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         const uint32_t* su = l == 0 ? u : (const uint32_t*)(ws + plan.lv[l - 1].offU);
         const uint32_t* sv = l == 0 ? v : (const uint32_t*)(ws + plan.lv[l - 1].offV);
         if (l == 0 && top_rows_ok(Lv)) {   // (B = 8 via k_eval_top_rows<8> measured slower: 128 CTAs for C3)
-            if ((s = launch_eval_top_rows(Lv, su, sv, (uint32_t*)(ws + Lv.offU), (uint32_t*)(ws + Lv.offV), st)))
+            if ((s = launch_eval_top_rows(Lv, su, sv, (uint32_t*)(ws + Lv.offU), (uint32_t*)(ws + Lv.offV), st, plan.square)))
                 return s;
             continue;
         }
-        if ((s = launch_eval(Lv.B, l == 0, su, sv, (uint32_t*)(ws + Lv.offU), (uint32_t*)(ws + Lv.offV), Lv.count, Lv.n,
+        if ((s = launch_eval(Lv.B, l == 0, su, plan.square ? nullptr : sv, (uint32_t*)(ws + Lv.offU),
+                             plan.square ? nullptr : (uint32_t*)(ws + Lv.offV), Lv.count, Lv.n,
                              Lv.b, Lv.e, st)))
             return s;
     }
@@ -1908,7 +1939,7 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         // a long parent level writes row-major children; a warp-per-product top
         // interpolation reads row-major products
         const int mode = top ? 1 : (plan.lv[L - 2].lng ? 2 : (plan.top_warp ? 3 : 0));
-        if ((s = launch_fused(Lv, mode, su, sv, out, st))) return s;
+        if ((s = launch_fused(Lv, mode, su, sv, out, st, plan.square))) return s;
     } else {
         const Level& Lv = plan.lv[L - 1];
         if ((s = launch_base(Lv.e, (const uint32_t*)(ws + Lv.offU), (const uint32_t*)(ws + Lv.offV),
@@ -1972,7 +2003,7 @@ static size_t ws_need(const Plan& plan, size_t chunk, size_t n) {
 }
 
 static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
-                           const toom_plan_t& p, cudaStream_t st, bool sgn = false);
+                           const toom_plan_t& p, cudaStream_t st, bool sgn = false, bool sq = false);
 
 // the batch in g_split_streams parts, each on its own stream with its own
 // workspace part, joined back into `st` with events
@@ -2030,7 +2061,7 @@ static bool g_verify = false;   // toom_set_verify: residue check of every unsig
 static bool g_check = false;    // toom_set_check: device exact-division checks
 
 static toom_status batched_core(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
-                                const toom_plan_t& p, cudaStream_t st, bool sgn);
+                                const toom_plan_t& p, cudaStream_t st, bool sgn, bool sq);
 
 static void launch_verify(const uint32_t* u, size_t nu, const uint32_t* v, size_t nv, const uint32_t* w, size_t batch,
                           cudaStream_t st) {
@@ -2040,8 +2071,8 @@ static void launch_verify(const uint32_t* u, size_t nu, const uint32_t* v, size_
 }
 
 static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
-                           const toom_plan_t& p, cudaStream_t st, bool sgn) {
-    toom_status s = batched_core(w, u, v, n, batch, p, st, sgn);
+                           const toom_plan_t& p, cudaStream_t st, bool sgn, bool sq) {
+    toom_status s = batched_core(w, u, v, n, batch, p, st, sgn, sq && u == v && !sgn);
     if (s == TOOM_OK && g_verify && !sgn && batch) {
         launch_verify(u, n, v, n, w, batch, st);
         if (cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
@@ -2050,7 +2081,7 @@ static toom_status batched(uint32_t* w, const uint32_t* u, const uint32_t* v, si
 }
 
 static toom_status batched_core(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch,
-                                const toom_plan_t& p, cudaStream_t st, bool sgn) {
+                                const toom_plan_t& p, cudaStream_t st, bool sgn, bool sq) {
     t_launches = 0;
     if (n == 0 || n > (1u << 30)) return TOOM_EINVAL;
     if (batch == 0) return TOOM_OK;
@@ -2062,13 +2093,13 @@ static toom_status batched_core(uint32_t* w, const uint32_t* u, const uint32_t* 
     size_t chunk = p.chunk ? p.chunk : batch;
     if (chunk > batch) chunk = batch;
     Plan plan;
-    if ((s = make_plan((int)n, chunk, p, plan, sgn))) return s;
+    if ((s = make_plan((int)n, chunk, p, plan, sgn, sq))) return s;
     plan.signed_in = sgn;
     if (sgn && plan.lv.size() > 1 && !plan.lv[0].lng) return TOOM_EUNSUPPORTED;   // signed top level: long path only
     // a large batch of short products (no long levels): halves on two streams,
     // so that the kernels of one half (different shared-memory / register
     // shapes) share the SMs with those of the other
-    if (!p.chunk && g_split_streams > 1 && batch >= 8192 && !plan.lv[0].lng && !t_prof && plan.lv.size() > 1)
+    if (!p.chunk && g_split_streams > 1 && batch >= 8192 && !plan.lv[0].lng && !t_prof && plan.lv.size() > 1 && !sq)
         return batched_split(w, u, v, n, batch, p, st, sgn);
     const size_t need = ws_need(plan, chunk, n);
     void* ws = nullptr;
@@ -2079,7 +2110,7 @@ static toom_status batched_core(uint32_t* w, const uint32_t* u, const uint32_t* 
         const size_t cnt = (batch - c0 < chunk) ? batch - c0 : chunk;
         if (cnt != chunk) {
             Plan p2;
-            if ((s = make_plan((int)n, cnt, p, p2, sgn))) return s;
+            if ((s = make_plan((int)n, cnt, p, p2, sgn, sq))) return s;
             p2.signed_in = sgn;
             if (sgn && p2.lv.size() > 1 && !p2.lv[0].lng) return TOOM_EUNSUPPORTED;
             if ((s = run_plan(p2, w + c0 * 2 * n, u + c0 * n, v + c0 * n, (int)n, cnt, (uint8_t*)ws, st))) return s;
@@ -2108,7 +2139,7 @@ static bool long_top_level(size_t n, size_t count, int B, Level& L) {
     L.npts = d.npts;
     L.b = (L.n + B - 1) / B;
     L.lentop = L.n - (B - 1) * L.b;
-    L.e = L.b + (bitlen(d.S) + 1 + 31) / 32;
+    L.e = L.b + d.grow;
     L.Lw = 2 * L.b + 1;
     L.lng = true;
     return true;
@@ -2133,6 +2164,7 @@ static toom_status run_long_standalone(size_t slot_limbs, size_t tiles, size_t n
     std::vector<LOpDev> ops;
     std::vector<LMultiDev> none;
     build((uint32_t*)base, ops);
+    if (lv_build_overflow()) { lv_build_overflow() = false; return TOOM_EUNSUPPORTED; }
     if (ops.size() > nops) return TOOM_EINVAL;
     if ((s = long_prepare(ops, none, ddesc, nullptr, status, tiles, ctr, nops, st))) return s;
     unsigned epoch = 1;
@@ -2160,6 +2192,7 @@ static toom_status run_long_call_standalone(size_t slot_limbs, size_t tiles, siz
     LBigDev* bdesc = (LBigDev*)(base + bS + bT + bC + bD + bM);
     LongCall lc;
     build((uint32_t*)base, lc);
+    if (lv_build_overflow()) { lv_build_overflow() = false; return TOOM_EUNSUPPORTED; }
     if (lc.up.size() > nops || lc.mup.size() > nops || lc.bup.size() > nops) return TOOM_EINVAL;
     if ((s = long_prepare(lc.up, lc.mup, ddesc, mdesc, status, tiles, ctr, nops, st, &lc.bup, bdesc))) return s;
     unsigned epoch = 1;
@@ -2259,16 +2292,22 @@ toom_status toom_mul_batched_plan(uint32_t* w, const uint32_t* u, const uint32_t
 
 toom_status toom_mul_batched(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t n, size_t batch, int B,
                              void* stream) {
-    if (B != 3 && B != 4 && B != 8 && B != 16) return fail(TOOM_EINVAL);
+    if (B != 3 && B != 4 && B != 8 && B != 16 && B != 32) return fail(TOOM_EINVAL);
     toom_plan_t p = toom_default_plan(B);
     return fail(batched(w, u, v, n, batch, p, (cudaStream_t)stream));
+}
+
+toom_status toom_sqr_batched(uint32_t* w, const uint32_t* u, size_t n, size_t batch, const toom_plan_t* plan,
+                             void* stream) {
+    if (!plan) return fail(TOOM_EINVAL);
+    return fail(batched(w, u, u, n, batch, *plan, (cudaStream_t)stream, false, true));
 }
 
 toom_status toom_mul(uint32_t* w, const uint32_t* u, size_t nu, const uint32_t* v, size_t nv, int B, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     t_launches = 0;
     if (!w || (nu && !u) || (nv && !v)) return fail(TOOM_EINVAL);
-    if (B != 3 && B != 4 && B != 8 && B != 16) return fail(TOOM_EINVAL);
+    if (B != 3 && B != 4 && B != 8 && B != 16 && B != 32) return fail(TOOM_EINVAL);
     if ((nu && overlaps(w, (nu + nv) * 4, u, nu * 4)) || (nv && overlaps(w, (nu + nv) * 4, v, nv * 4)))
         return fail(TOOM_EINVAL);
     toom_status s = check_device();
@@ -2279,7 +2318,7 @@ toom_status toom_mul(uint32_t* w, const uint32_t* u, size_t nu, const uint32_t* 
     }
     const size_t n = nu > nv ? nu : nv;
     toom_plan_t p = toom_default_plan(B);
-    if (nu == nv) return fail(batched(w, u, v, n, 1, p, st));   // w has exactly 2n limbs: no copies
+    if (nu == nv) return fail(batched(w, u, v, n, 1, p, st, false, u == v));   // w has 2n limbs: no copies; u == v squares
     // unbalanced: the shorter operand zero-padded to n limbs in
     // the call's workspace, behind the plan's own scratch; w has nu+nv < 2n
     // limbs, so the 2n-limb product also lives in the workspace and its low
@@ -2543,7 +2582,7 @@ size_t toom_eval_width(size_t n, int B) {
     const PSDesc d = ps_desc(B);
     if (!d.B || n == 0) return 0;
     const size_t b = (n + B - 1) / B;
-    return b + (bitlen(d.S) + 1 + 31) / 32;
+    return b + d.grow;
 }
 
 toom_status toom_eval_top(uint32_t* out, const uint32_t* a, size_t n, size_t batch, int B, void* stream) {

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
 // mad.wide.u32 per nonzero term); positions past every block (t >= b) carry
 // only the running carry.  Requires n, b multiples of 4.
 // ------------------------------------------------------------------------
-template <int B, int K>
+template <int B, int K, bool SQ = false>
 __device__ __forceinline__ void eval_top_v4_chunk(const uint32_t* __restrict__ Su, const uint32_t* __restrict__ Sv,
                                                   int lane, int t0, int tend, uint64_t& au, uint64_t& av,
                                                   uint32_t*& pu, uint32_t*& pv, size_t stride_limb) {
@@ -143,7 +143,7 @@ __device__ __forceinline__ void eval_top_v4_chunk(const uint32_t* __restrict__ S
             if (tg_evalc_cx<B>(K, j) != 0) {
                 const int off = (j * 32 + lane) * CH + 4 * (q ^ sw);
                 xu[j] = *reinterpret_cast<const uint4*>(Su + off);
-                xv[j] = *reinterpret_cast<const uint4*>(Sv + off);
+                if constexpr (!SQ) xv[j] = *reinterpret_cast<const uint4*>(Sv + off);
             }
         }
 #pragma unroll
@@ -155,16 +155,22 @@ __device__ __forceinline__ void eval_top_v4_chunk(const uint32_t* __restrict__ S
                 const long long cf = tg_evalc_cx<B>(K, j);
                 if (cf == 0) continue;
                 const uint32_t x = r == 0 ? xu[j].x : r == 1 ? xu[j].y : r == 2 ? xu[j].z : xu[j].w;
-                const uint32_t y = r == 0 ? xv[j].x : r == 1 ? xv[j].y : r == 2 ? xv[j].z : xv[j].w;
-                if (cf > 0) { lu = tg_madw((uint32_t)cf, x, lu); lv = tg_madw((uint32_t)cf, y, lv); }
-                else { lu = tg_msubw((uint32_t)(-cf), x, lu); lv = tg_msubw((uint32_t)(-cf), y, lv); }
+                if (cf > 0) lu = tg_madw((uint32_t)cf, x, lu);
+                else lu = tg_msubw((uint32_t)(-cf), x, lu);
+                if constexpr (!SQ) {
+                    const uint32_t y = r == 0 ? xv[j].x : r == 1 ? xv[j].y : r == 2 ? xv[j].z : xv[j].w;
+                    if (cf > 0) lv = tg_madw((uint32_t)cf, y, lv);
+                    else lv = tg_msubw((uint32_t)(-cf), y, lv);
+                }
             }
             *pu = (uint32_t)lu;
-            *pv = (uint32_t)lv;
             pu += stride_limb;
-            pv += stride_limb;
             au = (uint64_t)((int64_t)lu >> 32);
-            av = (uint64_t)((int64_t)lv >> 32);
+            if constexpr (!SQ) {
+                *pv = (uint32_t)lv;
+                pv += stride_limb;
+                av = (uint64_t)((int64_t)lv >> 32);
+            }
         }
     }
 }
@@ -172,7 +178,8 @@ __device__ __forceinline__ void eval_top_v4_chunk(const uint32_t* __restrict__ S
 #ifndef TG_EVAL_V4_MINB
 #define TG_EVAL_V4_MINB 4   // 72 registers, four CTAs per SM (1: 122 registers, 91 us on C2; 4: 75 us)
 #endif
-template <int B>
+// SQ: squaring (V = U): only u is staged and evaluated, V1 is not written
+template <int B, bool SQ = false>
 __global__ void __launch_bounds__(32 * (2 * B - 1), TG_EVAL_V4_MINB) k_eval_top_v4(
     const uint32_t* __restrict__ u, const uint32_t* __restrict__ v, uint32_t* __restrict__ U1,
     uint32_t* __restrict__ V1, size_t count, int n, int b, int e) {
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1), TG_EVAL_V4_MINB) k_eval_top_
     const int nin = (int)min((size_t)G, count - c0);
     const int lentop = n - (B - 1) * b;
     auto stage = [&](int buf, int t0) {
-        constexpr int NE = 2 * B * G * NQ;
+        constexpr int NE = (SQ ? 1 : 2) * B * G * NQ;
         for (int idx = threadIdx.x; idx < NE; idx += blockDim.x) {
             const int q = idx % NQ, i = (idx / NQ) % G, j = (idx / (NQ * G)) % B, op = idx / (NQ * G * B);
             const int t = t0 + 4 * q;
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1), TG_EVAL_V4_MINB) k_eval_top_
     };
     const size_t stride_limb = (size_t)NP * count;
     uint32_t* pu = U1 + (size_t)warp * count + c0 + lane;
-    uint32_t* pv = V1 + (size_t)warp * count + c0 + lane;
+    uint32_t* pv = SQ ? nullptr : V1 + (size_t)warp * count + c0 + lane;
     uint64_t au = 0, av = 0;
     const int tb = min(b, e);                 // staged positions; [tb, e) are carries only
     const int nch = (tb + CH - 1) / CH;
@@ -216,13 +223,13 @@ __global__ void __launch_bounds__(32 * (2 * B - 1), TG_EVAL_V4_MINB) k_eval_top_
             const uint32_t* Sv = &S[ci & 1][1][0][0][0];
             const int tend = min(t0 + CH, tb);
             switch (warp) {
-                case 0: eval_top_v4_chunk<B, 0>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
-                case 1: eval_top_v4_chunk<B, 1>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
-                case 2: eval_top_v4_chunk<B, 2>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
-                case 3: eval_top_v4_chunk<B, 3>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
-                case 4: eval_top_v4_chunk<B, 4>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
-                case 5: if constexpr (B >= 4) eval_top_v4_chunk<B, 5>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
-                default: if constexpr (B >= 4) eval_top_v4_chunk<B, 6>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 0: eval_top_v4_chunk<B, 0, SQ>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 1: eval_top_v4_chunk<B, 1, SQ>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 2: eval_top_v4_chunk<B, 2, SQ>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 3: eval_top_v4_chunk<B, 3, SQ>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 4: eval_top_v4_chunk<B, 4, SQ>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                case 5: if constexpr (B >= 4) eval_top_v4_chunk<B, 5, SQ>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
+                default: if constexpr (B >= 4) eval_top_v4_chunk<B, 6, SQ>(Su, Sv, lane, t0, tend, au, av, pu, pv, stride_limb); break;
             }
         }
         __syncthreads();
@@ -230,11 +237,13 @@ __global__ void __launch_bounds__(32 * (2 * B - 1), TG_EVAL_V4_MINB) k_eval_top_
     if (lane < nin) {
         for (int t = tb; t < e; ++t) {
             *pu = (uint32_t)au;
-            *pv = (uint32_t)av;
             pu += stride_limb;
-            pv += stride_limb;
             au = (uint64_t)((int64_t)au >> 32);
-            av = (uint64_t)((int64_t)av >> 32);
+            if constexpr (!SQ) {
+                *pv = (uint32_t)av;
+                pv += stride_limb;
+                av = (uint64_t)((int64_t)av >> 32);
+            }
         }
     }
 }
@@ -1028,7 +1037,7 @@ namespace tg {
 // (Eq. 1.3) runs one thread per (segment, product) with carry-in 0, and one
 // thread per product resolves the segment carries and adds them.
 // ------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_interp_rows_p8(const uint32_t* __restrict__ P1, uint32_t* __restrict__ W,
+__global__ void __launch_bounds__(128, 4) k_interp_rows_p8(const uint32_t* __restrict__ P1, uint32_t* __restrict__ W,
                                                          size_t count, int ywidth, int Lw) {
     constexpr int NP = 15;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1043,6 +1052,13 @@ __global__ void __launch_bounds__(128) k_interp_rows_p8(const uint32_t* __restri
     for (int k = 0; k < NP; ++k) {
         m[k] = tg_brow_m_P8[j][k];
         fill[k] = (__ldg(yb + (size_t)(ywidth - 1) * S + (size_t)k * count) >> 31) ? 0xFFFFFFFFu : 0u;
+    }
+    // exactness check: the window holds y_k mod 2^(32 window), a negative y_k
+    // adds -m_k 2^(32 window) to the dividend (csrc/check.cuh)
+    long long corr = 0;
+    if (tg_check_on) {
+#pragma unroll
+        for (int k = 0; k < NP; ++k) corr += m[k] * (long long)(fill[k] & 1u);
     }
     const uint32_t o1 = tg_brow_o1_P8[j], o2 = tg_brow_o2_P8[j], i1 = tg_brow_i1_P8[j], i2 = tg_brow_i2_P8[j];
     const int sh = tg_brow_s_P8[j], a = sh >> 5, r = sh & 31;
@@ -1090,9 +1106,7 @@ __global__ void __launch_bounds__(128) k_interp_rows_p8(const uint32_t* __restri
         // the tlast-limb window holds y_k mod 2^(32 tlast): negative y_k add
         // -m_k 2^(32 tlast) (csrc/check.cuh); the first quotient's own carry
         // past the window is then (acc - b1) / o1
-        long long ac = acc;
-#pragma unroll
-        for (int k = 0; k < NP; ++k) ac -= m[k] * (long long)(fill[k] & 1u);
+        const long long ac = acc - corr;
         tg_check_end((uint64_t)ac, b1, o1);
         if (o2 > 1) tg_check_end((uint64_t)((ac - (long long)b1) / (long long)o1), b2, o2);
     }

@@ -1237,7 +1237,10 @@ def emit_long_tables(ps: PointSet) -> str:
         assert W == conv, ps.name
     lines = [f"// long-vector tables for {ps.name} (csrc/longvec.cuh)"]
     nm = ps.name
-    lines.append(f"constexpr unsigned long long tg_growthS_{nm} = {_growth_S(ps)}ull;")
+    S = _growth_S(ps)
+    lines.append(f"constexpr unsigned long long tg_growthS_{nm} = {S if S < (1 << 64) else 0}ull;")
+    # limbs an evaluated operand grows by: e = b + ceil((bitlen(S) + 1) / 32)
+    lines.append(f"constexpr int tg_growthLimbs_{nm} = {(S.bit_length() + 1 + 31) // 32};")
     if ps.B <= 4:
         # combined interpolation + recomposition over the common denominator
         # (PAPER.md:162 matrix form, Eq. 1.3): Dc w = sum_j 2^(32 b j) sum_k A'_jk y_k
@@ -1552,7 +1555,10 @@ def generate_all():
         meta[ps.name] = dict(B=ps.B, points=ps.points, eval=stats(ev), interp=stats(it))
     parts.append(emit_bigrow_tables(pointset_paper(8)))
     parts.append(LONG_HEADER)
-    for ps in [pointset_T3(), pointset_T4(), pointset_paper(8), pointset_T16_31()]:
+    # P32: the paper's own points 0, +-2^j (j < 31) at B = 32 (PAPER.md:208,
+    # "64-bit ... allows B = 32"): divisors up to 2^60 run as
+    # 2-adic divisions by their 32-bit word factors on 32-bit limbs
+    for ps in [pointset_T3(), pointset_T4(), pointset_paper(8), pointset_T16_31(), pointset_paper(32)]:
         parts.append(emit_long_tables(ps))
     parts.append(emit_t16_matrix_tables())
     return "\n\n".join(parts) + "\n", meta

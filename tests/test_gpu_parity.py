@@ -568,3 +568,83 @@ def test_t16_matrix_form_equals_newton_program(n):
     want = oracle.schoolbook(u, v) if n <= 20011 else oracle.toom(u, v, top_B=16)
     for k, w in got.items():
         assert np.array_equal(w, want), k
+
+
+# ------------------------------------------------------------ squaring
+
+
+@pytest.mark.parametrize("B,n,kw,batch", [(4, 256, dict(t4=32, t3=32), 3000), (3, 96, dict(t4=10**9, t3=10**9), 260),
+                                          (8, 2048, {}, 64), (4, 1000, {}, 50), (3, 300, dict(t4=64, t3=64), 77),
+                                          (4, 250, dict(t4=32, t3=32), 99)])
+def test_squaring_batched(B, n, kw, batch):
+    """toom_sqr_batched (one evaluation per level, squaring base case) against
+    the oracle's schoolbook u*u, with all-ones and negative-point cases."""
+    rng = np.random.default_rng(n * 11 + B)
+    u = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    u[0] = 0xFFFFFFFF
+    u[1] = 0
+    u[2, 1::2] = 0xFFFFFFFF
+    u[2, ::2] = 0
+    w = host(tg.toom_sqr_batched(dev(u), B=B, **kw))
+    assert np.array_equal(w, oracle.schoolbook_batched(u, u))
+    # and the plain multiply of u by a copy of u agrees
+    w2 = run_batched(u, u.copy(), B, **kw)
+    assert np.array_equal(w, w2)
+
+
+@pytest.mark.parametrize("B,n", [(4, 20000), (16, 9000), (4, 4100)])
+def test_squaring_long_path(B, n):
+    """toom_mul(a, a): the long-vector and instance-resident levels evaluate
+    once; result equal to the schoolbook square."""
+    rng = np.random.default_rng(n + B)
+    a = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    a[: n // 4] = 0xFFFFFFFF
+    da = dev(a)
+    w = host(tg.toom_mul(da, da, B=B))
+    assert np.array_equal(w, oracle.schoolbook(a, a))
+
+
+def test_squaring_c3_square_classes():
+    """C3's all-ones and alternating quarters are squares (u = v): the
+    squaring path gives their closed forms."""
+    u, _ = synth.config_inputs(3)
+    sub = np.concatenate([u[0:64], u[1024:1088]])
+    w = host(tg.toom_sqr_batched(dev(sub), B=8))
+    N = 65536
+    ones = synth.from_int((1 << (2 * N)) - (1 << (N + 1)) + 1, 4096)
+    assert (w[:64] == ones[None, :]).all()
+    alt = synth.to_int(u[1024])
+    assert (w[64:] == synth.from_int(alt * alt, 4096)[None, :]).all()
+
+
+# ------------------------------------------------------------ B = 32 (SURVEY §8(f)3)
+
+
+@pytest.mark.parametrize("n", [700, 5000, 40000])
+def test_b32_paper_points_long_path(n):
+    """B = 32 with the paper's points 0, +-2^j, j < 31 (the
+    64-bit CPU code allows B = 32): divisors up to 2^60 run as 2-adic divisions
+    by their 32-bit word factors on 32-bit limbs.  Bit-exact against the
+    schoolbook, including all-ones operands (long carry chains)."""
+    rng = np.random.default_rng(n)
+    a = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    info = tg.plan_describe(n, 1, B=32)
+    assert info["levels"][0]["B"] == 32 and info["levels"][0]["npts"] == 63 and info["levels"][0]["long"]
+    w = host(tg.toom_mul(dev(a), dev(b), B=32))
+    assert np.array_equal(w, oracle.schoolbook(a, b))
+    ones = np.full(n, 0xFFFFFFFF, np.uint32)
+    w = host(tg.toom_mul(dev(ones), dev(b), B=32))
+    assert np.array_equal(w, oracle.schoolbook(ones, b))
+
+
+def test_b32_stage_exports():
+    n = 3000
+    rng = np.random.default_rng(32)
+    u = rng.integers(0, 2**32, (1, n), dtype=np.uint64).astype(np.uint32)
+    v = rng.integers(0, 2**32, (1, n), dtype=np.uint64).astype(np.uint32)
+    U, V = tg.eval_points(dev(u), 32), tg.eval_points(dev(v), 32)
+    assert U.shape[0] == 63
+    Y = tg.mul_signed_batched(U[:, 0].contiguous(), V[:, 0].contiguous(), B=4)
+    w = host(tg.interp_recompose(Y.view(63, 1, -1).contiguous(), n, 32))
+    assert np.array_equal(w[0], oracle.schoolbook(u[0], v[0]))
