@@ -103,6 +103,17 @@ toom_status toom_sqr_batched(uint32_t *w, const uint32_t *u, size_t n, size_t ba
 toom_status toom_mul(uint32_t *w, const uint32_t *u, size_t nu, const uint32_t *v, size_t nv,
                      int B, void *stream);
 
+/* Toom as a top-level wrapper over a different inner multiplier (PAPER.md
+ * §5, :188-196: Toom-Cook "as a top-level threading wrapper" around GMP's FFT;
+ * SURVEY.md §8(f)4).  w[0 .. nu+nv) = u * v (device pointers, nu, nv >= 1):
+ * B in {3, 4, 8, 16, 32}: the Toom-B top level on the long-vector kernels
+ * (evaluation at the 2B-1 points, interpolation, recomposition), its 2B-1
+ * pointwise products by an exact number-theoretic transform over the prime
+ * p = 2^64 - 2^32 + 1 (16-bit digits; every convolution coefficient < 2^53 < p);
+ * B = 0: the NTT product alone.  Errors as toom_mul.                        */
+toom_status toom_mul_ntt(uint32_t *w, const uint32_t *u, size_t nu, const uint32_t *v, size_t nv, int B,
+                         void *stream);
+
 /* End-to-end variant with HOST buffers (pinned or pageable): copies u, v to
  * the device, multiplies, copies w back, and synchronizes `stream` before
  * returning.  Layouts as toom_mul_batched.                                 */

@@ -70,6 +70,7 @@ SIGNATURES = {
     "toom_mul_signed_batched": (_I, [_P, _P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
     "toom_product_width_point": (_SZ, [_SZ, _I]),
     "toom_set_check": (None, [_I]),
+    "toom_mul_ntt": (_I, [_P, _P, _SZ, _P, _SZ, _I, _P]),
     "toom_sqr_batched": (_I, [_P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
     "toom_set_t16_matrix": (None, [_I]),
     "toom_set_verify": (None, [_I]),
@@ -343,3 +344,17 @@ def set_t16_matrix(on: bool = True):
     """Toom-16 top-level interpolation: matrix form (default) or the staged
     Newton program."""
     lib().toom_set_t16_matrix(1 if on else 0)
+
+
+def toom_mul_ntt(u: torch.Tensor, v: torch.Tensor, B: int = 16, out: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+    """Toom-B top level with its 2B-1 products by the NTT inner multiplier
+    (B = 0: the NTT product alone); 1-D uint32 CUDA tensors, nu + nv limbs."""
+    if u.dim() != 1 or v.dim() != 1 or u.dtype != v.dtype:
+        raise ValueError("u and v must be 1-D tensors of one dtype")
+    nu, nv = u.numel(), v.numel()
+    if out is None:
+        out = torch.empty(nu + nv, dtype=u.dtype, device=u.device)
+    _check(lib().toom_mul_ntt(_out(out, "out", (nu + nv,), u), _dev(u, "u"), nu, _dev(v, "v"), nv, B,
+                              _stream(stream)), "toom_mul_ntt")
+    return out

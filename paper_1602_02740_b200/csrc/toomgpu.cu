@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 #include "longvec.cuh"
 #include "longvec2.cuh"
 #include "level34.cuh"
+#include "ntt.cuh"
 #include "toplevel.cuh"
 namespace tg {
 
@@ -2209,6 +2210,129 @@ static toom_status run_long_call_standalone(size_t slot_limbs, size_t tiles, siz
     return TOOM_OK;
 }
 
+// ---- NTT inner multiplier (ntt.cuh) ----------------------
+struct NttTables {
+    int N = 0;
+    uint64_t* tw = nullptr;    // omega^k, k < N/2
+    uint64_t* twi = nullptr;   // omega^-k
+    uint64_t ninv = 0;
+};
+static std::mutex g_ntt_mu;
+static std::vector<NttTables> g_ntt_tables;
+
+static toom_status ntt_tables(int N, NttTables& out) {
+    std::lock_guard<std::mutex> g(g_ntt_mu);
+    for (auto& t : g_ntt_tables)
+        if (t.N == N) { out = t; return TOOM_OK; }
+    NttTables t;
+    t.N = N;
+    const uint64_t w = gl_pow(NTT_G, (NTT_P - 1) / (uint64_t)N), wi = gl_pow(w, NTT_P - 2);
+    std::vector<uint64_t> h((size_t)N / 2), hi((size_t)N / 2);
+    uint64_t x = 1, y = 1;
+    for (int k = 0; k < N / 2; ++k) { h[k] = x; hi[k] = y; x = gl_mul(x, w); y = gl_mul(y, wi); }
+    if (cudaMalloc(&t.tw, (size_t)N / 2 * 8) != cudaSuccess || cudaMalloc(&t.twi, (size_t)N / 2 * 8) != cudaSuccess) {
+        cudaGetLastError();
+        return TOOM_ENOMEM;
+    }
+    cudaMemcpy(t.tw, h.data(), (size_t)N / 2 * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.twi, hi.data(), (size_t)N / 2 * 8, cudaMemcpyHostToDevice);
+    t.ninv = gl_pow((uint64_t)N, NTT_P - 2);
+    g_ntt_tables.push_back(t);
+    out = t;
+    return TOOM_OK;
+}
+
+static int ntt_size(int e) {
+    int N = NTT_SB;
+    while (N < 4 * e) N <<= 1;
+    return N;
+}
+// workspace of ntt_products: digit arrays A, B ([count][N] u64), lowest-nonzero
+// indices, the carry op's tile records / counters / descriptor
+static size_t ntt_ws_bytes(int e, int count) {
+    const size_t N = (size_t)ntt_size(e);
+    const size_t tiles = long_tiles((size_t)count, 2 * e);
+    return 2 * N * count * 8 + 3 * 256 + (size_t)count * 16 + tiles * sizeof(LStatus) + 256 + sizeof(LOpDev) + 1024;
+}
+
+// Y[c] = U[c] * V[c] (two's complement, e limbs each -> 2e limbs) for c < count,
+// through the exact NTT over p = 2^64 - 2^32 + 1 (magnitudes, sign applied)
+static toom_status ntt_products(uint32_t* Y, long long y_is, const uint32_t* U, long long u_is, const uint32_t* V,
+                                long long v_is, int e, int count, uint8_t* ws, cudaStream_t st, bool sgn = true) {
+    if (count == 0) return TOOM_OK;
+    const int N = ntt_size(e);
+    NttTables T;
+    toom_status s;
+    if ((s = ntt_tables(N, T))) return s;
+    auto rnd = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    uint64_t* A = (uint64_t*)ws;
+    uint64_t* Bv = A + (size_t)N * count;
+    uint8_t* p = ws + 2 * (size_t)N * count * 8;
+    int* zu = (int*)p;
+    int* zv = zu + count;
+    int* zw = zv + count;
+    p += rnd((size_t)count * 12);
+    LStatus* status = (LStatus*)p;
+    const size_t tiles = long_tiles((size_t)count, 2 * e);
+    p += rnd(tiles * sizeof(LStatus));
+    unsigned* ctr = (unsigned*)p;
+    p += 256;
+    LOpDev* desc = (LOpDev*)p;
+    cudaMemsetAsync(zu, 0x7F, (size_t)count * 12, st);
+    const dim3 gz((unsigned)std::min(64, (e + 255) / 256), (unsigned)count);
+    k_ntt_lowest_nz<<<gz, 256, 0, st>>>(U, u_is, e, zu);
+    k_ntt_lowest_nz<<<gz, 256, 0, st>>>(V, v_is, e, zv);
+    const dim3 gd((unsigned)std::min(1024, N / 256), (unsigned)count);
+    k_ntt_digits<<<gd, 256, 0, st>>>(U, u_is, e, sgn ? 1 : 0, zu, A, N);
+    k_ntt_digits<<<gd, 256, 0, st>>>(V, v_is, e, sgn ? 1 : 0, zv, Bv, N);
+    t_launches += 4;
+    const dim3 gs((unsigned)std::min(2048, N / 2 / 256), (unsigned)count), gt((unsigned)(N / NTT_SB), (unsigned)count);
+    const dim3 g8((unsigned)std::min(2048, std::max(1, N / 8 / 256)), (unsigned)count);
+    for (uint64_t* X : {A, Bv}) {
+        // global stages three at a time (radix 8), the rest radix 2, then the
+        // stages below NTT_SB in shared memory
+        int h = N / 2;
+        for (; h / 4 >= NTT_SB; h /= 8) { k_ntt_r8<false><<<g8, 256, 0, st>>>(X, N, h / 4, T.tw); ++t_launches; }
+        for (; h >= NTT_SB; h >>= 1) { k_ntt_dif_stage<<<gs, 256, 0, st>>>(X, N, h, T.tw); ++t_launches; }
+        k_ntt_dif_tail<<<gt, 512, 0, st>>>(X, N, T.tw);
+        ++t_launches;
+    }
+    k_ntt_pointwise<<<2048, 256, 0, st>>>(A, Bv, (long long)N * count, T.ninv);
+    k_ntt_dit_head<<<gt, 512, 0, st>>>(A, N, T.twi);
+    t_launches += 2;
+    {
+        int h = NTT_SB;
+        const int nglob = [&] { int k = 0; for (int x = NTT_SB; x < N; x <<= 1) ++k; return k; }();
+        for (int r = 0; r < nglob % 3; ++r, h <<= 1) { k_ntt_dit_stage<<<gs, 256, 0, st>>>(A, N, h, T.twi); ++t_launches; }
+        for (; h < N; h <<= 3) { k_ntt_r8<true><<<g8, 256, 0, st>>>(A, N, h, T.twi); ++t_launches; }
+    }
+    // w = sum_k c_k 2^(16 k), c_k = lo_k + hi_k 2^32 < 2^53: four strided word
+    // slices of the coefficient array (lo/hi of the even / odd digits)
+    {
+        const uint32_t* X = (const uint32_t*)A;
+        LOpBuilder b(Y, y_is, 1, 2 * e, count);
+        const long long is = 2ll * N;
+        b.add(LVec{X + 0, is, 4, N / 2, 0}, 1, 0);
+        b.add(LVec{X + 2, is, 4, N / 2, 0}, 1, 16);
+        b.add(LVec{X + 1, is, 4, N / 2, 0}, 1, 32);
+        b.add(LVec{X + 3, is, 4, N / 2, 0}, 1, 48);
+        b.op.wide = 0;
+        std::vector<LOpDev> ops(1, b.op);
+        std::vector<LMultiDev> none;
+        if ((s = long_prepare(ops, none, desc, nullptr, status, tiles, ctr, 1, st))) return s;
+        unsigned epoch = 1;
+        if ((s = launch_long_ops(ops, 0, desc, status, ctr, epoch, CAT_BASE, st))) return s;
+    }
+    // the sign: negate the products of operands of different signs
+    const dim3 gw((unsigned)std::min(64, (2 * e + 255) / 256), (unsigned)count);
+    if (sgn) {
+        k_ntt_lowest_nz<<<gw, 256, 0, st>>>(Y, y_is, 2 * e, zw);
+        k_ntt_negate<<<gw, 256, 0, st>>>(Y, y_is, 2 * e, U, u_is, e, V, v_is, e, zw);
+        t_launches += 2;
+    }
+    return cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA;
+}
+
 }  // namespace tg
 
 using namespace tg;
@@ -2272,6 +2396,79 @@ toom_status toom_interp_recompose(uint32_t* w, const uint32_t* y, size_t n, size
                             (cudaStream_t)stream);
     if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
     return fail(s);
+}
+
+toom_status toom_mul_ntt(uint32_t* w, const uint32_t* u, size_t nu, const uint32_t* v, size_t nv, int B, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    t_launches = 0;
+    if (!w || !u || !v || nu == 0 || nv == 0 || nu > (1u << 28) || nv > (1u << 28)) return fail(TOOM_EINVAL);
+    if (overlaps(w, (nu + nv) * 4, u, nu * 4) || overlaps(w, (nu + nv) * 4, v, nv * 4)) return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    const size_t n = std::max(nu, nv);
+    auto rnd = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    if (B == 0) {   // the inner multiplier alone: one product of n-limb (zero-padded) operands
+        const size_t e = n;       // unsigned operands (no sign handling)
+        const size_t bU = rnd(e * 4), bY = rnd(2 * e * 4), bN = rnd(ntt_ws_bytes((int)e, 1));
+        void* ws = nullptr;
+        WsGuard wg;
+        if ((s = get_ws(2 * bU + bY + bN, &ws, st))) return fail(s);
+        wg.on = true;
+        uint32_t* pu = (uint32_t*)ws;
+        uint32_t* pv = (uint32_t*)((uint8_t*)ws + bU);
+        uint32_t* py = (uint32_t*)((uint8_t*)ws + 2 * bU);
+        k_pad_copy<<<nblk(e, 256), 256, 0, st>>>(u, nu, pu, e);
+        k_pad_copy<<<nblk(e, 256), 256, 0, st>>>(v, nv, pv, e);
+        if ((s = ntt_products(py, 2 * e, pu, e, pv, e, (int)e, 1, (uint8_t*)ws + 2 * bU + bY, st, false))) return fail(s);
+        k_pad_copy<<<nblk(nu + nv, 256), 256, 0, st>>>(py, nu + nv, w, nu + nv);
+        t_launches += 3;
+        return fail(cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA);
+    }
+    // Toom-B top level on the long-vector kernels, its 2B-1 products by the NTT
+    Level L;
+    if (!long_top_level(n, 1, B, L)) return fail(TOOM_EINVAL);
+    const size_t np = (size_t)L.npts, e = (size_t)L.e;
+    LongTables T;
+    long_tables(B, T);
+    const int Wt = long_Wt(L);
+    // scratch of the stage calls (the larger of evaluation and interpolation)
+    const size_t stage = rnd((size_t)long_nslots(B, T.nslots) * Wt * 4) +
+                         rnd(long_tiles(1, std::max(Wt, 2 * L.n)) * (size_t)L.npts * sizeof(LStatus)) +
+                         rnd(4096 * 4) + rnd(4096 * sizeof(LOpDev)) + rnd(64 * sizeof(LMultiDev)) +
+                         rnd(64 * sizeof(LBigDev)) + (1 << 20);
+    const size_t bP = rnd(n * 4), bE = rnd(np * e * 4), bY = rnd(np * 2 * e * 4), bN = rnd(ntt_ws_bytes((int)e, (int)np));
+    void* ws = nullptr;
+    WsGuard wg;
+    if ((s = get_ws(2 * bP + 2 * bE + bY + std::max(bN, stage) + rnd(2 * n * 4), &ws, st))) return fail(s);
+    wg.on = true;
+    uint8_t* p = (uint8_t*)ws;
+    uint32_t* pu = (uint32_t*)p; p += bP;
+    uint32_t* pv = (uint32_t*)p; p += bP;
+    uint32_t* EU = (uint32_t*)p; p += bE;
+    uint32_t* EV = (uint32_t*)p; p += bE;
+    uint32_t* Yp = (uint32_t*)p; p += bY;
+    uint32_t* pw = (uint32_t*)p; p += rnd(2 * n * 4);
+    uint8_t* scratch = p;
+    k_pad_copy<<<nblk(n, 256), 256, 0, st>>>(u, nu, pu, n);
+    k_pad_copy<<<nblk(n, 256), 256, 0, st>>>(v, nv, pv, n);
+    size_t launches = 2;
+    // the stage exports run with the scratch region as their workspace
+    t_ws_override = scratch;
+    t_ws_override_bytes = std::max(bN, stage);
+    s = toom_eval_points(EU, pu, n, 1, B, 0, stream);
+    launches += t_launches;
+    if (!s) { s = toom_eval_points(EV, pv, n, 1, B, 0, stream); launches += t_launches; }
+    t_launches = 0;
+    if (!s) s = ntt_products(Yp, 2 * e, EU, e, EV, e, (int)e, (int)np, scratch, st);
+    launches += t_launches;
+    if (!s) { s = toom_interp_recompose(pw, Yp, n, 1, B, stream); launches += t_launches; }
+    t_ws_override = nullptr;
+    t_ws_override_bytes = 0;
+    if (s) return fail(s);
+    k_pad_copy<<<nblk(nu + nv, 256), 256, 0, st>>>(pw, nu + nv, w, nu + nv);
+    t_launches = launches + 1;
+    if (g_verify) launch_verify(u, nu, v, nv, w, 1, st);
+    return fail(cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA);
 }
 
 toom_plan_t toom_default_plan(int B) {

@@ -648,3 +648,30 @@ def test_b32_stage_exports():
     Y = tg.mul_signed_batched(U[:, 0].contiguous(), V[:, 0].contiguous(), B=4)
     w = host(tg.interp_recompose(Y.view(63, 1, -1).contiguous(), n, 32))
     assert np.array_equal(w[0], oracle.schoolbook(u[0], v[0]))
+
+
+# ------------------------------------------------------------ NTT inner multiplier (§5)
+
+
+@pytest.mark.parametrize("nu,nv", [(700, 700), (5000, 3001), (1 << 15, 1 << 15)])
+def test_ntt_inner_multiplier(nu, nv):
+    rng = np.random.default_rng(nu + nv)
+    a = rng.integers(0, 2**32, nu, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 2**32, nv, dtype=np.uint64).astype(np.uint32)
+    a[: nu // 5] = 0xFFFFFFFF
+    w = host(tg.toom_mul_ntt(dev(a), dev(b), B=0))
+    assert np.array_equal(w, oracle.schoolbook(a, b))
+
+
+@pytest.mark.parametrize("B,n", [(16, 20011), (4, 9000), (3, 5000), (16, 1 << 16)])
+def test_toom_wrapper_over_ntt(B, n):
+    """Toom-B top level (long path) with its 2B-1 signed pointwise products by
+    the NTT: bit-exact against the oracle."""
+    seed = synth.seed_for(5)
+    u = synth.uniform_limbs(seed, 31, 1, 0, n)[0]
+    v = synth.uniform_limbs(seed, 31, 1, 1, n)[0]
+    v[n // 2:] = 0xFFFFFFFF
+    w = host(tg.toom_mul_ntt(dev(u), dev(v), B=B))
+    want = oracle.schoolbook(u, v) if n <= 20011 else oracle.toom(u, v, top_B=16)
+    assert np.array_equal(w, want)
+    check_residues(u, v, w)
