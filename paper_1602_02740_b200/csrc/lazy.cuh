@@ -1,0 +1,256 @@
+// Lazy Toom-3/4 levels: the levels of a single large product (C4, and the
+// Toom-4 levels under C5's Toom-16 top) from the top down to the fused bottom
+// level, run without any carry propagation or division on the way.
+//
+// A lazy vector of W positions is two uint32 arrays LO, HI with
+//     value = sum_p (LO[p] + HI[p]) 2^(32 p),   LO unsigned, HI signed (small),
+// i.e. position p holds v_p = LO[p] + HI[p] with |v_p| < 2^33.  Every step of
+// the method on these levels is linear in its inputs:
+//   a2 evaluation   U(x_k)[t] = sum_j c_kj u_j[t]          (Eq. 1.1, 4.1)
+//   a4+a5           Dc w = sum_j 2^(32 b j) N_j,  N_j = sum_k c'_jk y_k
+//                   (the even-odd + listing program composed over the common
+//                   denominator Dc = lcm D_j; DESIGN reading 12)
+// so each is one elementwise pass: position p of the output is a linear form
+// lin_p of input positions, stored as LO = lin_p mod 2^32 at p and
+// HI = floor(lin_p / 2^32) at p + 1 (the carry is kept, not propagated).  The
+// exact divisions are deferred: the products coming up from a lazy level carry
+// the factor Dc of every lazy level below, and the division by
+// prod Dc = 2^s o1 o2 .. (word factors) plus the carry propagation runs once at
+// the top of the lazy block (k_lz_fin, the two-pass scan of longvec2.cuh).
+// The deepest lazy level writes carry-normalised children (k_lz_eval_last),
+// the input of the fused bottom level.
+//
+// Layout: every lazy family is INTERLEAVED, position p of row R at p*rows + R
+// (row R = k*count + c for child k of parent c), and every kernel maps its
+// linear thread index to (position, row) with the row fastest, so that all
+// reads and writes of a warp are contiguous for any count (count = 1 is the
+// row-major single product).
+//
+// Bounds: |v_p| < 2^32 + 2^31 on every lazy vector (|HI| < 2^17 below), the
+// evaluation forms are < 15 * 2^33 < 2^37, the interpolation forms
+// < 3 * 2520 * 2^33 < 2^47 (T4: row sums of |c'_jk| <= 2520): int64 throughout.
+#pragma once
+
+namespace tg {
+
+// a family of vectors of n positions: position p of row r at r*is + p*ps
+struct LzSrc {
+    const uint32_t* lo;   // normalised limbs, or the LO array of a lazy family
+    const uint32_t* hi;   // nullptr: normalised (two's complement if sgn)
+    long long is, ps;     // row and position strides
+    int n;                // positions per row
+    int sgn;              // normalised rows: top limb signed
+};
+
+__device__ __forceinline__ long long lz_get(const LzSrc& S, long long row, int p) {
+    if (p >= S.n) return 0;
+    const long long o = row * S.is + (long long)p * S.ps;
+    const uint32_t x = __ldg(S.lo + o);
+    if (S.hi) return (long long)x + (long long)(int)__ldg(S.hi + o);
+    return (S.sgn && p == S.n - 1) ? (long long)(int)x : (long long)x;
+}
+
+template <int B>
+__device__ __forceinline__ constexpr long long lz_evalc(int k, int j) {
+    if constexpr (B == 3) return tg_evalc_cx_T3(k, j);
+    else return tg_evalc_cx_T4(k, j);
+}
+template <int B>
+__device__ __forceinline__ constexpr long long lz_comb(int j, int k) {
+    if constexpr (B == 3) return tg_combA_cx_T3(j, k);
+    else return tg_combA_cx_T4(j, k);
+}
+
+// ---- a2: evaluation of one lazy level -------------------------------------
+// child k of parent c at position t: lin = sum_j c_kj par_j[t], block j =
+// parent positions [j b, j b + len_j); written to the interleaved lazy family
+// (rows NP*count, e positions).  Thread g = t*count + c (blockIdx.y: operand).
+template <int B>
+__global__ void __launch_bounds__(256) k_lz_eval(LzSrc pu, LzSrc pv, uint32_t* __restrict__ ulo, uint32_t* __restrict__ uhi,
+                                                 uint32_t* __restrict__ vlo, uint32_t* __restrict__ vhi, long long count,
+                                                 int b, int lentop, int e) {
+    constexpr int NP = 2 * B - 1;
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long t = g / count;
+    if (t >= e) return;
+    const long long c = g - t * count;
+    const LzSrc& S = blockIdx.y ? pv : pu;
+    uint32_t* lo = blockIdx.y ? vlo : ulo;
+    uint32_t* hi = blockIdx.y ? vhi : uhi;
+    long long x[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+        const int len = (j == B - 1) ? lentop : b;
+        x[j] = t < len ? lz_get(S, c, j * b + (int)t) : 0ll;
+    }
+    const long long rows = NP * count;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        long long lin = 0;
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            const long long m = lz_evalc<B>(k, j);
+            if (m == 1) lin += x[j];
+            else if (m == -1) lin -= x[j];
+            else if (m != 0) lin += m * x[j];
+        }
+        const long long R = k * count + c;
+        lo[t * rows + R] = (uint32_t)lin;
+        if (t + 1 < e) hi[(t + 1) * rows + R] = (uint32_t)(int)(lin >> 32);
+        if (t == 0) hi[R] = 0u;
+    }
+}
+
+// ---- a2 of the deepest lazy level: evaluation + carry normalisation --------
+// One thread per (parent, operand): the 2B-1 children position by position,
+// each with its own carry chain, written as e two's-complement limbs to the
+// interleaved family [e][NP*count] (the fused bottom level's MODE 0 input).
+template <int B>
+__global__ void __launch_bounds__(128) k_lz_eval_last(LzSrc pu, LzSrc pv, uint32_t* __restrict__ du,
+                                                      uint32_t* __restrict__ dv, long long count, int b, int lentop,
+                                                      int e) {
+    constexpr int NP = 2 * B - 1;
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    const LzSrc& S = blockIdx.y ? pv : pu;
+    uint32_t* dst = (blockIdx.y ? dv : du) + c;
+    const long long rows = NP * count;
+    long long cy[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) cy[k] = 0;
+#pragma unroll 1
+    for (int t = 0; t < e; ++t) {
+        long long x[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            const int len = (j == B - 1) ? lentop : b;
+            x[j] = t < len ? lz_get(S, c, j * b + t) : 0ll;
+        }
+        uint32_t* d = dst + (long long)t * rows;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            long long lin = cy[k];
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                const long long m = lz_evalc<B>(k, j);
+                if (m == 1) lin += x[j];
+                else if (m == -1) lin -= x[j];
+                else if (m != 0) lin += m * x[j];
+            }
+            d[k * count] = (uint32_t)lin;
+            cy[k] = lin >> 32;
+        }
+    }
+}
+
+// ---- a4 + a5: interpolation and recomposition of one lazy level ------------
+// X = Dc w = sum_j 2^(32 b j) N_j, N_j = sum_k c'_jk y_k; position P = s b + r
+// receives N_{s-m}[m b + r] for every segment m of the products.  Thread
+// g = r*count + c, r in [0, b): it reads y_k[m b + r] once for all m, k and
+// writes the positions s b + r of the interleaved lazy output [Wx][count].
+// Products of point k of parent c: row k*count + c of `y`.
+template <int B, int MM>
+__global__ void __launch_bounds__(256) k_lz_interp(LzSrc y, uint32_t* __restrict__ xlo, uint32_t* __restrict__ xhi,
+                                                   long long count, int b, int Wx) {
+    constexpr int NP = 2 * B - 1;
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long rr = g / count;
+    if (rr >= b) return;
+    const int r = (int)rr;
+    const long long c = g - rr * count;
+    long long X[NP + MM - 1];
+#pragma unroll
+    for (int s = 0; s < NP + MM - 1; ++s) X[s] = 0;
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+        const int p = m * b + r;
+        long long yk[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) yk[k] = lz_get(y, (long long)k * count + c, p);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            long long s = 0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const long long a = lz_comb<B>(j, k);
+                if (a != 0) s += a * yk[k];
+            }
+            X[j + m] += s;
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < NP + MM - 1; ++s) {
+        const int P = s * b + r;
+        if (P >= Wx) break;
+        xlo[(long long)P * count + c] = (uint32_t)X[s];
+        if (P + 1 < Wx) xhi[(long long)(P + 1) * count + c] = (uint32_t)(int)(X[s] >> 32);
+        if (P == 0) xhi[c] = 0u;
+    }
+}
+
+// ---- normalisation + the deferred exact division (two-pass scan) ----------
+// dst row c (Wout limbs, two's complement) = ((sum_p v_p 2^(32p)) / o) >> (32 sa + sr)
+struct LzFin {
+    LzSrc x;                   // lazy rows (or normalised)
+    uint32_t* dst;
+    long long dst_is;
+    int Wout, tpi;
+    long long rows;
+    uint32_t o, oinv, p32, Mch, mi;
+    int sa, sr;
+};
+
+template <int CH>
+__global__ void __launch_bounds__(LV_NT, 3) k_lz_fin(LzFin F, LTile* __restrict__ tiles, int phase) {
+    __shared__ L2Smem s_sh;
+    extern __shared__ uint32_t Q[];
+    const int tid = threadIdx.x, NT = blockDim.x, TL = NT * CH;
+    // blocks position-major (the rows of one position range run together:
+    // interleaved inputs share their sectors); tile records row-major
+    const long long kt = blockIdx.x / F.rows;
+    const long long inst = blockIdx.x - kt * F.rows;
+    const unsigned tile = (unsigned)(inst * F.tpi + kt);
+    const int tstart = (int)kt * TL;
+    long long lin[CH];
+    // reads at positions tstart + tid + q NT, transposed through smem to CH
+    // consecutive positions per thread (two 32-bit halves)
+    {
+        const int NP1 = NT + 1;
+        uint32_t* Sx = Q + lv2_qwords(TL, CH);
+        long long xv[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) xv[q] = lz_get(F.x, inst, tstart + tid + q * NT);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int pos = tid + q * NT;
+                Sx[(pos % CH) * NP1 + pos / CH] = h ? (uint32_t)(xv[q] >> 32) : (uint32_t)xv[q];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const uint32_t w = Sx[q * NP1 + tid];
+                if (h) lin[q] += (long long)(int)w << 32;
+                else lin[q] = (long long)w;
+            }
+        }
+        __syncthreads();
+    }
+    const LMod M{F.o, F.o > 1 ? ~0ull / F.o : 0ull};
+    lv2_tile<long long, CH>(lin, M,
+                            LFinish{F.oinv, F.p32, F.Mch, F.mi, F.sa, F.sr, F.Wout, reinterpret_cast<LStatus*>(tiles), 1,
+                                    F.dst + inst * F.dst_is, 1},
+                            tile, tstart, s_sh, Q,
+                            [&](long long (&hl)[LV_MAXHALO]) {
+#pragma unroll
+                                for (int h = 0; h < LV_MAXHALO; ++h) hl[h] = lz_get(F.x, inst, tstart + TL + h);
+                            },
+                            phase);
+}
+inline size_t lz_fin_smem(int nthreads, int ch) {
+    return 4 * ((size_t)lv2_qwords(nthreads * ch, ch) + (size_t)ch * (nthreads + 1));
+}
+
+}  // namespace tg

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 #include "longvec2.cuh"
 #include "level34.cuh"
 #include "ntt.cuh"
+#include "lazy.cuh"
 #include "toplevel.cuh"
 namespace tg {
 
@@ -394,7 +395,10 @@ struct Level {
     int npts = 0;
     bool lng = false;   // long-vector (limb-parallel) level: row-major child layouts
     bool res = false;   // ... run instance-resident (one CTA per instance, level34.cuh)
+    bool lazy = false;  // ... run lazy (csrc/lazy.cuh): carry-save values, deferred division
+    int Wy = 0, Wx = 0; // lazy: positions of the child products read / of the product written
     size_t offU = 0, offV = 0, offP = 0, offW = 0;   // child operands/products, this level's scratch
+    size_t offLzU = 0, offLzV = 0, offLzP = 0;        // lazy children (LO | HI) and lazy child products
 };
 
 struct Plan {
@@ -414,6 +418,13 @@ struct Plan {
     size_t offEDesc = 0;     // multi-output evaluation descriptors
     size_t offBDesc = 0;     // wide-multiplier multi-output descriptors (matrix-form T16)
     bool top_warp = false;   // top interpolation one warp per product (fused level writes row-major)
+    // lazy block [lz0, lz1) of long levels (csrc/lazy.cuh): the product of
+    // their common denominators 2^lz_s lz_o, the top lazy output X and the
+    // two-pass tile records of the finishing scans
+    int lz0 = -1, lz1 = -1;
+    std::vector<uint32_t> lz_o;   // odd part of prod Dc as word factors (one finishing division each)
+    int lz_s = 0;
+    size_t offLzX = 0, offLzT = 0, offLzTiles = 0, nLzTiles = 0;
 };
 
 // generated long-vector tables of a point set
@@ -505,6 +516,13 @@ static bool g_res_on = [] {
     return e ? atoi(e) != 0 : true;
 }();
 
+// lazy long levels (csrc/lazy.cuh); TOOM_LAZY=0 runs them on the two-pass
+// long-op executor instead (tests compare both)
+static int g_lazy = [] {
+    const char* e = getenv("TOOM_LAZY");
+    return e ? atoi(e) : 1;
+}();
+
 // the matrix-form Toom-16 interpolation (f1) instead of the 459-op staged
 // Newton program: TOOM_T16_MATRIX=0 restores the latter (tests compare both)
 static bool g_t16_matrix = [] {
@@ -588,6 +606,56 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         for (size_t l = 0; l + 1 < plan.lv.size(); ++l)
             if ((plan.lv[l].B == 16 || plan.lv[l].B == 32) && !plan.lv[l].lng) return TOOM_EUNSUPPORTED;   // long only
     }
+    // lazy block (csrc/lazy.cuh): from the first long Toom-3/4 level (below a
+    // long Toom-16/P32 top, or at the top) down to the level above the fused
+    // bottom level (every level in between is elementwise when lazy, however
+    // many instances it has); without a fused bottom level, the long,
+    // non-resident prefix only.  The odd part of prod Dc is kept as word
+    // factors for the finishing divisions.
+    plan.lz0 = plan.lz1 = -1;
+    plan.lz_o.clear();
+    plan.lz_s = 0;
+    if (g_lazy) {
+        const size_t NL = plan.lv.size() - 1;
+        const Level& Bt = plan.lv[NL - (NL ? 1 : 0)];
+        const bool fusable = NL >= 2 && !g_disable_fused && (Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) &&
+                             Bt.e == Bt.b + 1 && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
+                             2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e;
+        const size_t fl = fusable ? NL - 1 : NL;   // first level that stays non-lazy
+        uint64_t word = 1;
+        for (size_t l = 0; l < fl; ++l) {
+            Level& L = plan.lv[l];
+            const bool t34 = (L.B == 3 || L.B == 4) && L.e == L.b + 1 && l + 1 < NL;
+            const bool ok = t34 && (plan.lz0 >= 0 ? (fusable || (L.lng && !L.res)) : (L.lng && (fusable || !L.res)));
+            if (!ok) {
+                if (plan.lz0 >= 0 || !L.lng) break;
+                continue;
+            }
+            const uint64_t o = L.B == 3 ? tg_combO_T3 : tg_combO_T4;
+            const int sh = L.B == 3 ? tg_combS_T3 : tg_combS_T4;
+            if (plan.lz_s + sh > 32 * (LV_MAXHALO - 2)) break;
+            if (plan.lz0 < 0) plan.lz0 = (int)l;
+            plan.lz1 = (int)l + 1;
+            if (word * o > 0xFFFFFFFFull) { plan.lz_o.push_back((uint32_t)word); word = 1; }
+            word *= o;
+            plan.lz_s += sh;
+            L.lazy = true;
+            L.lng = true;
+            L.res = false;
+        }
+        if (word > 1) plan.lz_o.push_back((uint32_t)word);
+        if (plan.lz0 >= 0) {
+            // product widths, deepest first: normalised 2e below the block
+            for (int l = plan.lz1 - 1; l >= plan.lz0; --l) {
+                Level& L = plan.lv[l];
+                L.Wy = (l == plan.lz1 - 1) ? 2 * L.e : plan.lv[l + 1].Wx;
+                L.Wx = (2 * L.B - 2) * L.b + L.Wy + 1;
+                if ((L.Wy + L.b - 1) / L.b > 4) return TOOM_EUNSUPPORTED;
+            }
+            // levels below the block are not long any more
+            for (size_t l = plan.lz1; l < NL; ++l) { plan.lv[l].lng = false; plan.lv[l].res = false; }
+        }
+    }
     // fused bottom level?
     plan.fused = false;
     if (plan.lv.size() >= 2 && !g_disable_fused && !plan.lv[plan.lv.size() - 2].lng) {
@@ -607,15 +675,38 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
     for (size_t l = 0; l < nstaged; ++l) {
         Level& L = plan.lv[l];
         const size_t cc = L.count * (size_t)L.npts;
+        if (L.lazy) {
+            // lazy children (LO | HI) and, above the deepest lazy level, the
+            // lazy child products in the same region (the children are dead
+            // once the level below has evaluated them)
+            const bool deepest = (int)l + 1 == plan.lz1;
+            const bool deep_il = (size_t)plan.lz1 + 1 >= plan.lv.size() || !plan.lv[plan.lz1].lng;
+            const size_t ch = (deepest && deep_il) ? 0 : (size_t)(square ? 2 : 4) * L.e * cc;
+            const size_t pr = deepest ? 0 : (size_t)2 * plan.lv[l + 1].Wx * cc;
+            const size_t reg = take(std::max(ch, pr));
+            L.offLzU = reg;
+            L.offLzV = square ? reg : reg + (size_t)2 * L.e * cc * 4;
+            L.offLzP = reg;
+            if (!deepest) continue;   // no normalised children / products
+        }
         L.offU = take((size_t)L.e * cc);
         L.offV = square ? L.offU : take((size_t)L.e * cc);   // squaring: V = U
         L.offP = take((size_t)2 * L.e * cc);
         L.offW = L.lng ? 0 : take((size_t)L.npts * L.Lw * L.count);
     }
+    if (plan.lz0 >= 0) {
+        const Level& L0 = plan.lv[plan.lz0];
+        const Level& Ld = plan.lv[plan.lz1 - 1];
+        plan.offLzX = take((size_t)2 * L0.Wx * L0.count);
+        if (plan.lz_o.size() > 1) plan.offLzT = take((size_t)2 * L0.Wx * L0.count);   // two normalised intermediates
+        plan.nLzTiles = std::max((size_t)L0.count * (size_t)((L0.Wx + LV_TL - 1) / LV_TL),
+                                 (size_t)Ld.count * Ld.npts * (size_t)((Ld.e + LV_TL - 1) / LV_TL));
+        plan.offLzTiles = take((plan.nLzTiles * sizeof(LTile) + 3) / 4);
+    }
     size_t slot_limbs = 0, tiles = 0, nops = 0;
     for (size_t l = 0; l < nstaged; ++l) {
         const Level& L = plan.lv[l];
-        if (!L.lng || L.res) continue;
+        if (!L.lng || L.res || L.lazy) continue;
         LongTables T;
         long_tables(L.B, T);
         const int Wt = long_Wt(L);
@@ -628,7 +719,7 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         size_t Tl = 0;
         while (Tl + 1 < plan.lv.size() && plan.lv[Tl].lng) ++Tl;
         const size_t nTL = plan.lv.size() - 1;
-        if (Tl >= 1 && Tl < nstaged) {   // level Tl is a staged instance-parallel Toom level
+        if (Tl >= 1 && Tl < nstaged && !plan.lv[Tl - 1].lazy) {   // level Tl is a staged instance-parallel Toom level
             const Level& L = plan.lv[Tl - 1];
             plan.bnd = (int)(Tl - 1);
             plan.offT = take((size_t)2 * L.e * L.count * L.npts);
@@ -1822,6 +1913,174 @@ static toom_status launch_res(const Plan& plan, size_t l, bool down, uint32_t* w
     return TOOM_OK;
 }
 
+// ---- lazy levels (csrc/lazy.cuh) ------------------------------------------
+// one finishing op: rows of `x` normalised and divided by 2^(32 sa + sr) o
+static void lazy_finish(const LzSrc& x, size_t rows, uint32_t* dst, long long dst_is, int Wout, uint32_t o, int shift,
+                        LTile* tiles, int cat, cudaStream_t st) {
+    if (rows == 0) return;
+    ProfScope ps(cat, st);
+    constexpr int CH = 16;
+    LzFin F;
+    F.x = x;
+    F.dst = dst;
+    F.dst_is = dst_is;
+    F.Wout = Wout;
+    F.rows = (long long)rows;
+    int nt = LV_NT;
+    if (Wout <= LV_TL) nt = std::max(32, (int)(((Wout + CH - 1) / CH + 31) / 32 * 32));   // one tile per row
+    const int TL = nt * CH;
+    F.tpi = (Wout + TL - 1) / TL;
+    F.o = o;
+    F.oinv = o > 1 ? host_inv32(o) : 1u;
+    F.p32 = o > 1 ? host_powmod(2, 32, o) : 0u;
+    F.Mch = o > 1 ? host_powmod(2, 32ull * CH, o) : 0u;
+    F.mi = o > 1 ? host_invmod(F.Mch, o) : 0u;
+    F.sa = shift / 32;
+    F.sr = shift % 32;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_lz_fin<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        attr = true;
+    }
+    const size_t sm = lz_fin_smem(nt, CH);
+    const unsigned grid = (unsigned)(rows * (size_t)F.tpi);
+    if (F.tpi == 1) {
+        k_lz_fin<CH><<<grid, nt, sm, st>>>(F, tiles, 3);
+        ++t_launches;
+    } else {
+        k_lz_fin<CH><<<grid, nt, sm, st>>>(F, tiles, 1);
+        const unsigned long long orcp = o > 1 ? ~0ull / o : 0ull;
+        launch_scan2(tiles, (int)rows, F.tpi, 1, nt, &F.o, &orcp, &F.Mch, &F.mi, st);
+        k_lz_fin<CH><<<grid, nt, sm, st>>>(F, tiles, 2);
+        t_launches += 2;
+    }
+    ps.done(st);
+}
+
+// the level below the lazy block reads interleaved children (fused bottom or a
+// staged instance-parallel level) unless it is a long / resident level
+static bool lazy_deep_interleaved(const Plan& plan) {
+    const size_t nl = (size_t)plan.lz1;
+    return nl + 1 >= plan.lv.size() || !plan.lv[nl].lng;
+}
+
+static toom_status launch_lazy(const Plan& plan, size_t l, bool down, uint32_t* w, const uint32_t* u, const uint32_t* v,
+                               uint8_t* ws, cudaStream_t st) {
+    const Level& L = plan.lv[l];
+    if (L.count == 0) return TOOM_OK;
+    const size_t cc = L.count * (size_t)L.npts;
+    LTile* tiles = reinterpret_cast<LTile*>(ws + plan.offLzTiles);
+    const bool deepest = (int)l + 1 == plan.lz1;
+    const bool il = lazy_deep_interleaved(plan);
+    const long long cnt = (long long)L.count;
+    if (down) {
+        // parents: the user operands (rows), the interleaved lazy children of
+        // the lazy level above, or the normalised children of a long level above
+        LzSrc pu{}, pv{};
+        if (l == 0) {
+            pu = LzSrc{u, nullptr, L.n, 1, L.n, plan.signed_in ? 1 : 0};
+            pv = LzSrc{v, nullptr, L.n, 1, L.n, plan.signed_in ? 1 : 0};
+        } else if (plan.lv[l - 1].lazy) {
+            const Level& P = plan.lv[l - 1];
+            const size_t half = (size_t)P.e * P.count * P.npts;
+            const uint32_t* a = (const uint32_t*)(ws + P.offLzU);
+            const uint32_t* b = (const uint32_t*)(ws + P.offLzV);
+            pu = LzSrc{a, a + half, 1, cnt, L.n, 0};
+            pv = LzSrc{b, b + half, 1, cnt, L.n, 0};
+        } else {
+            const LVec a = child_vec(plan, l - 1, ws, plan.lv[l - 1].offU, L.n, 0);
+            const LVec b = child_vec(plan, l - 1, ws, plan.lv[l - 1].offV, L.n, 0);
+            if (a.ls != 1 || b.ls != 1) return TOOM_EUNSUPPORTED;
+            pu = LzSrc{a.base, nullptr, L.n, 1, L.n, 1};
+            pv = LzSrc{b.base, nullptr, L.n, 1, L.n, 1};
+        }
+        const unsigned ny = plan.square ? 1 : 2;
+        if (deepest && il) {   // evaluation + carry normalisation, interleaved children
+            ProfScope ps(CAT_EVAL, st);
+            dim3 grid((unsigned)((L.count + 127) / 128), ny);
+            uint32_t* du = (uint32_t*)(ws + L.offU);
+            uint32_t* dv = (uint32_t*)(ws + L.offV);
+            if (L.B == 3) k_lz_eval_last<3><<<grid, 128, 0, st>>>(pu, pv, du, dv, cnt, L.b, L.lentop, L.e);
+            else k_lz_eval_last<4><<<grid, 128, 0, st>>>(pu, pv, du, dv, cnt, L.b, L.lentop, L.e);
+            ps.done(st);
+            ++t_launches;
+            return cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA;
+        }
+        uint32_t* ul = (uint32_t*)(ws + L.offLzU);
+        uint32_t* vl = (uint32_t*)(ws + L.offLzV);
+        const size_t half = (size_t)L.e * cc;
+        {
+            ProfScope ps(CAT_EVAL, st);
+            dim3 grid((unsigned)(((size_t)L.e * L.count + 255) / 256), ny);
+            if (L.B == 3) k_lz_eval<3><<<grid, 256, 0, st>>>(pu, pv, ul, ul + half, vl, vl + half, cnt, L.b, L.lentop, L.e);
+            else k_lz_eval<4><<<grid, 256, 0, st>>>(pu, pv, ul, ul + half, vl, vl + half, cnt, L.b, L.lentop, L.e);
+            ps.done(st);
+            ++t_launches;
+        }
+        if (deepest) {   // row-major normalised children for a long / resident level below
+            for (int opd = 0; opd < (plan.square ? 1 : 2); ++opd) {
+                const uint32_t* src = opd ? vl : ul;
+                const LVec d = child_vec(plan, l, ws, opd ? L.offV : L.offU, L.e, 0);
+                if (d.ls != 1) return TOOM_EUNSUPPORTED;
+                lazy_finish(LzSrc{src, src + half, 1, (long long)cc, L.e, 0}, cc, (uint32_t*)d.base, L.e, L.e, 1u, 0,
+                            tiles, CAT_EVAL, st);
+            }
+        }
+        return cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA;
+    }
+    // up: the child products, normalised (from below the block) or lazy
+    LzSrc y{};
+    if (deepest) {
+        if (il) {
+            y = LzSrc{(const uint32_t*)(ws + L.offP), nullptr, 1, (long long)cc, 2 * L.e, 1};
+        } else {
+            const LVec a = child_vec(plan, l, ws, L.offP, 2 * L.e, 0);
+            if (a.ls != 1) return TOOM_EUNSUPPORTED;
+            y = LzSrc{a.base, nullptr, 2 * L.e, 1, 2 * L.e, 1};
+        }
+    } else {
+        const uint32_t* a = (const uint32_t*)(ws + L.offLzP);
+        y = LzSrc{a, a + (size_t)L.Wy * cc, 1, (long long)cc, L.Wy, 0};
+    }
+    // output: interleaved [Wx][count] (the lazy products of the level above)
+    uint32_t* xo = (uint32_t*)(ws + ((int)l == plan.lz0 ? plan.offLzX : plan.lv[l - 1].offLzP));
+    const size_t xhalf = (size_t)L.Wx * L.count;
+    const int MM = (L.Wy + L.b - 1) / L.b;
+    {
+        ProfScope ps(CAT_INTERP, st);
+        const unsigned grid = (unsigned)(((size_t)L.b * L.count + 255) / 256);
+#define TG_LZI(BB, M) k_lz_interp<BB, M><<<grid, 256, 0, st>>>(y, xo, xo + xhalf, cnt, L.b, L.Wx)
+        if (L.B == 3) { if (MM <= 3) TG_LZI(3, 3); else TG_LZI(3, 4); }
+        else { if (MM <= 3) TG_LZI(4, 3); else TG_LZI(4, 4); }
+#undef TG_LZI
+        ps.done(st);
+        ++t_launches;
+    }
+    if ((int)l == plan.lz0) {   // the deferred division, into w or the parent's products
+        uint32_t* dst;
+        if (l == 0) {
+            dst = w;
+        } else {
+            const LVec d = child_vec(plan, l - 1, ws, plan.lv[l - 1].offP, 2 * L.n, 0);
+            if (d.ls != 1) return TOOM_EUNSUPPORTED;
+            dst = (uint32_t*)d.base;
+        }
+        // one finishing division per word factor of the odd part, the shift
+        // with the last one; normalised row-major intermediates ping-pong in offLzT
+        const size_t nw = plan.lz_o.size();
+        LzSrc src{xo, xo + xhalf, 1, cnt, L.Wx, 0};
+        uint32_t* tb = (uint32_t*)(ws + plan.offLzT);
+        for (size_t i = 0; i < nw; ++i) {
+            const bool last = i + 1 == nw;
+            uint32_t* d = last ? dst : tb + (i & 1) * (size_t)L.Wx * L.count;
+            lazy_finish(src, L.count, d, last ? 2ll * L.n : (long long)L.Wx, last ? 2 * L.n : L.Wx, plan.lz_o[i],
+                        last ? plan.lz_s : 0, tiles, CAT_INTERP, st);
+            src = LzSrc{d, nullptr, L.Wx, 1, L.Wx, 1};
+        }
+    }
+    return cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA;
+}
+
 static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, const uint32_t* v, int n, size_t batch,
                             uint8_t* ws, cudaStream_t st) {
     const size_t L = plan.lv.size() - 1;   // number of Toom levels
@@ -1847,6 +2106,8 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             toom_status r;
             if (stp.first == 2) {
                 r = launch_res(plan, (size_t)stp.second, cat == CAT_EVAL, w, u, v, ws, st);
+            } else if (stp.first == 4) {
+                r = launch_lazy(plan, (size_t)stp.second, cat == CAT_EVAL, w, u, v, ws, st);
             } else if (stp.first == 3) {
                 r = launch_long_big(bops[stp.second], bdesc + stp.second, status, cat, st);
             } else if (stp.first == 0) {
@@ -1866,6 +2127,11 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             if (plan.lv[l].res) {   // instance-resident level: kind 2 steps
                 sdown.push_back({2, (int)l});
                 ups[l].push_back({2, (int)l});
+                continue;
+            }
+            if (plan.lv[l].lazy) {   // lazy level: kind 4 steps
+                sdown.push_back({4, (int)l});
+                ups[l].push_back({4, (int)l});
                 continue;
             }
             LongCall one;
@@ -1939,7 +2205,7 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         uint32_t* out = top ? w : (uint32_t*)(ws + plan.lv[L - 2].offP);
         // a long parent level writes row-major children; a warp-per-product top
         // interpolation reads row-major products
-        const int mode = top ? 1 : (plan.lv[L - 2].lng ? 2 : (plan.top_warp ? 3 : 0));
+        const int mode = top ? 1 : (plan.lv[L - 2].lazy ? 0 : (plan.lv[L - 2].lng ? 2 : (plan.top_warp ? 3 : 0)));
         if ((s = launch_fused(Lv, mode, su, sv, out, st, plan.square))) return s;
     } else {
         const Level& Lv = plan.lv[L - 1];
@@ -2756,9 +3022,9 @@ size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t* plan, char*
         const Level& L = pl.lv[l];
         char tmp[512];
         snprintf(tmp, sizeof tmp,
-                 "%s{\"B\": %d, \"count\": %zu, \"n\": %d, \"b\": %d, \"lentop\": %d, \"e\": %d, \"Lw\": %d, \"npts\": %d, \"long\": %s, \"res\": %s}",
+                 "%s{\"B\": %d, \"count\": %zu, \"n\": %d, \"b\": %d, \"lentop\": %d, \"e\": %d, \"Lw\": %d, \"npts\": %d, \"long\": %s, \"res\": %s, \"lazy\": %s}",
                  l ? ", " : "", L.B, L.count, L.n, L.b, L.lentop, L.e, L.Lw, L.npts, L.lng ? "true" : "false",
-                 L.res ? "true" : "false");
+                 L.res ? "true" : "false", L.lazy ? "true" : "false");
         js += tmp;
     }
     char tail[128];

@@ -762,6 +762,16 @@ def emit_row_tables(ps: PointSet) -> str:
     L.append(f"constexpr unsigned tg_combO_{ps.name} = {oc}u;")
     L.append(f"constexpr unsigned tg_combInv_{ps.name} = 0x{_inv32(oc):08X}u;")
     L.append(f"constexpr int tg_combS_{ps.name} = {sc};")
+    # the combined rows as a constexpr function (lazy long levels, csrc/lazy.cuh)
+    L.append(f"TG_HD constexpr long long tg_combA_cx_{ps.name}(int j, int k) {{")
+    L.append(f"  return")
+    for j in range(NP):
+        for k in range(NP):
+            c = A[j][k] * (Dc // Ds[j])
+            if c:
+                L.append(f"    (j == {j} && k == {k}) ? {c}ll :")
+    L.append("    0ll;")
+    L.append("}")
     return "\n".join(L)
 
 
