@@ -50,6 +50,29 @@ __device__ __forceinline__ long long lz_get(const LzSrc& S, long long row, int p
     return (S.sgn && p == S.n - 1) ? (long long)(int)x : (long long)x;
 }
 
+// g = q d + r for a linear thread index g (< 2^63) and the row count d, with
+// dinv = floor((2^64 - 1) / d): one high multiply and one correction
+__device__ __forceinline__ long long lz_div(long long g, long long d, unsigned long long dinv, long long& r) {
+    unsigned long long q = __umul64hi((unsigned long long)g, dinv);
+    long long rem = g - (long long)q * d;
+    if (rem >= d) { ++q; rem -= d; }
+    r = rem;
+    return (long long)q;
+}
+
+// position p of row `row` in split form v = lo + hi + hs 2^32: hi the lazy
+// carry of the position (same weight), hs the sign of a normalised top limb
+__device__ __forceinline__ void lz_get2(const LzSrc& S, long long row, int p, uint32_t& lo, int& hi, int& hs) {
+    lo = 0;
+    hi = 0;
+    hs = 0;
+    if (p >= S.n) return;
+    const long long o = row * S.is + (long long)p * S.ps;
+    lo = __ldg(S.lo + o);
+    if (S.hi) hi = (int)__ldg(S.hi + o);
+    else if (S.sgn && p == S.n - 1) hs = -(int)(lo >> 31);
+}
+
 template <int B>
 __device__ __forceinline__ constexpr long long lz_evalc(int k, int j) {
     if constexpr (B == 3) return tg_evalc_cx_T3(k, j);
@@ -68,36 +91,43 @@ __device__ __forceinline__ constexpr long long lz_comb(int j, int k) {
 template <int B>
 __global__ void __launch_bounds__(256) k_lz_eval(LzSrc pu, LzSrc pv, uint32_t* __restrict__ ulo, uint32_t* __restrict__ uhi,
                                                  uint32_t* __restrict__ vlo, uint32_t* __restrict__ vhi, long long count,
-                                                 int b, int lentop, int e) {
+                                                 unsigned long long cinv, int b, int lentop, int e) {
     constexpr int NP = 2 * B - 1;
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long t = g / count;
+    long long c;
+    const long long t = lz_div(g, count, cinv, c);
     if (t >= e) return;
-    const long long c = g - t * count;
     const LzSrc& S = blockIdx.y ? pv : pu;
     uint32_t* lo = blockIdx.y ? vlo : ulo;
     uint32_t* hi = blockIdx.y ? vhi : uhi;
-    long long x[B];
+    uint32_t xl[B];
+    int xh[B], xs[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
         const int len = (j == B - 1) ? lentop : b;
-        x[j] = t < len ? lz_get(S, c, j * b + (int)t) : 0ll;
+        xl[j] = 0;
+        xh[j] = 0;
+        xs[j] = 0;
+        if (t < len) lz_get2(S, c, j * b + (int)t, xl[j], xh[j], xs[j]);
     }
     const long long rows = NP * count;
+    uint32_t* pl = lo + t * rows + c;
+    uint32_t* ph = hi + (t + 1) * rows + c;
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
-        long long lin = 0;
+        uint64_t P = 0, N = 0;
+        int H = 0, Hs = 0;
 #pragma unroll
         for (int j = 0; j < B; ++j) {
             const long long m = lz_evalc<B>(k, j);
-            if (m == 1) lin += x[j];
-            else if (m == -1) lin -= x[j];
-            else if (m != 0) lin += m * x[j];
+            if (m > 0) P += (uint64_t)m * xl[j];
+            else if (m < 0) N += (uint64_t)(-m) * xl[j];
+            if (m != 0) { H += (int)m * xh[j]; Hs += (int)m * xs[j]; }
         }
-        const long long R = k * count + c;
-        lo[t * rows + R] = (uint32_t)lin;
-        if (t + 1 < e) hi[(t + 1) * rows + R] = (uint32_t)(int)(lin >> 32);
-        if (t == 0) hi[R] = 0u;
+        const long long lin = (long long)(P - N) + (long long)H + ((long long)Hs << 32);
+        pl[k * count] = (uint32_t)lin;
+        if (t + 1 < e) ph[k * count] = (uint32_t)(int)(lin >> 32);
+        if (t == 0) hi[k * count + c] = 0u;
     }
 }
 
@@ -118,25 +148,31 @@ __global__ void __launch_bounds__(128) k_lz_eval_last(LzSrc pu, LzSrc pv, uint32
     long long cy[NP];
 #pragma unroll
     for (int k = 0; k < NP; ++k) cy[k] = 0;
-#pragma unroll 1
+#pragma unroll 2
     for (int t = 0; t < e; ++t) {
-        long long x[B];
+        uint32_t xl[B];
+        int xh[B], xs[B];
 #pragma unroll
         for (int j = 0; j < B; ++j) {
             const int len = (j == B - 1) ? lentop : b;
-            x[j] = t < len ? lz_get(S, c, j * b + t) : 0ll;
+            xl[j] = 0;
+            xh[j] = 0;
+            xs[j] = 0;
+            if (t < len) lz_get2(S, c, j * b + t, xl[j], xh[j], xs[j]);
         }
         uint32_t* d = dst + (long long)t * rows;
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
-            long long lin = cy[k];
+            uint64_t P = 0, N = 0;
+            int H = 0, Hs = 0;
 #pragma unroll
             for (int j = 0; j < B; ++j) {
                 const long long m = lz_evalc<B>(k, j);
-                if (m == 1) lin += x[j];
-                else if (m == -1) lin -= x[j];
-                else if (m != 0) lin += m * x[j];
+                if (m > 0) P += (uint64_t)m * xl[j];
+                else if (m < 0) N += (uint64_t)(-m) * xl[j];
+                if (m != 0) { H += (int)m * xh[j]; Hs += (int)m * xs[j]; }
             }
+            const long long lin = cy[k] + (long long)(P - N) + (long long)H + ((long long)Hs << 32);
             d[k * count] = (uint32_t)lin;
             cy[k] = lin >> 32;
         }
@@ -148,44 +184,60 @@ __global__ void __launch_bounds__(128) k_lz_eval_last(LzSrc pu, LzSrc pv, uint32
 // receives N_{s-m}[m b + r] for every segment m of the products.  Thread
 // g = r*count + c, r in [0, b): it reads y_k[m b + r] once for all m, k and
 // writes the positions s b + r of the interleaved lazy output [Wx][count].
-// Products of point k of parent c: row k*count + c of `y`.
-template <int B, int MM>
+// Products of point k of parent c: row k*count + c of `y` (interleaved).
+// Each term c'_jk (LO + HI) is one IMAD.WIDE.U32 into a positive or negative
+// 64-bit accumulator (by the sign of the constant) plus a 32-bit MAD of HI.
+template <int B, int MM, bool LZ>
 __global__ void __launch_bounds__(256) k_lz_interp(LzSrc y, uint32_t* __restrict__ xlo, uint32_t* __restrict__ xhi,
-                                                   long long count, int b, int Wx) {
-    constexpr int NP = 2 * B - 1;
+                                                   long long count, unsigned long long cinv, int b, int Wx) {
+    constexpr int NP = 2 * B - 1, NS = NP + MM - 1;
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long rr = g / count;
+    long long c;
+    const long long rr = lz_div(g, count, cinv, c);
     if (rr >= b) return;
     const int r = (int)rr;
-    const long long c = g - rr * count;
-    long long X[NP + MM - 1];
+    uint64_t Xp[NS], Xn[NS];
+    int Xh[NS];
 #pragma unroll
-    for (int s = 0; s < NP + MM - 1; ++s) X[s] = 0;
+    for (int s = 0; s < NS; ++s) { Xp[s] = 0; Xn[s] = 0; Xh[s] = 0; }
+    const long long ks = count * y.is, ms = (long long)b * y.ps;
+    const uint32_t* ylo = y.lo + c * y.is + (long long)r * y.ps;
+    const uint32_t* yhi = LZ ? y.hi + c * y.is + (long long)r * y.ps : nullptr;
 #pragma unroll
     for (int m = 0; m < MM; ++m) {
         const int p = m * b + r;
-        long long yk[NP];
+        const bool in = m < MM - 1 || p < y.n;
 #pragma unroll
-        for (int k = 0; k < NP; ++k) yk[k] = lz_get(y, (long long)k * count + c, p);
-#pragma unroll
-        for (int j = 0; j < NP; ++j) {
-            long long s = 0;
-#pragma unroll
-            for (int k = 0; k < NP; ++k) {
-                const long long a = lz_comb<B>(j, k);
-                if (a != 0) s += a * yk[k];
+        for (int k = 0; k < NP; ++k) {
+            const long long o = k * ks + m * ms;
+            uint32_t lo = 0;
+            int hi = 0;
+            if (in) {
+                lo = __ldg(ylo + o);
+                if constexpr (LZ) hi = (int)__ldg(yhi + o);
+                else hi = (y.sgn && p == y.n - 1) ? -(int)(lo >> 31) : 0;
             }
-            X[j + m] += s;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                const long long a = lz_comb<B>(j, k);
+                if (a > 0) Xp[j + m] += (uint64_t)a * lo;
+                else if (a < 0) Xn[j + m] += (uint64_t)(-a) * lo;
+                if (a != 0) Xh[j + m] += (int)a * hi;
+            }
         }
     }
+    uint32_t* ol = xlo + c + (long long)r * count;
+    uint32_t* oh = xhi + c + (long long)(r + 1) * count;
+    const long long sb = (long long)b * count;
 #pragma unroll
-    for (int s = 0; s < NP + MM - 1; ++s) {
+    for (int s = 0; s < NS; ++s) {
         const int P = s * b + r;
         if (P >= Wx) break;
-        xlo[(long long)P * count + c] = (uint32_t)X[s];
-        if (P + 1 < Wx) xhi[(long long)(P + 1) * count + c] = (uint32_t)(int)(X[s] >> 32);
-        if (P == 0) xhi[c] = 0u;
+        const long long X = (long long)(Xp[s] - Xn[s]) + (LZ ? (long long)Xh[s] : ((long long)Xh[s] << 32));
+        ol[s * sb] = (uint32_t)X;
+        if (P + 1 < Wx) oh[s * sb] = (uint32_t)(int)(X >> 32);
     }
+    if (r == 0) xhi[c] = 0u;
 }
 
 // ---- normalisation + the deferred exact division (two-pass scan) ----------

@@ -2012,8 +2012,9 @@ static toom_status launch_lazy(const Plan& plan, size_t l, bool down, uint32_t* 
         {
             ProfScope ps(CAT_EVAL, st);
             dim3 grid((unsigned)(((size_t)L.e * L.count + 255) / 256), ny);
-            if (L.B == 3) k_lz_eval<3><<<grid, 256, 0, st>>>(pu, pv, ul, ul + half, vl, vl + half, cnt, L.b, L.lentop, L.e);
-            else k_lz_eval<4><<<grid, 256, 0, st>>>(pu, pv, ul, ul + half, vl, vl + half, cnt, L.b, L.lentop, L.e);
+            const unsigned long long cinv = ~0ull / (unsigned long long)cnt;
+            if (L.B == 3) k_lz_eval<3><<<grid, 256, 0, st>>>(pu, pv, ul, ul + half, vl, vl + half, cnt, cinv, L.b, L.lentop, L.e);
+            else k_lz_eval<4><<<grid, 256, 0, st>>>(pu, pv, ul, ul + half, vl, vl + half, cnt, cinv, L.b, L.lentop, L.e);
             ps.done(st);
             ++t_launches;
         }
@@ -2049,9 +2050,12 @@ static toom_status launch_lazy(const Plan& plan, size_t l, bool down, uint32_t* 
     {
         ProfScope ps(CAT_INTERP, st);
         const unsigned grid = (unsigned)(((size_t)L.b * L.count + 255) / 256);
-#define TG_LZI(BB, M) k_lz_interp<BB, M><<<grid, 256, 0, st>>>(y, xo, xo + xhalf, cnt, L.b, L.Wx)
-        if (L.B == 3) { if (MM <= 3) TG_LZI(3, 3); else TG_LZI(3, 4); }
-        else { if (MM <= 3) TG_LZI(4, 3); else TG_LZI(4, 4); }
+        const unsigned long long cinv = ~0ull / (unsigned long long)cnt;
+#define TG_LZI(BB, M, Z) k_lz_interp<BB, M, Z><<<grid, 256, 0, st>>>(y, xo, xo + xhalf, cnt, cinv, L.b, L.Wx)
+#define TG_LZI2(BB, M) { if (y.hi) TG_LZI(BB, M, true); else TG_LZI(BB, M, false); }
+        if (L.B == 3) { if (MM <= 3) TG_LZI2(3, 3) else TG_LZI2(3, 4) }
+        else { if (MM <= 3) TG_LZI2(4, 3) else TG_LZI2(4, 4) }
+#undef TG_LZI2
 #undef TG_LZI
         ps.done(st);
         ++t_launches;
