@@ -215,14 +215,30 @@ __global__ void __launch_bounds__(256) k_lz_interp(LzSrc y, uint32_t* __restrict
             if (in) {
                 lo = __ldg(ylo + o);
                 if constexpr (LZ) hi = (int)__ldg(yhi + o);
-                else hi = (y.sgn && p == y.n - 1) ? -(int)(lo >> 31) : 0;
             }
 #pragma unroll
             for (int j = 0; j < NP; ++j) {
                 const long long a = lz_comb<B>(j, k);
                 if (a > 0) Xp[j + m] += (uint64_t)a * lo;
                 else if (a < 0) Xn[j + m] += (uint64_t)(-a) * lo;
-                if (a != 0) Xh[j + m] += (int)a * hi;
+                if constexpr (LZ) { if (a != 0) Xh[j + m] += (int)a * hi; }
+            }
+        }
+    }
+    if constexpr (!LZ) {
+        // normalised two's-complement products: the top limb (position n-1,
+        // segment m = (n-1) / b) of a negative y_k weighs -2^32 more
+        const int p = y.n - 1, m = p / b;
+        if (y.sgn && p - m * b == r) {
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const int neg = (int)(__ldg(ylo + k * ks + m * ms) >> 31);
+#pragma unroll
+                for (int mm = 0; mm < MM; ++mm)
+                    if (mm == m) {
+#pragma unroll
+                        for (int j = 0; j < NP; ++j) Xh[j + mm] -= (int)lz_comb<B>(j, k) * neg;
+                    }
             }
         }
     }
