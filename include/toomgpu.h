@@ -234,6 +234,19 @@ void toom_set_t16_matrix(int on);
 toom_status toom_base_interleaved(uint32_t *w, const uint32_t *u, const uint32_t *v,
                                   size_t E, size_t count, void *stream);
 
+/* The same base case on the 5th-generation tensor cores (SURVEY.md §8(f)2,
+ * an experiment: north_star allows tensor cores only where they beat the
+ * integer-MAD path; the paper is silent on the base case):
+ * |u|, |v| as 4E bytes, one tcgen05.mma.cta_group::1.kind::i8 per product
+ * (M = 128 rows of the Toeplitz byte windows of |u|, N = 16 >= ceil(4E/32)
+ * reversed 32-byte chunks of |v|, K = 32, u8 x u8 -> s32 in TMEM, exact:
+ * every partial sum < 2^21), byte columns summed and carried into 2E limbs,
+ * the sign applied.  Same layout and result as toom_base_interleaved.
+ * E in {2, 5, 9, 16, 17, 18, 23, 24} (compiled instances), else
+ * TOOM_EUNSUPPORTED.  Not used by the multiplication paths.              */
+toom_status toom_base_interleaved_tc(uint32_t *w, const uint32_t *u, const uint32_t *v,
+                                     size_t E, size_t count, void *stream);
+
 /* Evaluation alone (step a2) at the top level: for each of the `batch`
  * unsigned operands a[batch][n], the 2B-1 values at the point set of B,
  * written INTERLEAVED as out[e][npoints*batch] (value of point k of operand

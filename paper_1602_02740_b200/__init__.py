@@ -55,6 +55,7 @@ SIGNATURES = {
     "toom_status_string": (ctypes.c_char_p, [_I]),
     "toom_last_launch_count": (_SZ, []),
     "toom_base_interleaved": (_I, [_P, _P, _P, _SZ, _SZ, _P]),
+    "toom_base_interleaved_tc": (_I, [_P, _P, _P, _SZ, _SZ, _P]),
     "toom_eval_top": (_I, [_P, _P, _SZ, _SZ, _I, _P]),
     "toom_eval_width": (_SZ, [_SZ, _I]),
     "toom_npoints": (_I, [_I]),
@@ -196,6 +197,16 @@ def base_interleaved(u: torch.Tensor, v: torch.Tensor, stream=None) -> torch.Ten
     out = torch.empty((2 * E, count), dtype=u.dtype, device=u.device)
     _check(lib().toom_base_interleaved(_dev(out, "out"), _dev(u, "u"), _dev(v, "v"), E, count, _stream(stream)),
            "toom_base_interleaved")
+    return out
+
+
+def base_interleaved_tc(u: torch.Tensor, v: torch.Tensor, stream=None) -> torch.Tensor:
+    """Stage a3 on the int8 tensor cores (tcgen05 kind::i8, SURVEY §8(f)2):
+    u, v interleaved [E][count] signed; returns [2E][count]."""
+    E, count = u.shape
+    out = torch.empty((2 * E, count), dtype=u.dtype, device=u.device)
+    _check(lib().toom_base_interleaved_tc(_dev(out, "out"), _dev(u, "u"), _dev(v, "v"), E, count, _stream(stream)),
+           "toom_base_interleaved_tc")
     return out
 
 

@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 #include "ntt.cuh"
 #include "lazy.cuh"
 #include "toplevel.cuh"
+#include "tc_base.cuh"
 namespace tg {
 
 // ------------------------------------------------------------------------
@@ -2982,6 +2983,32 @@ toom_status toom_base_interleaved(uint32_t* w, const uint32_t* u, const uint32_t
     if (s) return fail(s);
     s = launch_base((int)E, u, v, w, count, (cudaStream_t)stream);
     if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+    return fail(s);
+}
+
+// the base case on the int8 tensor cores (csrc/tc_base.cuh)
+toom_status toom_base_interleaved_tc(uint32_t* w, const uint32_t* u, const uint32_t* v, size_t E, size_t count,
+                                     void* stream) {
+    t_launches = 0;
+    if (!w || !u || !v || E < 1) return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    if (count == 0) return TOOM_OK;
+    const cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::min<size_t>(count, (size_t)sms * 8);
+    ProfScope ps(CAT_BASE, st);
+    switch (E) {
+#define TG_TCB(EE) case EE: k_base_tc<EE><<<grid, 128, 0, st>>>(u, v, w, count); break;
+        TG_TCB(2) TG_TCB(5) TG_TCB(9) TG_TCB(16) TG_TCB(17) TG_TCB(18) TG_TCB(23) TG_TCB(24)
+#undef TG_TCB
+        default: return fail(TOOM_EUNSUPPORTED);
+    }
+    ps.done(st);
+    ++t_launches;
+    s = cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA;
     return fail(s);
 }
 

@@ -73,6 +73,45 @@ def test_base_case_signed_interleaved(E):
         assert sval(w[:, c]) == want
 
 
+@pytest.mark.parametrize("E", [2, 5, 9, 16, 17, 18, 23, 24])
+def test_base_case_tensor_core_int8(E):
+    """SURVEY §8(f)2: the base case on tcgen05 kind::i8 (Toeplitz byte windows
+    x reversed 32-byte chunks, s32 accumulation in TMEM) equals the IMAD.WIDE
+    path element by element, and the oracle's schoolbook (w = uv
+    is unique) on sampled products, adversarial magnitudes included (all-ones
+    bytes give the largest partial sums, 32 * 255^2 per MMA output)."""
+    rng = np.random.default_rng(100 + E)
+    count = 3000 + E
+    a = rng.integers(0, 2**32, (E, count), dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 2**32, (E, count), dtype=np.uint64).astype(np.uint32)
+    a[:, 0] = 0xFFFFFFFF            # -1
+    b[:, 1] = 0                     # 0
+    a[:, 2] = 0
+    a[E - 1, 2] = 0x80000000        # most negative
+    b[:, 2] = a[:, 2]
+    a[:, 3] = 0xFFFFFFFF            # |x| = 2^(32E-1) - 1: all-ones magnitude bytes
+    a[E - 1, 3] = 0x7FFFFFFF
+    b[:, 3] = a[:, 3]
+    got = host(tg.base_interleaved_tc(dev(a), dev(b)))
+    assert np.array_equal(got, host(tg.base_interleaved(dev(a), dev(b))))
+
+    def sval(col):
+        x = I(col)
+        return x - (1 << (32 * len(col))) if x >> (32 * len(col) - 1) else x
+
+    for c in list(range(8)) + list(rng.integers(0, count, 32)):
+        x, y = sval(a[:, c]), sval(b[:, c])
+        mag = I(oracle.schoolbook(synth.from_int(abs(x), E), synth.from_int(abs(y), E)))
+        want = mag if (x < 0) == (y < 0) else -mag
+        assert sval(got[:, c]) == want
+
+
+def test_base_case_tensor_core_rejects_unsupported_width():
+    a = torch.zeros((40, 4), dtype=torch.uint32, device="cuda")
+    with pytest.raises(RuntimeError):
+        tg.base_interleaved_tc(a, a)
+
+
 # ------------------------------------------------------------ stage a2 alone
 
 
