@@ -81,7 +81,10 @@ def test_long_count_controls():
     never = levels(1 << 20, 1, 4, long_count=1)
     assert not any(L["long"] for L in never[:-1] if L["B"] != 16)
     always = levels(300, 9, 3, long_count=1 << 30)
-    assert all(L["long"] for L in always[:-1])
+    # every Toom level above the fused bottom level is long (the lazy block,
+    # csrc/lazy.cuh, ends at the fused level, which stays instance-parallel)
+    assert all(L["long"] for L in always[:-2])
+    assert always[0]["lazy"] and not always[-2]["long"]
 
 
 def test_workspace_grows_with_batch():
