@@ -226,6 +226,17 @@ void toom_set_top_stream(int on);
  * are exact; tests compare them.  Affects later calls only.                */
 void toom_set_t16_matrix(int on);
 
+/* C2-shaped batches (256-limb operands, Toom-4 -> Toom-4 -> 18-limb
+ * schoolbook, reading 18).  mode 2 (default): the bottom level
+ * forms X = 360 y in the common-denominator matrix form (no
+ * division) and the top level runs ONE exact division by 360^2 over its own
+ * common-denominator sum, split into segments by the closed-form 2-adic
+ * borrow; 1: the bottom divides its rows itself, the top divides by 360 the
+ * same way; 0: both levels divide row by row (the listing rows, PAPER.md:
+ * 114-120, 154-158, composed).  Same results; tests compare all three.
+ * Affects later calls only.                                              */
+void toom_set_c2_mode(int mode);
+
 /* ---- stage exports (tests, bench) ------------------------------------- */
 
 /* Base case alone (step a3): batched schoolbook of signed two's-complement

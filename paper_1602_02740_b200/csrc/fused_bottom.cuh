@@ -342,6 +342,46 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
             fv = (__ldg(srcV + (c0 + lane) * (size_t)n + n - 1) >> 31) ? 0xFFFFFFFFu : 0u;
         }
         constexpr int ROWS = B * E, ITER = (ROWS + NP - 1) / NP;
+        if constexpr (ST && (MODE == 0 || MODE == 3) && B * E - N_ <= NP && E > BB_) {
+            // compile-time shape: source limb row l (coalesced across the 32
+            // parents) is block j = min(l / b, B - 1), limb l - j b, smem row
+            // l + j (E - b); the B E - n pad rows (zero, or the sign fill of
+            // the top block) take one warp each
+            constexpr int IT = (N_ + NP - 1) / NP, LT = N_ - (B - 1) * BB_, NPAD = B * E - N_;
+            const size_t stp = (size_t)NP * count;
+            const uint32_t* pu = srcU + (size_t)warp * count + c0 + lane;
+            const uint32_t* pv = srcV + (size_t)warp * count + c0 + lane;
+            uint32_t yu[IT], yv[IT];
+#pragma unroll
+            for (int q = 0; q < IT; ++q) {
+                const int l = warp + NP * q;
+                yu[q] = yv[q] = 0u;
+                if (l < N_ && lane < nin) {
+                    yu[q] = __ldg(pu);
+                    yv[q] = __ldg(pv);
+                }
+                pu += stp;
+                pv += stp;
+            }
+#pragma unroll
+            for (int q = 0; q < IT; ++q) {
+                const int l = warp + NP * q;
+                if (l < N_) {
+                    const int j = min(l / BB_, B - 1);
+                    const int r = l + j * (E - BB_);
+                    Pu[r * PP + lane] = yu[q];
+                    Pv[r * PP + lane] = yv[q];
+                }
+            }
+            if (warp < NPAD) {
+                // pad row `warp`: rows j E + [b, E) of blocks j < B - 1 (zero),
+                // then (B - 1) E + [lentop, E) of the top block (fill)
+                constexpr int ZP = (B - 1) * (E - BB_);
+                const int r = warp < ZP ? (warp / (E - BB_)) * E + BB_ + warp % (E - BB_) : (B - 1) * E + LT + (warp - ZP);
+                Pu[r * PP + lane] = warp < ZP ? 0u : fu;
+                Pv[r * PP + lane] = warp < ZP ? 0u : fv;
+            }
+        } else {
         uint32_t xu[ITER], xv[ITER];
         if constexpr (MODE == 0 || MODE == 3) {
             // interleaved parents: row r = warp + q NP is block j limb t; both
@@ -404,6 +444,7 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
                 Pu[r * PP + lane] = xu[q];
                 Pv[r * PP + lane] = xv[q];
             }
+        }
         }
     }
     __syncthreads();

@@ -1,0 +1,258 @@
+// The C2 bottom level (Toom-4 on 65-limb signed parents, b = 17, 18-limb
+// base products) with the common denominator of its interpolation DEFERRED to
+// the top level (reading 18).
+//
+// The per-coefficient matrix form over the common denominator Dc = 360
+// (reading 12):
+//     Dc * w = X = sum_j 2^(32 b j) N_j,   N_j = sum_k A'_jk y_k
+// has no division, so it is elementwise in the limb position: limb P of X is
+//     X[P] = sum_j sum_k A'_jk y_k[P - 17 j]          (|X[P]| < 2^46)
+// which every thread of the CTA can form for any position (no serial row
+// chains, no per-row exact division).  One carry pass normalises X modulo
+// 2^(32*130) -- X = 360 w fits 130 signed limbs for C2's operands, whose
+// evaluated values are below 15 * 2^2048 -- and the top-level interpolation
+// divides by 360^2 instead of 360 in the one exact division it runs anyway.
+//
+// CTA = 32 parents (one per lane) x 7 warps:
+//   A0  stage the parents' blocks in smem (row l of the source is block
+//       l / 17, limb l % 17; one pad row per warp)
+//   A   warp k: evaluate U(x_k), V(x_k), multiply (register Comba) into the
+//       warp's product slot Y[k][36][32]; the product's sign to SG[k]
+//   B1  class r = P mod 17 (warp w: r = w, w + 7, w + 14): the columns
+//       t = r, r + 17 (, r + 34) of the seven products give X[r + 17 m],
+//       m = 0..7; a class reads and then overwrites only its own columns
+//       (lo words in (k = m, t = r), packed 16-bit high words in
+//       (k = 1 + m/2, t = r + 17)), so no barrier separates the reads and
+//       the writes
+//   B2  warp w: carry pass over its segment of positions (carry-in 0),
+//       limbs 1.. written (interleaved), limb 0 and the carry-out kept
+//   B3  warp 0: the segments' carries in order; limb 0 written, a carry
+//       that wraps limb 0 (probability ~2^-17) ripples through the segment
+// The top level (csrc/toplevel_cls.cuh, DEF) divides by 360^2 in its one
+// division over the common denominator.
+#pragma once
+
+namespace tg {
+
+namespace c2dc {
+constexpr int N = 65, BB = 17, E = 18, W2 = 36, WOUT = 130, NP = 7, G = 32, PP = 33, NSEG = 7;
+constexpr long long DC = (long long)tg_combO_T4 << tg_combS_T4;   // 360
+static_assert(DC == 360, "Toom-4 common denominator");
+template <int J, int K> constexpr long long combA_v = tg_combA_cx_T4(J, K);
+// segment s of the carry pass: positions [seg0(s), seg0(s + 1))
+__host__ __device__ constexpr int seg0(int s) { return s < 4 ? 19 * s : 76 + 18 * (s - 4); }
+static_assert(seg0(NSEG) == WOUT, "segments cover the 130 output limbs");
+}  // namespace c2dc
+
+// X[r + 17 m] of class r from the columns t = r + 17 i of the products
+template <int J, int K>
+__device__ __forceinline__ void c2dc_cterm(uint32_t y, uint64_t& p, uint64_t& n) {
+    constexpr long long A = c2dc::combA_v<J, K>;   // folded at compile time
+    if constexpr (A > 0) p = tg_madw((uint32_t)A, y, p);
+    else if constexpr (A < 0) n = tg_madw((uint32_t)(-A), y, n);
+}
+template <int J>
+__device__ __forceinline__ void c2dc_row(const uint32_t (&y)[7], uint64_t& p, uint64_t& n) {
+    c2dc_cterm<J, 0>(y[0], p, n);
+    c2dc_cterm<J, 1>(y[1], p, n);
+    c2dc_cterm<J, 2>(y[2], p, n);
+    c2dc_cterm<J, 3>(y[3], p, n);
+    c2dc_cterm<J, 4>(y[4], p, n);
+    c2dc_cterm<J, 5>(y[5], p, n);
+    c2dc_cterm<J, 6>(y[6], p, n);
+}
+template <int I>
+__device__ __forceinline__ void c2dc_column(const uint32_t (&y)[7], uint64_t (&aP)[8], uint64_t (&aN)[8]) {
+    c2dc_row<0>(y, aP[I], aN[I]);
+    c2dc_row<1>(y, aP[I + 1], aN[I + 1]);
+    if constexpr (I + 2 <= 7) c2dc_row<2>(y, aP[I + 2], aN[I + 2]);
+    if constexpr (I + 3 <= 7) c2dc_row<3>(y, aP[I + 3], aN[I + 3]);
+    if constexpr (I + 4 <= 7) c2dc_row<4>(y, aP[I + 4], aN[I + 4]);
+    if constexpr (I + 5 <= 7) c2dc_row<5>(y, aP[I + 5], aN[I + 5]);
+    if constexpr (I + 6 <= 7) c2dc_row<6>(y, aP[I + 6], aN[I + 6]);
+}
+
+__device__ __forceinline__ void c2dc_class(int r, uint32_t* Y, const uint32_t* SG, int lane) {
+    using namespace c2dc;
+    uint64_t aP[8], aN[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) aP[m] = aN[m] = 0ull;
+    uint32_t* col0 = Y + r * G + lane;          // cells (k, t = r)
+    uint32_t* col1 = col0 + BB * G;             // cells (k, t = r + 17)
+    {
+        uint32_t y[7];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = col0[k * W2 * G];
+        c2dc_column<0>(y, aP, aN);
+    }
+    {
+        uint32_t y[7];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = col1[k * W2 * G];
+        c2dc_column<1>(y, aP, aN);
+    }
+    if (r < 2) {            // t = r + 34 (stored columns 34, 35)
+        uint32_t y[7];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = col1[(k * W2 + BB) * G];
+        c2dc_column<2>(y, aP, aN);
+    } else if (r == 2) {    // t = 36: the sign terms, y_k = -s_k (two's complement products)
+        uint32_t s[7];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) s[k] = SG[k * G + lane];
+        c2dc_column<2>(s, aN, aP);   // -A s: the positive and negative sums swap
+    }
+    // X[r + 17 m] = aP - aN: lo words in (k = m, t = r) (m = 7: (0, r + 17)),
+    // high words (|X| < 2^46: 16 bits) packed two per cell in (1 + m/2, r + 17)
+    uint32_t hw[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const uint64_t x = aP[m] - aN[m];
+        if (m < 7) col0[m * W2 * G] = (uint32_t)x;
+        hw[m] = (uint32_t)(x >> 32) & 0xFFFFu;
+    }
+    if (r <= 10) col1[0] = (uint32_t)(aP[7] - aN[7]);   // position r + 119 <= 129
+#pragma unroll
+    for (int h = 0; h < 4; ++h) col1[(1 + h) * W2 * G] = hw[2 * h] | (hw[2 * h + 1] << 16);
+}
+
+__host__ __device__ constexpr size_t c2dc_smem_bytes() {
+    return (size_t)4 * (c2dc::NP * c2dc::W2 * c2dc::G + 2 * 4 * c2dc::E * c2dc::PP + c2dc::NP * c2dc::G);
+}
+
+__global__ void __launch_bounds__(224, 4) k_fused_c2_dc(const uint32_t* __restrict__ srcU, const uint32_t* __restrict__ srcV,
+                                                       uint32_t* __restrict__ out, size_t count) {
+    using namespace c2dc;
+    extern __shared__ uint32_t sm[];
+    uint32_t* Y = sm;                       // [7][36][32] products, then X (class cells)
+    uint32_t* Pu = Y + NP * W2 * G;         // [4 * 18][33] staged parents
+    uint32_t* Pv = Pu + 4 * E * PP;
+    uint32_t* SG = Pv + 4 * E * PP;         // [7][32] product signs
+    uint32_t* L0 = Pu;                      // after phase A: [7][32] segment limb 0
+    uint32_t* CO = Pu + NSEG * G;           //                [7][32] segment carry-out
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t c0 = (size_t)blockIdx.x * G;
+    const int nin = (int)min((size_t)G, count - c0);
+    const bool valid = lane < nin;
+    const size_t c = c0 + lane;
+
+    // ---- A0: source row l (limb l of the parent) is block j = l / 17, limb
+    // l - 17 j, smem row j * 18 + l - 17 j = l + j; pad rows 17, 35, 53 (zero)
+    // and 68..71 (sign fill of the 14-limb top block)
+    {
+        const size_t st7 = (size_t)NP * count;
+        const uint32_t* pu = srcU + (size_t)warp * count + c;
+        const uint32_t* pv = srcV + (size_t)warp * count + c;
+        uint32_t xu[10], xv[10];
+#pragma unroll
+        for (int q = 0; q < 10; ++q) {
+            const int l = warp + NP * q;
+            xu[q] = xv[q] = 0u;
+            if (l < N && valid) {
+                xu[q] = __ldg(pu);
+                xv[q] = __ldg(pv);
+            }
+            pu += st7;
+            pv += st7;
+        }
+        uint32_t fu = 0u, fv = 0u;
+        if (warp >= 3 && valid) {
+            fu = (__ldg(srcU + (size_t)(N - 1) * count + c) >> 31) ? 0xFFFFFFFFu : 0u;
+            fv = (__ldg(srcV + (size_t)(N - 1) * count + c) >> 31) ? 0xFFFFFFFFu : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 10; ++q) {
+            const int l = warp + NP * q;
+            if (l < N) {
+                const int row = l + (l >= 17) + (l >= 34) + (l >= 51);
+                Pu[row * PP + lane] = xu[q];
+                Pv[row * PP + lane] = xv[q];
+            }
+        }
+        const int pr = warp < 3 ? 17 + 18 * warp : 65 + warp;
+        Pu[pr * PP + lane] = fu;
+        Pv[pr * PP + lane] = fv;
+    }
+    __syncthreads();
+
+    // ---- A: point `warp`, product into the warp's slot
+    {
+        uint32_t* slot = Y + (warp * W2) * G + lane;
+        eval_point_rows<4, E>(warp, Pu + lane, Pv + lane, slot, slot + E * G);
+        uint32_t a[E], bb[E];
+#pragma unroll
+        for (int t = 0; t < E; ++t) { a[t] = slot[t * G]; bb[t] = slot[(E + t) * G]; }
+        mul_twos_to_smem<E>(a, bb, slot);
+        SG[warp * G + lane] = slot[(W2 - 1) * G] >> 31;
+    }
+    __syncthreads();
+
+    // ---- B1: the classes r = warp, warp + 7, warp + 14
+    for (int r = warp; r < BB; r += NP) c2dc_class(r, Y, SG, lane);
+    __syncthreads();
+
+    // ---- B2: carry pass over segment `warp` with carry-in 0
+    {
+        const int P0 = seg0(warp), L = seg0(warp + 1) - P0;
+        int m = P0 / BB, r = P0 - BB * m;
+        auto plo = [&](int mm) { return Y + (mm < 7 ? mm * W2 : BB) * G + lane; };
+        auto phi = [&](int mm) { return Y + ((1 + (mm >> 1)) * W2 + BB) * G + lane; };
+        const uint32_t* pl = plo(m) + r * G;
+        const uint32_t* ph = phi(m) + r * G;
+        int hs = (m & 1) ? 0 : 16;
+        uint32_t* po = out + (size_t)P0 * count + c;
+        long long carry = 0;
+        uint32_t l0 = 0;
+        for (int q = 0; q < L; ++q) {
+            const long long hi = (long long)((int32_t)(*ph << hs) >> 16);
+            const long long x = (long long)*pl + (hi << 32) + carry;
+            const uint32_t limb = (uint32_t)x;
+            carry = x >> 32;
+            if (q == 0) l0 = limb;
+            else if (valid) *po = limb;
+            po += count;
+            if (++r == BB) {
+                r = 0;
+                ++m;
+                pl = plo(m);
+                ph = phi(m);
+                hs = (m & 1) ? 0 : 16;
+            } else {
+                pl += G;
+                ph += G;
+            }
+        }
+        L0[warp * G + lane] = l0;
+        CO[warp * G + lane] = (uint32_t)(int32_t)carry;
+    }
+    __syncthreads();
+
+    // ---- B3: carries between the segments (one lane per parent)
+    if (warp != 0 || !valid) return;
+    long long cin = 0;
+#pragma unroll 1
+    for (int s = 0; s < NSEG; ++s) {
+        const int P0 = seg0(s), L = seg0(s + 1) - P0;
+        const long long x = (long long)L0[s * G + lane] + cin;
+        uint32_t* po = out + (size_t)P0 * count + c;
+        // fault injection (tests): X_0 = 360 y_0 of the first
+        // parent made odd, so the top level's division by 360^2 is not exact
+        // (X changes by 360 mod 2^6: its check of the low bits catches it)
+        const uint32_t flt = (tg_fault && s == 0 && c == 0) ? 1u : 0u;
+        *po = (uint32_t)x ^ flt;
+        long long d = x >> 32;   // -1, 0, +1
+        cin = (long long)(int32_t)CO[s * G + lane];
+        if (d != 0) {            // rare: limb 0 wrapped
+            for (int q = 1; q < L && d != 0; ++q) {
+                po += count;
+                const uint32_t v = *po;
+                const uint32_t nv = v + (uint32_t)d;
+                *po = nv;
+                d = (d > 0) ? (nv == 0u ? 1 : 0) : (v == 0u ? -1 : 0);
+            }
+            cin += d;
+        }
+    }
+}
+
+}  // namespace tg

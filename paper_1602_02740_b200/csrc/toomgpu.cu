@@ -374,12 +374,14 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 
 }  // namespace tg
 #include "fused_bottom.cuh"
+#include "fused_c2.cuh"
 #include "longvec.cuh"
 #include "longvec2.cuh"
 #include "level34.cuh"
 #include "ntt.cuh"
 #include "lazy.cuh"
 #include "toplevel.cuh"
+#include "toplevel_cls.cuh"
 #include "tc_base.cuh"
 namespace tg {
 
@@ -419,6 +421,7 @@ struct Plan {
     size_t offEDesc = 0;     // multi-output evaluation descriptors
     size_t offBDesc = 0;     // wide-multiplier multi-output descriptors (matrix-form T16)
     bool top_warp = false;   // top interpolation one warp per product (fused level writes row-major)
+    int c2mode = 0;          // C2 shape: 1 top level by classes (toplevel_cls.cuh), 2 + deferred bottom (fused_c2.cuh)
     // lazy block [lz0, lz1) of long levels (csrc/lazy.cuh): the product of
     // their common denominators 2^lz_s lz_o, the top lazy output X and the
     // two-pass tile records of the finishing scans
@@ -529,6 +532,17 @@ static int g_lazy = [] {
 static bool g_t16_matrix = [] {
     const char* e = getenv("TOOM_T16_MATRIX");
     return e ? atoi(e) != 0 : true;
+}();
+// C2-shaped batches: the top level as one division over the common
+// denominator (csrc/toplevel_cls.cuh) and the bottom level with that
+// denominator deferred to it (csrc/fused_c2.cuh); TOOM_C2_CLS=0 /
+// TOOM_DEFERRED_BOTTOM=0 run the per-row kernels instead (tests compare all)
+static int g_c2mode = [] {
+    const char* a = getenv("TOOM_C2_CLS");
+    const char* b = getenv("TOOM_DEFERRED_BOTTOM");
+    const bool cls = a ? atoi(a) != 0 : true;
+    const bool dc = b ? atoi(b) != 0 : true;
+    return cls ? (dc ? 2 : 1) : 0;
 }();
 constexpr int F1_SLOTS = 61;   // E, O, R, T (15 each) + y'
 static int long_nslots(int B, int nslots) { return (B == 16 && g_t16_matrix) ? std::max(nslots, F1_SLOTS) : nslots; }
@@ -669,6 +683,12 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
     // can run one warp per product on row-major products (fused MODE 3)
     plan.top_warp = plan.fused && plan.lv.size() == 3 && !plan.lv[0].lng && g_top_stream == 3 &&
                     top_warp_ch(plan.lv[0]) > 0 && plan.lv[0].Lw == 2 * plan.lv[0].b + 1;
+    // the C2 shape (256 -> 65 -> 18 limbs, Toom-4 twice, batched)
+    const bool c2shape = plan.fused && !square && plan.lv.size() == 3 && !plan.lv[0].lng && !plan.top_warp &&
+                         plan.lv[0].B == 4 && plan.lv[0].n == 256 && plan.lv[0].b == 64 && plan.lv[0].e == 65 &&
+                         plan.lv[0].Lw == 129 && plan.lv[1].B == 4 && plan.lv[1].n == 65 && plan.lv[1].b == 17 &&
+                         plan.lv[1].e == 18 && plan.lv[1].Lw == 35;
+    plan.c2mode = (c2shape && g_its_static && g_top_stream == 2) ? g_c2mode : 0;
     // workspace layout
     size_t off = 0;
     auto take = [&](size_t limbs) { size_t o = off; off += ((limbs * 4 + 255) / 256) * 256; return o; };
@@ -1027,6 +1047,42 @@ static toom_status launch_fused(const Level& Lv, int mode, const uint32_t* su, c
     TG_F(4, 6) TG_F(4, 9) TG_F(4, 18) TG_F(4, 23) TG_F(4, 27) TG_F(4, 33)
 #undef TG_F
     return TOOM_EUNSUPPORTED;
+}
+
+// the C2 bottom with the deferred denominator (csrc/fused_c2.cuh)
+static toom_status launch_fused_c2dc(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out,
+                                     cudaStream_t st) {
+    if (Lv.count == 0) return TOOM_OK;
+    ProfScope ps(CAT_BASE, st);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_fused_c2_dc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2dc_smem_bytes());
+        cudaFuncSetAttribute(k_fused_c2_dc, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    const unsigned grid = (unsigned)((Lv.count + 31) / 32);
+    k_fused_c2_dc<<<grid, 224, c2dc_smem_bytes(), st>>>(su, sv, out, Lv.count);
+    ps.done(st);
+    ++t_launches;
+    return TOOM_OK;
+}
+
+// the C2 top level as one division over the common denominator (csrc/toplevel_cls.cuh)
+static toom_status launch_interp_top_cls(const Level& Lv, const uint32_t* P1, uint32_t* w, bool def, cudaStream_t st) {
+    if (Lv.count == 0) return TOOM_OK;
+    ProfScope ps(CAT_INTERP, st);
+    static bool attr[2] = {false, false};
+    auto kern = def ? k_interp_top_cls<true> : k_interp_top_cls<false>;
+    if (!attr[def]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cls_smem_bytes());
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr[def] = true;
+    }
+    const unsigned grid = (unsigned)((Lv.count + cls::G - 1) / cls::G);
+    kern<<<grid, 224, cls_smem_bytes(), st>>>(P1, w, Lv.count);
+    ps.done(st);
+    ++t_launches;
+    return TOOM_OK;
 }
 
 static bool g_disable_toprows = false;
@@ -2211,7 +2267,11 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         // a long parent level writes row-major children; a warp-per-product top
         // interpolation reads row-major products
         const int mode = top ? 1 : (plan.lv[L - 2].lazy ? 0 : (plan.lv[L - 2].lng ? 2 : (plan.top_warp ? 3 : 0)));
-        if ((s = launch_fused(Lv, mode, su, sv, out, st, plan.square))) return s;
+        if (plan.c2mode == 2) {
+            if ((s = launch_fused_c2dc(Lv, su, sv, out, st))) return s;
+        } else if ((s = launch_fused(Lv, mode, su, sv, out, st, plan.square))) {
+            return s;
+        }
     } else {
         const Level& Lv = plan.lv[L - 1];
         if ((s = launch_base(Lv.e, (const uint32_t*)(ws + Lv.offU), (const uint32_t*)(ws + Lv.offV),
@@ -2227,6 +2287,10 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
             launch_interp_top_warp(Lv, (const uint32_t*)(ws + Lv.offP), w, st);
             ps.done(st);
             ++t_launches;
+            continue;
+        }
+        if (l == 0 && plan.c2mode) {   // one division over the common denominator (360, or 360^2)
+            if ((s = launch_interp_top_cls(Lv, (const uint32_t*)(ws + Lv.offP), w, plan.c2mode == 2, st))) return s;
             continue;
         }
         if (l == 0 && top_rows_ok(Lv) && g_top_stream != 4) {   // mode 4: the per-thread streaming kernel
@@ -3017,6 +3081,7 @@ int toom_npoints(int B) { return ps_desc(B).npts; }
 void toom_set_top_stream(int on) { g_top_stream = on; }
 
 void toom_set_t16_matrix(int on) { g_t16_matrix = on != 0; }
+void toom_set_c2_mode(int mode) { g_c2mode = (mode >= 0 && mode <= 2) ? mode : 0; }
 
 void toom_set_fused(int on) {
     // 0: every level staged (k_eval / k_base / k_interp); 1: fused bottom level

@@ -29,6 +29,7 @@ def _reset():
     if not torch.cuda.is_available():
         pytest.fail("no CUDA device: GPU tests must run on the B200 box")
     tg.lib()
+    tg.last_error()          # a status left by an earlier test (e.g. an expected TOOM_ENOMEM)
     yield
     tg.debug_fault(0)
     tg.set_check(True)       # read back (and clear) any device flag, then switch off
@@ -82,6 +83,23 @@ def test_fault_injection_reports_inexact_division():
     tg.debug_fault(0)
     tg.toom_mul_batched(dev(u), dev(v), B=4, t4=32, t3=32)
     assert tg.last_error() == tg.TOOM_OK
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fault_injection_other_c2_modes(mode):
+    """The per-row C2 bottom (modes 0, 1) flips a product bit; its own row
+    divisions catch it."""
+    u, v = synth.config_inputs(2, batch=256)
+    tg.set_c2_mode(mode)
+    try:
+        tg.set_check(True)
+        tg.last_error()
+        tg.debug_fault(1)
+        tg.toom_mul_batched(dev(u), dev(v), B=4, t4=32, t3=32)
+        assert tg.last_error() == tg.TOOM_EINEXACT
+    finally:
+        tg.debug_fault(0)
+        tg.set_c2_mode(2)
 
 
 def test_fault_injection_caught_by_verify_alone():

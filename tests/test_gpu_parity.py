@@ -182,6 +182,35 @@ def test_c2_full_batch_bit_exact():
         check_residues(u[i], v[i], w[i])
 
 
+@pytest.mark.parametrize("batch", [1, 29, 1234])
+def test_c2_modes_equal_oracle(batch):
+    """The three C2 paths (reading 18): 2 = bottom with the deferred
+    common denominator + top level as one division by 360^2 (csrc/fused_c2.cuh,
+    csrc/toplevel_cls.cuh), 1 = per-row bottom + one top division by 360,
+    0 = per-row divisions at both levels; all equal to the oracle, with
+    extreme operands (all-ones: the largest evaluated values and products,
+    carries through whole segments; alternating limbs; zero; one top bit) and
+    ragged CTA tails (28 products per top CTA, 32 children per bottom CTA)."""
+    rng = np.random.default_rng(batch)
+    n = 256
+    u = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    v = rng.integers(0, 2**32, (batch, n), dtype=np.uint64).astype(np.uint32)
+    pats = [np.full(n, 0xFFFFFFFF, np.uint32), np.tile(np.array([0, 0xFFFFFFFF], np.uint32), n // 2),
+            np.zeros(n, np.uint32), np.r_[np.zeros(n - 1, np.uint32), np.uint32(1 << 31)]]
+    for i in range(min(batch, 16)):
+        u[i] = pats[i % 4]
+        v[i] = pats[(i // 4) % 4]
+    want = oracle.schoolbook_batched(u, v)
+    try:
+        for mode in (2, 1, 0):
+            tg.set_c2_mode(mode)
+            w = run_batched(u, v, 4, **C2_PLAN)
+            bad = np.nonzero((w != want).any(axis=1))[0]
+            assert bad.size == 0, f"mode {mode}: {bad.size} products differ, first {bad[:8]}"
+    finally:
+        tg.set_c2_mode(2)
+
+
 def test_c2_chunked_equals_unchunked():
     u, v = synth.config_inputs(2, batch=5000)
     a = run_batched(u, v, 4, **C2_PLAN)
