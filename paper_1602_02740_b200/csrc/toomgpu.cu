@@ -1079,7 +1079,7 @@ static toom_status launch_interp_top_cls(const Level& Lv, const uint32_t* P1, ui
         attr[def] = true;
     }
     const unsigned grid = (unsigned)((Lv.count + cls::G - 1) / cls::G);
-    kern<<<grid, 224, cls_smem_bytes(), st>>>(P1, w, Lv.count);
+    kern<<<grid, 32 * cls::NW, cls_smem_bytes(), st>>>(P1, w, Lv.count);
     ps.done(st);
     ++t_launches;
     return TOOM_OK;

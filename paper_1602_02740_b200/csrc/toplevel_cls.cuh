@@ -15,7 +15,7 @@
 //   1  class r = P mod 64 (warp w: r = w, w + 7, ...): the columns t = r,
 //      r + 64 (, r + 128 / the sign column 130) give X[r + 64 m], m = 0..8,
 //      written over the class's own columns (lo words, packed 16-bit highs)
-//   2  segment s (warp s): carries with carry-in 0 -> limbs z, the carry-out
+//   2  segment s (warp s of 14): carries with carry-in 0 -> limbs z, the carry-out
 //      and the residue of the segment's X mod o
 //   3  warp 0: the true carry-ins (a carry that wraps limb 0 ripples) and
 //      the borrow-ins, segment by segment
@@ -26,8 +26,9 @@
 namespace tg {
 
 namespace cls {
-constexpr int NP = 7, BB = 64, YW = 130, G = 28, WOUT = 512, NPOS = 513, NSEG = 7;
-__host__ __device__ constexpr int seg0(int s) { return 73 * s + (s > 5 ? s - 5 : 0); }
+constexpr int NP = 7, BB = 64, YW = 130, G = 28, WOUT = 512, NPOS = 513;
+constexpr int NW = 14, NSEG = NW;   // warps per CTA (two CTAs per SM by shared memory), one segment each
+__host__ __device__ constexpr int seg0(int s) { return 36 * s + (s > 5 ? s - 5 : 0); }
 static_assert(seg0(NSEG) == NPOS, "segments cover the 513 quotient limbs");
 __host__ __device__ constexpr uint32_t modpow32(uint32_t o, long long e) {   // 2^(32 e) mod o, e >= 0
     uint64_t r = 1 % o, b = (uint64_t)(((unsigned __int128)1 << 32) % o);
@@ -52,14 +53,14 @@ template <bool DEF> struct Den {
 static_assert(Den<false>::o << Den<false>::s == 360u && (uint64_t)Den<true>::o << Den<true>::s == 129600u, "D");
 static_assert(Den<true>::oinv * 2025u == 1u, "2-adic inverse");
 template <uint32_t O> struct Pw {
-    uint32_t p[75];     // 2^(32 i) mod O, i = 0..74
-    uint32_t ip[2];     // 2^(-32 L) mod O for L = 73, 74
+    uint32_t p[40];     // 2^(32 i) mod O, i = 0..39
+    uint32_t ip[2];     // 2^(-32 L) mod O for L = 36, 37
 };
 template <uint32_t O> __host__ __device__ constexpr Pw<O> make_pw() {
     Pw<O> t{};
-    for (int i = 0; i < 75; ++i) t.p[i] = modpow32(O, i);
-    t.ip[0] = invmod(modpow32(O, 73), O);
-    t.ip[1] = invmod(modpow32(O, 74), O);
+    for (int i = 0; i < 40; ++i) t.p[i] = modpow32(O, i);
+    t.ip[0] = invmod(modpow32(O, 36), O);
+    t.ip[1] = invmod(modpow32(O, 37), O);
     return t;
 }
 }  // namespace cls
@@ -174,11 +175,18 @@ __device__ __forceinline__ void cls_carry_run(uint32_t* pl, const uint32_t* ph, 
 template <uint32_t O, uint32_t OINV>
 __device__ __forceinline__ void cls_div_run(uint32_t* pl, int n, uint32_t& bor) {
 #pragma unroll 4
-    for (int i = 0; i < n; ++i) pl[i * cls::G] = tg_divexact_step(pl[i * cls::G], bor, OINV, O);
+    for (int i = 0; i < n; ++i) {
+        // one limb of the 2-adic exact division (ref [4]): q = (t - bor) o^-1,
+        // bor' = hi(q o) + (t < bor)
+        const uint32_t t = pl[i * cls::G];
+        const uint32_t q = (t - bor) * OINV;
+        bor = __umulhi(q, O) + (t < bor ? 1u : 0u);
+        pl[i * cls::G] = q;
+    }
 }
 
 template <bool DEF>
-__global__ void __launch_bounds__(224, 2) k_interp_top_cls(const uint32_t* __restrict__ P1, uint32_t* __restrict__ w,
+__global__ void __launch_bounds__(32 * cls::NW, 2) k_interp_top_cls(const uint32_t* __restrict__ P1, uint32_t* __restrict__ w,
                                                           size_t count) {
     using namespace cls;
     constexpr uint32_t o = Den<DEF>::o, oinv = Den<DEF>::oinv;
@@ -196,10 +204,13 @@ __global__ void __launch_bounds__(224, 2) k_interp_top_cls(const uint32_t* __res
     const bool act = lane < G;
 
     // ---- 0: rows (k, t) of G contiguous words; row R = t * 7 + k in source
-    // order, 4 rows per warp instruction (7 lanes x 16 bytes each)
+    // order, 4 rows per warp instruction (7 lanes x 16 bytes each), a warp's
+    // rows keep their point k and advance t by 8
     {
         const bool v16 = ((count & 3) == 0) && ((((uintptr_t)P1) & 15) == 0);
         const int sub = lane / 7, q = lane - 7 * sub;
+        constexpr int TS = 4 * NW / NP;   // limb rows per step
+        static_assert(4 * NW == TS * NP, "rows per step: whole limb rows of all points");
         if (sub < 4) {
             const int R0 = warp * 4 + sub;
             const int k = R0 % NP;
@@ -207,13 +218,13 @@ __global__ void __launch_bounds__(224, 2) k_interp_top_cls(const uint32_t* __res
             const int g = q * 4;
             const uint32_t* sr = P1 + (size_t)t * SK + (size_t)k * count + c0 + g;
             uint32_t* dr = Y + (size_t)(k * YW + t) * G + g;
-            const size_t sstep = (size_t)4 * SK;
+            const size_t sstep = (size_t)TS * SK;
             if (v16 && g + 3 < nin) {
                 unsigned d = (unsigned)__cvta_generic_to_shared(dr);
-                for (; t < YW; t += 4, sr += sstep, d += 4u * 4 * G)
+                for (; t < YW; t += TS, sr += sstep, d += 4u * TS * G)
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(sr));
             } else {
-                for (; t < YW; t += 4, sr += sstep, dr += 4 * G) {
+                for (; t < YW; t += TS, sr += sstep, dr += TS * G) {
 #pragma unroll
                     for (int x = 0; x < 4; ++x) dr[x] = (g + x < nin) ? __ldg(sr + x) : 0u;
                 }
@@ -225,7 +236,7 @@ __global__ void __launch_bounds__(224, 2) k_interp_top_cls(const uint32_t* __res
 
     // ---- 1: the classes of this warp
     if (act)
-        for (int r = warp; r < BB; r += NP) cls_class(r, Y, lane);
+        for (int r = warp; r < BB; r += NW) cls_class(r, Y, lane);
     __syncthreads();
 
     // ---- 2: carries over segment `warp` (carry-in 0) and its residue mod o
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(224, 2) k_interp_top_cls(const uint32_t* __res
                 d = (d > 0) ? (nv == 0u ? 1 : 0) : (v == 0u ? -1 : 0);
             }
             c = (long long)(int32_t)CO[s * G + lane] + d;
-            T = (uint32_t)(((T + RH[s * G + lane]) % o) * (uint32_t)pw.ip[Ls == 73 ? 0 : 1] % o);
+            T = (uint32_t)(((T + RH[s * G + lane]) % o) * (uint32_t)pw.ip[Ls == 36 ? 0 : 1] % o);
         }
     }
     __syncthreads();
@@ -296,7 +307,7 @@ __global__ void __launch_bounds__(224, 2) k_interp_top_cls(const uint32_t* __res
         uint32_t* row = w + (c0 + lane) * (size_t)WOUT;
         const bool v4 = (((uintptr_t)w) & 15) == 0;
 #pragma unroll 1
-        for (int g = warp; g < WOUT / 4; g += NP) {
+        for (int g = warp; g < WOUT / 4; g += NW) {
             const int P = 4 * g;
             const uint32_t* pq = Y + cls_lo(P) + lane;
             uint32_t q[5];
