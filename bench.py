@@ -334,15 +334,19 @@ def main():
     lp_per_product = algorithmic_lp(n, B, C2["t4"], C2["t3"])
     # per-launch algorithmic work of the three kernels of a C2 step:
     #   eval   (k_eval_top_v4<4>)       : read u, v; write the 7 evaluated pairs
-    #   fused  (k_fused_bottom<4,18>)   : SURVEY §8(d)'s 14439 limb-products per
-    #                                     product (real child lengths, not 7 x 18^2 x 7)
-    #   interp (k_interp_top_smem<4>)   : read the 7 products; write w
+    #   bottom (k_fused_c2_dc, or k_fused_bottom<4,18> in c2 mode 0/1): SURVEY
+    #          §8(d)'s 14439 limb-products per product (real child lengths, not
+    #          7 x 18^2 x 7)
+    #   interp (k_interp_top_cls<DEF>, or k_interp_top_smem<4> in mode 0):
+    #          read the 7 products; write w
+    c2m = plan.get("c2_mode", 0)
     kern = {
         "eval": dict(name="k_eval_top_v4<4>", bound="hbm",
                      units=2 * (L0["count"] * L0["n"] + L0["count"] * L0["npts"] * L0["e"]) * 4),
-        "base": dict(name="k_fused_bottom<4,18>", bound="alu", units=batch * lp_per_product,
+        "base": dict(name="k_fused_c2_dc" if c2m == 2 else "k_fused_bottom<4,18>", bound="alu",
+                     units=batch * lp_per_product,
                      bytes=(2 * L1["count"] * L1["n"] + L1["count"] * 2 * L1["n"]) * 4),
-        "interp": dict(name="k_interp_top_smem<4>", bound="hbm",
+        "interp": dict(name=("k_interp_top_cls<%d>" % (c2m == 2)) if c2m else "k_interp_top_smem<4>", bound="hbm",
                        units=(L0["count"] * L0["npts"] * 2 * L0["e"] + L0["count"] * 2 * L0["n"]) * 4),
     }
     traffic = {}

@@ -3124,8 +3124,8 @@ size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t* plan, char*
         js += tmp;
     }
     char tail[128];
-    snprintf(tail, sizeof tail, "], \"workspace_bytes\": %zu, \"fused_bottom\": %s}", pl.bytes,
-             pl.fused ? "true" : "false");
+    snprintf(tail, sizeof tail, "], \"workspace_bytes\": %zu, \"fused_bottom\": %s, \"c2_mode\": %d}", pl.bytes,
+             pl.fused ? "true" : "false", pl.c2mode);
     js += tail;
     if (buf && len) {
         size_t k = js.size() < len - 1 ? js.size() : len - 1;

@@ -13,6 +13,7 @@ for r in rows[2:]:
     name = r[ki].split("(")[0].replace("void ", "").replace("tg::", "").replace(" ", "")
     name = re.sub(r"^k_fused_bottom<(\d+),(\d+).*>$", r"k_fused_bottom<\1,\2>", name)
     name = re.sub(r"<(\d+),.*>$", r"<\1>", name) if name.startswith("k_interp_top_smem") else name
+    name = name.replace("<true>", "<1>").replace("<false>", "<0>")
     b = float(r[ri].replace(",", "")) * scale[units[ri]] + float(r[wi].replace(",", "")) * scale[units[wi]]
     res.setdefault(name, b)
 json.dump(res, sys.stdout, indent=1)

@@ -91,3 +91,17 @@ def test_workspace_grows_with_batch():
     a = tg.workspace_bytes(256, 1024, B=4, t4=32, t3=32)
     b = tg.workspace_bytes(256, 4096, B=4, t4=32, t3=32)
     assert 0 < a < b
+
+
+def test_c2_plan_uses_the_common_denominator_kernels():
+    """C2 (BASELINE configs[1]): c2 mode 2 (deferred bottom + top by classes,
+    DESIGN.md reading 18); other shapes keep the per-row kernels."""
+    assert tg.plan_describe(256, 65536, B=4, t4=32, t3=32)["c2_mode"] == 2
+    assert tg.plan_describe(256, 1000, B=4, t4=32, t3=32)["c2_mode"] == 2
+    assert tg.plan_describe(96, 260, B=3, t4=10**9, t3=10**9)["c2_mode"] == 0
+    assert tg.plan_describe(2048, 4096, B=8)["c2_mode"] == 0
+    tg.set_c2_mode(0)
+    try:
+        assert tg.plan_describe(256, 65536, B=4, t4=32, t3=32)["c2_mode"] == 0
+    finally:
+        tg.set_c2_mode(2)
