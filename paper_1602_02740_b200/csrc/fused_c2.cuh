@@ -116,6 +116,33 @@ __device__ __forceinline__ void c2dc_class(int r, uint32_t* Y, const uint32_t* S
     for (int h = 0; h < 4; ++h) col1[(1 + h) * W2 * G] = hw[2 * h] | (hw[2 * h + 1] << 16);
 }
 
+// B2 run: X[P] = lo + hi 2^32 (hi the HALF of a packed cell) plus the carry;
+// limb 0 of the segment stays in its lo cell (written after B3), the others
+// go to out[P * count]
+template <bool HALF>
+__device__ __forceinline__ void c2dc_carry_run(uint32_t* pl, const uint32_t* ph, uint32_t* po, size_t count, int n,
+                                               bool first, bool valid, long long& carry) {
+    int i = 0;
+    if (first) {   // limb 0 of the segment
+        const uint32_t h = ph[0];
+        const int32_t hs = HALF ? ((int32_t)h >> 16) : ((int32_t)(h << 16) >> 16);
+        const long long x = (long long)(((unsigned long long)(uint32_t)hs << 32) | pl[0]) + carry;
+        carry = x >> 32;
+        pl[0] = (uint32_t)x;
+        po += count;
+        i = 1;
+    }
+#pragma unroll 4
+    for (; i < n; ++i) {
+        const uint32_t h = ph[i * c2dc::G];
+        const int32_t hs = HALF ? ((int32_t)h >> 16) : ((int32_t)(h << 16) >> 16);
+        const long long x = (long long)(((unsigned long long)(uint32_t)hs << 32) | pl[i * c2dc::G]) + carry;
+        carry = x >> 32;
+        if (valid) *po = (uint32_t)x;
+        po += count;
+    }
+}
+
 __host__ __device__ constexpr size_t c2dc_smem_bytes() {
     return (size_t)4 * (c2dc::NP * c2dc::W2 * c2dc::G + 2 * 4 * c2dc::E * c2dc::PP + c2dc::NP * c2dc::G);
 }
@@ -191,38 +218,23 @@ __global__ void __launch_bounds__(224, 4) k_fused_c2_dc(const uint32_t* __restri
     for (int r = warp; r < BB; r += NP) c2dc_class(r, Y, SG, lane);
     __syncthreads();
 
-    // ---- B2: carry pass over segment `warp` with carry-in 0
+    // ---- B2: carry pass over segment `warp` with carry-in 0, in runs of
+    // constant m = P / 17 (consecutive cells at stride G)
     {
         const int P0 = seg0(warp), L = seg0(warp + 1) - P0;
-        int m = P0 / BB, r = P0 - BB * m;
-        auto plo = [&](int mm) { return Y + (mm < 7 ? mm * W2 : BB) * G + lane; };
-        auto phi = [&](int mm) { return Y + ((1 + (mm >> 1)) * W2 + BB) * G + lane; };
-        const uint32_t* pl = plo(m) + r * G;
-        const uint32_t* ph = phi(m) + r * G;
-        int hs = (m & 1) ? 0 : 16;
         uint32_t* po = out + (size_t)P0 * count + c;
         long long carry = 0;
-        uint32_t l0 = 0;
-        for (int q = 0; q < L; ++q) {
-            const long long hi = (long long)((int32_t)(*ph << hs) >> 16);
-            const long long x = (long long)*pl + (hi << 32) + carry;
-            const uint32_t limb = (uint32_t)x;
-            carry = x >> 32;
-            if (q == 0) l0 = limb;
-            else if (valid) *po = limb;
-            po += count;
-            if (++r == BB) {
-                r = 0;
-                ++m;
-                pl = plo(m);
-                ph = phi(m);
-                hs = (m & 1) ? 0 : 16;
-            } else {
-                pl += G;
-                ph += G;
-            }
+        for (int P = P0; P < P0 + L;) {
+            const int m = P / BB, r = P - BB * m;
+            const int n = min(P0 + L, BB * (m + 1)) - P;
+            uint32_t* pl = Y + ((m < 7 ? m * W2 : BB) + r) * G + lane;
+            const uint32_t* ph = Y + ((1 + (m >> 1)) * W2 + BB + r) * G + lane;
+            if (m & 1) c2dc_carry_run<true>(pl, ph, po, count, n, P == P0, valid, carry);
+            else c2dc_carry_run<false>(pl, ph, po, count, n, P == P0, valid, carry);
+            po += (size_t)n * count;
+            P += n;
         }
-        L0[warp * G + lane] = l0;
+        L0[warp * G + lane] = Y[(P0 / BB < 7 ? (P0 / BB) * W2 : BB) * G + (P0 % BB) * G + lane];
         CO[warp * G + lane] = (uint32_t)(int32_t)carry;
     }
     __syncthreads();
