@@ -143,6 +143,56 @@ __device__ __forceinline__ void c2dc_carry_run(uint32_t* pl, const uint32_t* ph,
     }
 }
 
+// phase A evaluation on the ALU pipe: the Toom-4 point coefficients are 0,
+// +-1, +-2^s (s <= 3), so each term is two funnel shifts and a 64-bit add or
+// subtract instead of an IMAD.WIDE / IMAD.SHL + IMAD.HI (the fma pipe carries
+// the base products)
+__device__ __forceinline__ uint32_t c2dc_shl(uint32_t x, int s) {
+    uint32_t r;
+    asm("shf.l.clamp.b32 %0, 0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+__device__ __forceinline__ uint32_t c2dc_shr(uint32_t x, int s) {   // x >> (32 - s), 0 < s < 32
+    uint32_t r;
+    asm("shf.l.clamp.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+template <long long C>
+__device__ __forceinline__ void c2dc_eterm(uint64_t& acc, uint32_t x) {
+    if constexpr (C == 1) acc += x;
+    else if constexpr (C == -1) acc -= x;
+    else if constexpr (C != 0) {
+        constexpr long long A = C < 0 ? -C : C;
+        constexpr int S = A == 2 ? 1 : (A == 4 ? 2 : 3);
+        static_assert(A == (1ll << S), "Toom-4 point coefficients are powers of two");
+        const uint64_t t = ((uint64_t)c2dc_shr(x, S) << 32) | c2dc_shl(x, S);
+        if constexpr (C > 0) acc += t;
+        else acc -= t;
+    }
+}
+template <int K>
+__device__ __forceinline__ void c2dc_eval(const uint32_t* __restrict__ PU, const uint32_t* __restrict__ PV,
+                                          uint32_t* __restrict__ dU, uint32_t* __restrict__ dV) {
+    using namespace c2dc;
+    uint64_t cu = 0, cv = 0;
+#pragma unroll 1
+    for (int t = 0; t < E; ++t) {
+        uint64_t au = (uint64_t)((int64_t)cu >> 32), av = (uint64_t)((int64_t)cv >> 32);
+        c2dc_eterm<tg_evalc_cx_T4(K, 0)>(au, PU[t * PP]);
+        c2dc_eterm<tg_evalc_cx_T4(K, 0)>(av, PV[t * PP]);
+        c2dc_eterm<tg_evalc_cx_T4(K, 1)>(au, PU[(E + t) * PP]);
+        c2dc_eterm<tg_evalc_cx_T4(K, 1)>(av, PV[(E + t) * PP]);
+        c2dc_eterm<tg_evalc_cx_T4(K, 2)>(au, PU[(2 * E + t) * PP]);
+        c2dc_eterm<tg_evalc_cx_T4(K, 2)>(av, PV[(2 * E + t) * PP]);
+        c2dc_eterm<tg_evalc_cx_T4(K, 3)>(au, PU[(3 * E + t) * PP]);
+        c2dc_eterm<tg_evalc_cx_T4(K, 3)>(av, PV[(3 * E + t) * PP]);
+        dU[t * G] = (uint32_t)au;
+        dV[t * G] = (uint32_t)av;
+        cu = au;
+        cv = av;
+    }
+}
+
 __host__ __device__ constexpr size_t c2dc_smem_bytes() {
     return (size_t)4 * (c2dc::NP * c2dc::W2 * c2dc::G + 2 * 4 * c2dc::E * c2dc::PP + c2dc::NP * c2dc::G);
 }
@@ -205,7 +255,15 @@ __global__ void __launch_bounds__(224, 4) k_fused_c2_dc(const uint32_t* __restri
     // ---- A: point `warp`, product into the warp's slot
     {
         uint32_t* slot = Y + (warp * W2) * G + lane;
-        eval_point_rows<4, E>(warp, Pu + lane, Pv + lane, slot, slot + E * G);
+        switch (warp) {
+            case 0: c2dc_eval<0>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 1: c2dc_eval<1>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 2: c2dc_eval<2>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 3: c2dc_eval<3>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 4: c2dc_eval<4>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 5: c2dc_eval<5>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            default: c2dc_eval<6>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+        }
         uint32_t a[E], bb[E];
 #pragma unroll
         for (int t = 0; t < E; ++t) { a[t] = slot[t * G]; bb[t] = slot[(E + t) * G]; }
