@@ -334,7 +334,7 @@ def main():
     lp_per_product = algorithmic_lp(n, B, C2["t4"], C2["t3"])
     # per-launch algorithmic work of the three kernels of a C2 step:
     #   eval   (k_eval_top_v4<4>)       : read u, v; write the 7 evaluated pairs
-    #   bottom (k_fused_c2_dc, or k_fused_bottom<4,18> in c2 mode 0/1): SURVEY
+    #   bottom (k_fused_dc<4>, or k_fused_bottom<4,18> in c2 mode 0/1): SURVEY
     #          §8(d)'s 14439 limb-products per product (real child lengths, not
     #          7 x 18^2 x 7)
     #   interp (k_interp_top_cls<DEF>, or k_interp_top_smem<4> in mode 0):
@@ -343,7 +343,7 @@ def main():
     kern = {
         "eval": dict(name="k_eval_top_v4<4>", bound="hbm",
                      units=2 * (L0["count"] * L0["n"] + L0["count"] * L0["npts"] * L0["e"]) * 4),
-        "base": dict(name="k_fused_c2_dc" if c2m == 2 else "k_fused_bottom<4,18>", bound="alu",
+        "base": dict(name="k_fused_dc<4>" if c2m == 2 else "k_fused_bottom<4,18>", bound="alu",
                      units=batch * lp_per_product,
                      bytes=(2 * L1["count"] * L1["n"] + L1["count"] * 2 * L1["n"]) * 4),
         "interp": dict(name=("k_interp_top_cls<%d>" % (c2m == 2)) if c2m else "k_interp_top_smem<4>", bound="hbm",

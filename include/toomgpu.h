@@ -237,6 +237,13 @@ void toom_set_t16_matrix(int on);
  * Affects later calls only.                                              */
 void toom_set_c2_mode(int mode);
 
+/* Single large products (C4, C5): 1 (default) = the Toom-3 bottom level
+ * right under the lazy Toom-4 levels forms X = 6 y without dividing
+ * (PAPER.md:162 matrix form) and the factor 6 joins the lazy block's
+ * finishing division (readings 18, 19); 0 = the bottom divides
+ * its rows itself.  Same results; tests compare both.  Affects later calls. */
+void toom_set_lazy_bottom(int on);
+
 /* ---- stage exports (tests, bench) ------------------------------------- */
 
 /* Base case alone (step a3): batched schoolbook of signed two's-complement

@@ -75,6 +75,7 @@ SIGNATURES = {
     "toom_sqr_batched": (_I, [_P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
     "toom_set_t16_matrix": (None, [_I]),
     "toom_set_c2_mode": (None, [_I]),
+    "toom_set_lazy_bottom": (None, [_I]),
     "toom_set_verify": (None, [_I]),
     "toom_debug_fault": (None, [_I]),
 }
@@ -362,6 +363,12 @@ def set_c2_mode(mode: int = 2):
     """C2-shaped batches: 2 = deferred bottom + one top division by 360^2
     (default), 1 = top division by 360 over per-row bottom, 0 = per-row both."""
     lib().toom_set_c2_mode(int(mode))
+
+
+def set_lazy_bottom(on: bool = True):
+    """Single large products: the Toom-3 bottom under the lazy levels hands up
+    X = 6 y (default) or divides its rows itself."""
+    lib().toom_set_lazy_bottom(1 if on else 0)
 
 
 def toom_mul_ntt(u: torch.Tensor, v: torch.Tensor, B: int = 16, out: torch.Tensor | None = None,

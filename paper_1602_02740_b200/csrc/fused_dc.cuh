@@ -1,0 +1,362 @@
+// The bottom Toom level of a batch with the common denominator of its
+// interpolation DEFERRED to the level above (reading 18), for the
+// two static shapes that carry it:
+//   B = 4: C2's bottom (65-limb signed parents, b = 17, 18-limb products),
+//          X = 360 y handed to the top level (csrc/toplevel_cls.cuh, which
+//          divides by 360^2);
+//   B = 3: the bottom under the lazy levels of C4/C5 (66-limb parents,
+//          b = 22, 23-limb products), X = 6 y handed to the lazy block,
+//          whose finishing division (csrc/lazy.cuh) takes the factor 6 too.
+//
+// The per-coefficient matrix form over the common denominator Dc
+// (reading 12):
+//     Dc * w = X = sum_j 2^(32 b j) N_j,   N_j = sum_k A'_jk y_k
+// has no division, so it is elementwise in the limb position: limb P of X is
+//     X[P] = sum_j sum_k A'_jk y_k[P - b j]          (|X[P]| < 2^46)
+// which every thread of the CTA can form for any position (no serial row
+// chains, no per-row exact division).  One carry pass normalises X modulo
+// 2^(32 * 2n); X = Dc w fits the 2n signed limbs of the product slot for both
+// shapes (C2: |y| < 225 2^4096; C4/C5: |y| < 225 2^4160).
+//
+// CTA = 32 parents (one per lane) x NP = 2B - 1 warps:
+//   A0  stage the parents' blocks in smem (row l of the source is block
+//       l / b, limb l % b; one pad row per warp)
+//   A   warp k: evaluate U(x_k), V(x_k) (funnel shifts: the coefficients are
+//       powers of two), multiply (register Comba) into the warp's product
+//       slot Y[k][2E][32]; the product's sign to SG[k]
+//   B1  class r = P mod b (warp w: r = w, w + NP, ...): the columns t = r,
+//       r + b (, r + 2b) of the products give X[r + b m]; a class reads and
+//       then overwrites only its own columns (lo words in (k = m, t = r),
+//       packed 16-bit high words in (k = 1 + m/2, t = r + b)), so no barrier
+//       separates the reads and the writes
+//   B2  warp w: carry pass over its segment of positions (carry-in 0),
+//       limbs 1.. written (interleaved), limb 0 and the carry-out kept
+//   B3  warp 0: the segments' carries in order; limb 0 written, a carry
+//       that wraps limb 0 (probability ~2^-17) ripples through the segment
+#pragma once
+
+namespace tg {
+
+template <int B> struct DcShape;
+template <> struct DcShape<4> {   // C2 bottom
+    static constexpr int NP = 7, N = 65, BB = 17, E = 18;
+    static constexpr int Dc = tg_combO_T4 << tg_combS_T4;   // 360
+    __host__ __device__ static constexpr long long A(int j, int k) { return tg_combA_cx_T4(j, k); }
+    __host__ __device__ static constexpr long long C(int k, int j) { return tg_evalc_cx_T4(k, j); }
+};
+template <> struct DcShape<3> {   // bottom under the lazy levels (C4, C5)
+    static constexpr int NP = 5, N = 66, BB = 22, E = 23;
+    static constexpr int Dc = tg_combO_T3 << tg_combS_T3;   // 6
+    __host__ __device__ static constexpr long long A(int j, int k) { return tg_combA_cx_T3(j, k); }
+    __host__ __device__ static constexpr long long C(int k, int j) { return tg_evalc_cx_T3(k, j); }
+};
+template <int B> struct DcGeo : DcShape<B> {
+    using S = DcShape<B>;
+    static constexpr int G = 32, PP = 33, W2 = 2 * S::E, WOUT = 2 * S::N, NSEG = S::NP;
+    static constexpr int MMAX = (WOUT - 1) / S::BB;          // X[r + b m], m = 0..MMAX
+    static_assert(W2 == 2 * S::BB + 2, "product columns r, r + b, r + 2b (<= 2b + 1) and the sign column 2b + 2");
+    static_assert(MMAX == S::NP && 1 + (MMAX >> 1) <= S::NP - 1, "class cells: lo (m, r) / (0, r + b), hi (1 + m/2, r + b)");
+    static_assert(B * S::E - S::N <= S::NP, "one pad row per warp");
+    // segment s of the carry pass: positions [seg0(s), seg0(s + 1))
+    __host__ __device__ static constexpr int seg0(int s) { return (WOUT / NSEG) * s + (s < WOUT % NSEG ? s : WOUT % NSEG); }
+};
+static_assert(DcGeo<4>::seg0(7) == 130 && DcGeo<3>::seg0(5) == 132, "segments cover the output limbs");
+static_assert(DcShape<4>::Dc == 360 && DcShape<3>::Dc == 6, "common denominators");
+
+// X[r + b m] of class r from the columns t = r + b i of the products
+template <int B, int J, int K>
+__device__ __forceinline__ void dc_cterm(uint32_t y, uint64_t& p, uint64_t& n) {
+    constexpr long long A = DcShape<B>::A(J, K);   // folded at compile time
+    if constexpr (A > 0) p = tg_madw((uint32_t)A, y, p);
+    else if constexpr (A < 0) n = tg_madw((uint32_t)(-A), y, n);
+}
+template <int B, int J>
+__device__ __forceinline__ void dc_row(const uint32_t (&y)[2 * B - 1], uint64_t& p, uint64_t& n) {
+    dc_cterm<B, J, 0>(y[0], p, n);
+    dc_cterm<B, J, 1>(y[1], p, n);
+    dc_cterm<B, J, 2>(y[2], p, n);
+    dc_cterm<B, J, 3>(y[3], p, n);
+    dc_cterm<B, J, 4>(y[4], p, n);
+    if constexpr (B == 4) {
+        dc_cterm<B, J, 5>(y[5], p, n);
+        dc_cterm<B, J, 6>(y[6], p, n);
+    }
+}
+template <int B, int I, int J = 0>
+__device__ __forceinline__ void dc_column(const uint32_t (&y)[2 * B - 1], uint64_t (&aP)[DcGeo<B>::MMAX + 1],
+                                          uint64_t (&aN)[DcGeo<B>::MMAX + 1]) {
+    if constexpr (J < 2 * B - 1 && I + J <= DcGeo<B>::MMAX) {
+        dc_row<B, J>(y, aP[I + J], aN[I + J]);
+        dc_column<B, I, J + 1>(y, aP, aN);
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void dc_class(int r, uint32_t* Y, const uint32_t* SG, int lane) {
+    using Gm = DcGeo<B>;
+    constexpr int NP = Gm::NP, G = Gm::G, W2 = Gm::W2, BB = Gm::BB, MM = Gm::MMAX + 1;
+    uint64_t aP[MM], aN[MM];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) aP[m] = aN[m] = 0ull;
+    uint32_t* col0 = Y + r * G + lane;          // cells (k, t = r)
+    uint32_t* col1 = col0 + BB * G;             // cells (k, t = r + b)
+    {
+        uint32_t y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = col0[k * W2 * G];
+        dc_column<B, 0>(y, aP, aN);
+    }
+    {
+        uint32_t y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = col1[k * W2 * G];
+        dc_column<B, 1>(y, aP, aN);
+    }
+    if (r < 2) {            // t = r + 2b (the stored columns 2b, 2b + 1)
+        uint32_t y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = col1[(k * W2 + BB) * G];
+        dc_column<B, 2>(y, aP, aN);
+    } else if (r == 2) {    // t = 2b + 2: the sign terms, y_k = -s_k (two's complement products)
+        uint32_t s[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) s[k] = SG[k * G + lane];
+        dc_column<B, 2>(s, aN, aP);   // -A s: the positive and negative sums swap
+    }
+    // X[r + b m] = aP - aN: lo words in (k = m, t = r) (m = MMAX: (0, r + b)),
+    // high words (|X| < 2^46: 16 bits) packed two per cell in (1 + m/2, r + b)
+    uint32_t hw[MM + 1];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+        const uint64_t x = aP[m] - aN[m];
+        if (m < MM - 1) col0[m * W2 * G] = (uint32_t)x;
+        hw[m] = (uint32_t)(x >> 32) & 0xFFFFu;
+    }
+    hw[MM] = 0u;
+    if (r + BB * (MM - 1) < Gm::WOUT) col1[0] = (uint32_t)(aP[MM - 1] - aN[MM - 1]);
+#pragma unroll
+    for (int h = 0; 2 * h < MM; ++h) col1[(1 + h) * W2 * G] = hw[2 * h] | (hw[2 * h + 1] << 16);
+}
+
+// B2 run: X[P] = lo + hi 2^32 (hi the HALF of a packed cell) plus the carry;
+// limb 0 of the segment stays in its lo cell (written after B3), the others
+// go to out[P * count]
+template <bool HALF>
+__device__ __forceinline__ void dc_carry_run(uint32_t* pl, const uint32_t* ph, uint32_t* po, size_t count, int n,
+                                             bool first, bool valid, long long& carry) {
+    int i = 0;
+    if (first) {   // limb 0 of the segment
+        const uint32_t h = ph[0];
+        const int32_t hs = HALF ? ((int32_t)h >> 16) : ((int32_t)(h << 16) >> 16);
+        const long long x = (long long)(((unsigned long long)(uint32_t)hs << 32) | pl[0]) + carry;
+        carry = x >> 32;
+        pl[0] = (uint32_t)x;
+        po += count;
+        i = 1;
+    }
+#pragma unroll 4
+    for (; i < n; ++i) {
+        const uint32_t h = ph[i * 32];
+        const int32_t hs = HALF ? ((int32_t)h >> 16) : ((int32_t)(h << 16) >> 16);
+        const long long x = (long long)(((unsigned long long)(uint32_t)hs << 32) | pl[i * 32]) + carry;
+        carry = x >> 32;
+        if (valid) *po = (uint32_t)x;
+        po += count;
+    }
+}
+
+// phase A evaluation on the ALU pipe: the Toom-3/4 point coefficients are 0,
+// +-1, +-2^s (s <= 3), so each term is two funnel shifts and a 64-bit add or
+// subtract instead of an IMAD.WIDE / IMAD.SHL + IMAD.HI (the fma pipe carries
+// the base products)
+__device__ __forceinline__ uint32_t dc_shl(uint32_t x, int s) {
+    uint32_t r;
+    asm("shf.l.clamp.b32 %0, 0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+__device__ __forceinline__ uint32_t dc_shr(uint32_t x, int s) {   // x >> (32 - s), 0 < s < 32
+    uint32_t r;
+    asm("shf.l.clamp.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+template <long long C>
+__device__ __forceinline__ void dc_eterm(uint64_t& acc, uint32_t x) {
+    if constexpr (C == 1) acc += x;
+    else if constexpr (C == -1) acc -= x;
+    else if constexpr (C != 0) {
+        constexpr long long A = C < 0 ? -C : C;
+        constexpr int S = A == 2 ? 1 : (A == 4 ? 2 : 3);
+        static_assert(A == (1ll << S), "Toom-3/4 point coefficients are powers of two");
+        const uint64_t t = ((uint64_t)dc_shr(x, S) << 32) | dc_shl(x, S);
+        if constexpr (C > 0) acc += t;
+        else acc -= t;
+    }
+}
+template <int B, int K, int J = 0>
+__device__ __forceinline__ void dc_eval_terms(const uint32_t* PU, const uint32_t* PV, int t, uint64_t& au, uint64_t& av) {
+    if constexpr (J < B) {
+        constexpr int E = DcShape<B>::E, PP = 33;
+        dc_eterm<DcShape<B>::C(K, J)>(au, PU[(J * E + t) * PP]);
+        dc_eterm<DcShape<B>::C(K, J)>(av, PV[(J * E + t) * PP]);
+        dc_eval_terms<B, K, J + 1>(PU, PV, t, au, av);
+    }
+}
+template <int B, int K>
+__device__ __forceinline__ void dc_eval(const uint32_t* __restrict__ PU, const uint32_t* __restrict__ PV,
+                                        uint32_t* __restrict__ dU, uint32_t* __restrict__ dV) {
+    uint64_t cu = 0, cv = 0;
+#pragma unroll 1
+    for (int t = 0; t < DcShape<B>::E; ++t) {
+        uint64_t au = (uint64_t)((int64_t)cu >> 32), av = (uint64_t)((int64_t)cv >> 32);
+        dc_eval_terms<B, K>(PU, PV, t, au, av);
+        dU[t * 32] = (uint32_t)au;
+        dV[t * 32] = (uint32_t)av;
+        cu = au;
+        cv = av;
+    }
+}
+
+template <int B>
+__host__ __device__ constexpr size_t dc_smem_bytes() {
+    using Gm = DcGeo<B>;
+    return (size_t)4 * (Gm::NP * Gm::W2 * Gm::G + 2 * B * Gm::E * Gm::PP + Gm::NP * Gm::G);
+}
+
+template <int B>
+__global__ void __launch_bounds__(32 * (2 * B - 1), 4) k_fused_dc(const uint32_t* __restrict__ srcU,
+                                                                             const uint32_t* __restrict__ srcV,
+                                                                             uint32_t* __restrict__ out, size_t count) {
+    using Gm = DcGeo<B>;
+    constexpr int NP = Gm::NP, N = Gm::N, BB = Gm::BB, E = Gm::E, G = Gm::G, PP = Gm::PP, W2 = Gm::W2,
+                  NSEG = Gm::NSEG;
+    extern __shared__ uint32_t sm[];
+    uint32_t* Y = sm;                       // [NP][2E][32] products, then X (class cells)
+    uint32_t* Pu = Y + NP * W2 * G;         // [B * E][33] staged parents
+    uint32_t* Pv = Pu + B * E * PP;
+    uint32_t* SG = Pv + B * E * PP;         // [NP][32] product signs
+    uint32_t* L0 = Pu;                      // after phase A: [NSEG][32] segment limb 0
+    uint32_t* CO = Pu + NSEG * G;           //                [NSEG][32] segment carry-out
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t c0 = (size_t)blockIdx.x * G;
+    const int nin = (int)min((size_t)G, count - c0);
+    const bool valid = lane < nin;
+    const size_t c = c0 + lane;
+
+    // ---- A0: source row l (limb l of the parent) is block j = min(l / b,
+    // B - 1), limb l - j b, smem row j E + l - j b = l + j (E = b + 1); the
+    // B E - n pad rows: j E + b (zero, j < B - 1), then the top block's
+    // (B - 1) E + [lentop, E) (its sign fill)
+    {
+        constexpr int IT = (N + NP - 1) / NP, LT = N - (B - 1) * BB, ZP = B - 1, NPAD = B * E - N;
+        const size_t stp = (size_t)NP * count;
+        const uint32_t* pu = srcU + (size_t)warp * count + c;
+        const uint32_t* pv = srcV + (size_t)warp * count + c;
+        uint32_t xu[IT], xv[IT];
+#pragma unroll
+        for (int q = 0; q < IT; ++q) {
+            const int l = warp + NP * q;
+            xu[q] = xv[q] = 0u;
+            if (l < N && valid) {
+                xu[q] = __ldg(pu);
+                xv[q] = __ldg(pv);
+            }
+            pu += stp;
+            pv += stp;
+        }
+        uint32_t fu = 0u, fv = 0u;
+        if (warp >= ZP && warp < NPAD && valid) {
+            fu = (__ldg(srcU + (size_t)(N - 1) * count + c) >> 31) ? 0xFFFFFFFFu : 0u;
+            fv = (__ldg(srcV + (size_t)(N - 1) * count + c) >> 31) ? 0xFFFFFFFFu : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < IT; ++q) {
+            const int l = warp + NP * q;
+            if (l < N) {
+                const int row = l + min(l / BB, B - 1);
+                Pu[row * PP + lane] = xu[q];
+                Pv[row * PP + lane] = xv[q];
+            }
+        }
+        if (warp < NPAD) {
+            const int pr = warp < ZP ? warp * E + BB : (B - 1) * E + LT + (warp - ZP);
+            Pu[pr * PP + lane] = fu;
+            Pv[pr * PP + lane] = fv;
+        }
+    }
+    __syncthreads();
+
+    // ---- A: point `warp`, product into the warp's slot
+    {
+        uint32_t* slot = Y + (warp * W2) * G + lane;
+        switch (warp) {
+            case 0: dc_eval<B, 0>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 1: dc_eval<B, 1>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 2: dc_eval<B, 2>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 3: dc_eval<B, 3>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 4: dc_eval<B, 4>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            case 5: if constexpr (B == 4) dc_eval<B, 5>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+            default: if constexpr (B == 4) dc_eval<B, 6>(Pu + lane, Pv + lane, slot, slot + E * G); break;
+        }
+        uint32_t a[E], bb[E];
+#pragma unroll
+        for (int t = 0; t < E; ++t) { a[t] = slot[t * G]; bb[t] = slot[(E + t) * G]; }
+        mul_twos_to_smem<E>(a, bb, slot);
+        SG[warp * G + lane] = slot[(W2 - 1) * G] >> 31;
+    }
+    __syncthreads();
+
+    // ---- B1: the classes r = warp, warp + NP, ...
+    for (int r = warp; r < BB; r += NP) dc_class<B>(r, Y, SG, lane);
+    __syncthreads();
+
+    // ---- B2: carry pass over segment `warp` with carry-in 0, in runs of
+    // constant m = P / b (consecutive cells at stride G)
+    {
+        const int P0 = Gm::seg0(warp), L = Gm::seg0(warp + 1) - P0;
+        uint32_t* po = out + (size_t)P0 * count + c;
+        long long carry = 0;
+        for (int P = P0; P < P0 + L;) {
+            const int m = P / BB, r = P - BB * m;
+            const int n = min(P0 + L, BB * (m + 1)) - P;
+            uint32_t* pl = Y + ((m < NP ? m * W2 : BB) + r) * G + lane;
+            const uint32_t* ph = Y + ((1 + (m >> 1)) * W2 + BB + r) * G + lane;
+            if (m & 1) dc_carry_run<true>(pl, ph, po, count, n, P == P0, valid, carry);
+            else dc_carry_run<false>(pl, ph, po, count, n, P == P0, valid, carry);
+            po += (size_t)n * count;
+            P += n;
+        }
+        const int m0 = P0 / BB;
+        L0[warp * G + lane] = Y[((m0 < NP ? m0 * W2 : BB) + P0 - BB * m0) * G + lane];
+        CO[warp * G + lane] = (uint32_t)(int32_t)carry;
+    }
+    __syncthreads();
+
+    // ---- B3: carries between the segments (one lane per parent)
+    if (warp != 0 || !valid) return;
+    long long cin = 0;
+#pragma unroll 1
+    for (int s = 0; s < NSEG; ++s) {
+        const int P0 = Gm::seg0(s), L = Gm::seg0(s + 1) - P0;
+        const long long x = (long long)L0[s * G + lane] + cin;
+        uint32_t* po = out + (size_t)P0 * count + c;
+        // fault injection (tests): X_0 = Dc y_0 of the first
+        // parent made odd, so the division by Dc above is not exact (its
+        // check of the low bits catches it)
+        const uint32_t flt = (tg_fault && s == 0 && c == 0) ? 1u : 0u;
+        *po = (uint32_t)x ^ flt;
+        long long d = x >> 32;   // -1, 0, +1
+        cin = (long long)(int32_t)CO[s * G + lane];
+        if (d != 0) {            // rare: limb 0 wrapped
+            for (int q = 1; q < L && d != 0; ++q) {
+                po += count;
+                const uint32_t v = *po;
+                const uint32_t nv = v + (uint32_t)d;
+                *po = nv;
+                d = (d > 0) ? (nv == 0u ? 1 : 0) : (v == 0u ? -1 : 0);
+            }
+            cin += d;
+        }
+    }
+}
+
+}  // namespace tg

@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(128) k_interp_p8(const uint32_t* __restrict__ 
 
 }  // namespace tg
 #include "fused_bottom.cuh"
-#include "fused_c2.cuh"
+#include "fused_dc.cuh"
 #include "longvec.cuh"
 #include "longvec2.cuh"
 #include "level34.cuh"
@@ -421,7 +421,8 @@ struct Plan {
     size_t offEDesc = 0;     // multi-output evaluation descriptors
     size_t offBDesc = 0;     // wide-multiplier multi-output descriptors (matrix-form T16)
     bool top_warp = false;   // top interpolation one warp per product (fused level writes row-major)
-    int c2mode = 0;          // C2 shape: 1 top level by classes (toplevel_cls.cuh), 2 + deferred bottom (fused_c2.cuh)
+    int c2mode = 0;          // C2 shape: 1 top level by classes (toplevel_cls.cuh), 2 + deferred bottom (fused_dc.cuh)
+    bool lzdc = false;       // T3 bottom under the lazy block: X = 6 y, the factor joins the finishing division
     // lazy block [lz0, lz1) of long levels (csrc/lazy.cuh): the product of
     // their common denominators 2^lz_s lz_o, the top lazy output X and the
     // two-pass tile records of the finishing scans
@@ -535,8 +536,15 @@ static bool g_t16_matrix = [] {
 }();
 // C2-shaped batches: the top level as one division over the common
 // denominator (csrc/toplevel_cls.cuh) and the bottom level with that
-// denominator deferred to it (csrc/fused_c2.cuh); TOOM_C2_CLS=0 /
+// denominator deferred to it (csrc/fused_dc.cuh); TOOM_C2_CLS=0 /
 // TOOM_DEFERRED_BOTTOM=0 run the per-row kernels instead (tests compare all)
+// the Toom-3 bottom under the lazy levels (C4, C5) with its denominator 6
+// deferred into the lazy block's finishing division (csrc/fused_dc.cuh);
+// TOOM_LAZY_BOTTOM_DC=0 runs the per-row fused kernel instead
+static bool g_lzdc = [] {
+    const char* e = getenv("TOOM_LAZY_BOTTOM_DC");
+    return e ? atoi(e) != 0 : true;
+}();
 static int g_c2mode = [] {
     const char* a = getenv("TOOM_C2_CLS");
     const char* b = getenv("TOOM_DEFERRED_BOTTOM");
@@ -678,6 +686,22 @@ static toom_status make_plan(int n, size_t batch, const toom_plan_t& p, Plan& pl
         if ((Bt.B == 3 || Bt.B == 4) && fused_E_supported(Bt.e) && Bt.e == Bt.b + 1 && Bt.Lw == 2 * Bt.b + 1 && 2 * Bt.e > Bt.Lw &&
             2 * Bt.n <= (2 * Bt.B - 1) * 2 * Bt.e)
             plan.fused = true;
+    }
+    // the Toom-3 bottom of 66-limb parents right under the lazy block: its
+    // common denominator 6 = 2 * 3 joins the block's finishing division
+    plan.lzdc = false;
+    if (g_lzdc && g_its_static && plan.fused && !square && plan.lz1 >= 1 &&
+        (size_t)plan.lz1 + 2 == plan.lv.size()) {
+        const Level& Bt = plan.lv[plan.lz1];
+        if (Bt.B == 3 && Bt.n == 66 && Bt.b == 22 && Bt.e == 23 && Bt.Lw == 45 &&
+            plan.lz_s + tg_combS_T3 <= 32 * (LV_MAXHALO - 2)) {
+            plan.lzdc = true;
+            if (!plan.lz_o.empty() && (uint64_t)plan.lz_o.back() * tg_combO_T3 <= 0xFFFFFFFFull)
+                plan.lz_o.back() *= tg_combO_T3;
+            else
+                plan.lz_o.push_back(tg_combO_T3);
+            plan.lz_s += tg_combS_T3;
+        }
     }
     // a batched top level directly above the fused level: its interpolation
     // can run one warp per product on row-major products (fused MODE 3)
@@ -1049,19 +1073,21 @@ static toom_status launch_fused(const Level& Lv, int mode, const uint32_t* su, c
     return TOOM_EUNSUPPORTED;
 }
 
-// the C2 bottom with the deferred denominator (csrc/fused_c2.cuh)
-static toom_status launch_fused_c2dc(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out,
-                                     cudaStream_t st) {
+// a bottom level with the deferred denominator (csrc/fused_dc.cuh): B = 4 the
+// C2 shape, B = 3 the bottom under the lazy levels
+template <int B>
+static toom_status launch_fused_dc(const Level& Lv, const uint32_t* su, const uint32_t* sv, uint32_t* out,
+                                   cudaStream_t st) {
     if (Lv.count == 0) return TOOM_OK;
     ProfScope ps(CAT_BASE, st);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_fused_c2_dc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2dc_smem_bytes());
-        cudaFuncSetAttribute(k_fused_c2_dc, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_fused_dc<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dc_smem_bytes<B>());
+        cudaFuncSetAttribute(k_fused_dc<B>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
     const unsigned grid = (unsigned)((Lv.count + 31) / 32);
-    k_fused_c2_dc<<<grid, 224, c2dc_smem_bytes(), st>>>(su, sv, out, Lv.count);
+    k_fused_dc<B><<<grid, 32 * (2 * B - 1), dc_smem_bytes<B>(), st>>>(su, sv, out, Lv.count);
     ps.done(st);
     ++t_launches;
     return TOOM_OK;
@@ -2268,7 +2294,9 @@ static toom_status run_plan(const Plan& plan, uint32_t* w, const uint32_t* u, co
         // interpolation reads row-major products
         const int mode = top ? 1 : (plan.lv[L - 2].lazy ? 0 : (plan.lv[L - 2].lng ? 2 : (plan.top_warp ? 3 : 0)));
         if (plan.c2mode == 2) {
-            if ((s = launch_fused_c2dc(Lv, su, sv, out, st))) return s;
+            if ((s = launch_fused_dc<4>(Lv, su, sv, out, st))) return s;
+        } else if (plan.lzdc) {
+            if ((s = launch_fused_dc<3>(Lv, su, sv, out, st))) return s;
         } else if ((s = launch_fused(Lv, mode, su, sv, out, st, plan.square))) {
             return s;
         }
@@ -3082,6 +3110,7 @@ void toom_set_top_stream(int on) { g_top_stream = on; }
 
 void toom_set_t16_matrix(int on) { g_t16_matrix = on != 0; }
 void toom_set_c2_mode(int mode) { g_c2mode = (mode >= 0 && mode <= 2) ? mode : 0; }
+void toom_set_lazy_bottom(int on) { g_lzdc = on != 0; }
 
 void toom_set_fused(int on) {
     // 0: every level staged (k_eval / k_base / k_interp); 1: fused bottom level
@@ -3124,8 +3153,9 @@ size_t toom_plan_describe(size_t n, size_t batch, const toom_plan_t* plan, char*
         js += tmp;
     }
     char tail[128];
-    snprintf(tail, sizeof tail, "], \"workspace_bytes\": %zu, \"fused_bottom\": %s, \"c2_mode\": %d}", pl.bytes,
-             pl.fused ? "true" : "false", pl.c2mode);
+    snprintf(tail, sizeof tail,
+             "], \"workspace_bytes\": %zu, \"fused_bottom\": %s, \"c2_mode\": %d, \"lazy_bottom_dc\": %s}", pl.bytes,
+             pl.fused ? "true" : "false", pl.c2mode, pl.lzdc ? "true" : "false");
     js += tail;
     if (buf && len) {
         size_t k = js.size() < len - 1 ? js.size() : len - 1;

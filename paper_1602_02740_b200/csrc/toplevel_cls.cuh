@@ -3,7 +3,7 @@
 // common denominator (steps a4 + a5; reading 18):
 //     D w = X = sum_j 2^(32 b j) sum_k A'_jk y_k        (A' = tg_combA_T4)
 // with D = 360, or D = 360 * 360 when the children come from the deferred
-// bottom (csrc/fused_c2.cuh: y_k = 360 y'_k).  The matrix form
+// bottom (csrc/fused_dc.cuh: y_k = 360 y'_k).  The matrix form
 // has no division, so limb P of X,
 //     X[P] = sum_j sum_k A'_jk y_k[P - 64 j]     (|X[P]| < 2^45),
 // is elementwise in P; the one exact division by D = 2^s o (2-adic by o, ref

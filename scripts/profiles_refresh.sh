@@ -18,5 +18,5 @@ idx=[h.index(k) for k in keys if k in h]
 print(','.join(h[i] for i in idx)); print(','.join(r[1][i] for i in idx))
 for x in r[2:]: print(','.join('\"'+x[i]+'\"' if ',' in x[i] else x[i] for i in idx))
 " > profiles/${T}_c2_ncu_raw_summary.csv
-for k in k_fused_c2_dc k_interp_top_cls k_eval_top_v4; do python scripts/sass_hot.py gpurun_out/ev_prof_c2.ncu-rep $k > profiles/${T}_sass_hot_$k.txt 2>&1; done
+for k in k_fused_dc k_interp_top_cls k_eval_top_v4; do python scripts/sass_hot.py gpurun_out/ev_prof_c2.ncu-rep $k > profiles/${T}_sass_hot_$k.txt 2>&1; done
 cp gpurun_out/ev_pytest_gpu.log profiles/${T}_pytest_gpu.log

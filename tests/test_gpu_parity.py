@@ -211,6 +211,30 @@ def test_c2_modes_equal_oracle(batch):
         tg.set_c2_mode(2)
 
 
+@pytest.mark.parametrize("n", [1 << 16, 65538, 1 << 18])
+def test_lazy_bottom_deferred_equals_per_row_and_oracle(n):
+    """Single large products (the C4 recursion: lazy Toom-4 levels over the
+    Toom-3 bottom of 66-limb parents): the bottom handing X = 6 y into the
+    lazy block's finishing division (csrc/fused_dc.cuh, DESIGN.md readings
+    18-19) against the per-row bottom and the oracle, uniform and adversarial
+    operands."""
+    rng = np.random.default_rng(n)
+    a = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    b[: n // 3] = 0xFFFFFFFF
+    a[n // 2: n // 2 + 999] = 0
+    assert tg.plan_describe(n, 1, B=4)["lazy_bottom_dc"]
+    want = oracle.toom(a, b, top_B=4)
+    try:
+        for on in (True, False):
+            tg.set_lazy_bottom(on)
+            w = host(tg.toom_mul(dev(a), dev(b), B=4))
+            assert np.array_equal(w, want), on
+            check_residues(a, b, w)
+    finally:
+        tg.set_lazy_bottom(True)
+
+
 def test_c2_chunked_equals_unchunked():
     u, v = synth.config_inputs(2, batch=5000)
     a = run_batched(u, v, 4, **C2_PLAN)
