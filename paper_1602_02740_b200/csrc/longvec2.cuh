@@ -680,22 +680,45 @@ __global__ void __launch_bounds__(128, 3) k_lbig2(const LBigDev* __restrict__ dp
     }
     __syncthreads();
     auto staged = [&](int sI, int i) -> uint32_t { return Sb[(size_t)sI * CH * NP1 + (i % CH) * NP1 + i / CH]; };
+    static_assert(LB_PRE == LB_ND - 1, "the window of a thread starts LB_ND - 1 positions early");
     for (int o = 0; o < d.no; ++o) {
         const LMOut& O = d.out[o];
-        Acc lin[CH];
+        // each balanced 32-bit digit a = h 2^16 + l (0 <= l < 2^16) enters as
+        // two IMAD.WIDE.U32 terms into 64-bit sums of < 2^48 terms (no
+        // overflow for <= 2^16 terms): P0 = sum l y, P1 - N1 = sum h y, then
+        // lin = P0 + (P1 - N1) 2^16 (int128 once per output)
+        uint64_t P0[CH], P1[CH], N1[CH];
 #pragma unroll
-        for (int q = 0; q < CH; ++q) lin[q] = 0;
+        for (int q = 0; q < CH; ++q) P0[q] = P1[q] = N1[q] = 0ull;
         for (int sI = 0; sI < d.ns; ++sI) {
             const int nd = d.nd[o][sI];
-            for (int dd = 0; dd < nd; ++dd) {
+            // the source window of this thread: relative indices tid*CH + q', q' < CH + LB_PRE
+            uint32_t yw[CH + LB_PRE];
+            const uint32_t* sb = Sb + (size_t)sI * CH * NP1 + tid;
+#pragma unroll
+            for (int q = 0; q < CH + LB_PRE; ++q) yw[q] = sb[(q % CH) * NP1 + q / CH];
+#pragma unroll
+            for (int dd = 0; dd < LB_ND; ++dd) {
+                if (dd >= nd) break;
                 const long long a = d.a[o][sI][dd];
                 if (a == 0) continue;
-                // position p0 + q - dd  ->  relative index tid*CH + q - dd + LB_PRE
-                const int i0 = tid * CH - dd + LB_PRE;
+                const uint32_t l = (uint32_t)a & 0xFFFFu;
+                const long long h = (a - (long long)l) >> 16;
+                // position p0 + q - dd  ->  window index q - dd + LB_PRE
 #pragma unroll
-                for (int q = 0; q < CH; ++q) lin[q] += (Acc)(a * (long long)staged(sI, i0 + q));
+                for (int q = 0; q < CH; ++q) P0[q] = tg_madw(l, yw[q - dd + LB_PRE], P0[q]);
+                if (h > 0) {
+#pragma unroll
+                    for (int q = 0; q < CH; ++q) P1[q] = tg_madw((uint32_t)h, yw[q - dd + LB_PRE], P1[q]);
+                } else if (h < 0) {
+#pragma unroll
+                    for (int q = 0; q < CH; ++q) N1[q] = tg_madw((uint32_t)(-h), yw[q - dd + LB_PRE], N1[q]);
+                }
             }
         }
+        Acc lin[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) lin[q] = (Acc)P0[q] + ((Acc)(long long)(P1[q] - N1[q]) << 16);
         const LMod M{O.o, O.orcp};
         lv2_tile<Acc, CH>(lin, M,
                           LFinish{O.oinv, O.p32, O.Mch, O.mi, O.sa, O.sr, d.W,

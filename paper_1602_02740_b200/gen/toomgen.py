@@ -1028,15 +1028,11 @@ TG_HD TG_INLINE uint32_t tg_mulhi(uint32_t a, uint32_t b) {
   return (uint32_t)(((uint64_t)a * b) >> 32);
 #endif
 }
-// lin + m*x (64-bit accumulate; one IMAD.WIDE.U32 on the device)
+// lin + m*x (64-bit accumulate; one IMAD.WIDE.U32 on the device: written in
+// C, ptxas fuses the add into the IMAD.WIDE; an inline mad.wide.u32 was split
+// into a zero-addend IMAD.WIDE + IADD3 + IMAD.X)
 TG_HD TG_INLINE uint64_t tg_madw(uint32_t m, uint32_t x, uint64_t lin) {
-#ifdef __CUDA_ARCH__
-  uint64_t r;
-  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(m), "r"(x), "l"(lin));
-  return r;
-#else
   return lin + (uint64_t)m * x;
-#endif
 }
 // lin - m*x (mod 2^64): (2^32 - m)*x + lin - x*2^32
 TG_HD TG_INLINE uint64_t tg_msubw(uint32_t m, uint32_t x, uint64_t lin) {
