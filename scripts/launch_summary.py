@@ -6,10 +6,11 @@ top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 hdr = [i for i, r in enumerate(rows) if 'Kernel Name' in r][0]
 h = rows[hdr]
 ki, vi, gi, bi = h.index('Kernel Name'), h.index('Metric Value'), h.index('Grid Size'), h.index('Block Size')
+mi = h.index('Metric Name') if 'Metric Name' in h else None
 tot = 0.0
 agg = collections.OrderedDict()
 for r in rows[hdr + 1:]:
-    if len(r) < len(h):
+    if len(r) < len(h) or (mi is not None and r[mi] != 'gpu__time_duration.sum'):
         continue
     t = float(r[vi].replace(',', '')) / 1e3
     tot += t

@@ -20,3 +20,4 @@ for x in r[2:]: print(','.join('\"'+x[i]+'\"' if ',' in x[i] else x[i] for i in 
 " > profiles/${T}_c2_ncu_raw_summary.csv
 for k in k_fused_dc k_interp_top_cls k_eval_top_v4; do python scripts/sass_hot.py gpurun_out/ev_prof_c2.ncu-rep $k > profiles/${T}_sass_hot_$k.txt 2>&1; done
 cp gpurun_out/ev_pytest_gpu.log profiles/${T}_pytest_gpu.log
+cp gpurun_out/ev_launches_c5.csv profiles/${T}_c5_launches.csv 2>/dev/null && python scripts/launch_summary.py gpurun_out/ev_launches_c5.csv 40 > profiles/${T}_c5_launches_summary.txt
