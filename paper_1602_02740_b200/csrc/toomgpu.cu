@@ -911,11 +911,21 @@ struct WsGuard {
 
 static inline unsigned nblk(size_t threads, int bs = 128) { return (unsigned)((threads + bs - 1) / bs); }
 
+static bool g_eval_p8 = [] {   // TOOM_EVAL_P8=0: the per-product streaming program for C3's top level
+    const char* e = getenv("TOOM_EVAL_P8");
+    return e ? atoi(e) != 0 : true;
+}();
 static toom_status launch_eval(int B, bool top, const uint32_t* su, const uint32_t* sv, uint32_t* ou, uint32_t* ov,
                                size_t count, int n, int b, int e, cudaStream_t st) {
     const unsigned g = nblk((sv ? 2 : 1) * count);
     if (g == 0) return TOOM_OK;
     ProfScope ps(CAT_EVAL, st);
+    if (B == 8 && top && sv && g_eval_p8) {   // the paper's points: pairs of +-2^i by funnel shifts
+        k_eval_top_p8<<<(unsigned)((count + 7) / 8), 128, 0, st>>>(su, sv, ou, ov, count, n, b, e);
+        ps.done(st);
+        ++t_launches;
+        return TOOM_OK;
+    }
 #define TG_EV(BB)                                                                          \
     if (top) k_eval<BB, true><<<g, 128, 0, st>>>(su, sv, ou, ov, count, n, b, e);          \
     else k_eval<BB, false><<<g, 128, 0, st>>>(su, sv, ou, ov, count, n, b, e);

@@ -116,6 +116,86 @@ __global__ void __launch_bounds__(32 * (2 * B - 1)) k_eval_top_rows(
 }
 
 // ------------------------------------------------------------------------
+// k_eval_top_p8: the top-level evaluation at the paper's Toom-8 points
+// 0, +-2^i (i < 7; §4) of a batch (C3).  U(+-2^i) =
+// E_i +- O_i with E_i = sum_{j even} u_j 2^(i j), O_i = sum_{j odd}
+// u_j 2^(i j) (Eqs. 4.3-4.4): one thread per (product, operand, i) forms both
+// points of the pair, limb t of each shifted block as one funnel shift of its
+// limbs t - q and t - q - 1 (i j = 32 q + r), so there is no multiply; one
+// thread per (product, operand) copies block 0 (point 0).  A half-warp holds
+// the 16 tasks of one product (their loads of the same limbs coalesce into
+// one request); outputs interleaved [e][15 count].
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_eval_top_p8(const uint32_t* __restrict__ u, const uint32_t* __restrict__ v,
+                                                     uint32_t* __restrict__ U1, uint32_t* __restrict__ V1,
+                                                     size_t count, int n, int b, int e) {
+    constexpr int B = 8, NP = 15;
+    const int task = threadIdx.x & 15;   // 0..6 pair i of u, 7..13 pair i of v, 14 / 15 point 0 of u / v
+    const size_t c = (size_t)blockIdx.x * 8 + (threadIdx.x >> 4);
+    if (c >= count) return;
+    const bool opv = task == 15 || (task >= 7 && task < 14);
+    const uint32_t* src = (opv ? v : u) + c * (size_t)n;
+    uint32_t* out = (opv ? V1 : U1) + c;
+    const size_t st = (size_t)NP * count;
+    const int lentop = n - (B - 1) * b;
+    if (task >= 14) {   // point 0: block 0
+        for (int t = 0; t < e; ++t) out[(size_t)t * st] = t < b ? __ldg(src + t) : 0u;
+        return;
+    }
+    const int i = opv ? task - 7 : task;
+    uint32_t* op = out + (size_t)(2 * i + 1) * count;   // +2^i
+    uint32_t* om = op + count;                          // -2^i
+    int q[B], r[B];
+    uint32_t h1[B], h2[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+        q[j] = (i * j) >> 5;
+        r[j] = (i * j) & 31;
+        h1[j] = h2[j] = 0u;
+    }
+    long long cp = 0, cm = 0;
+    const bool v4 = ((b | n) & 3) == 0 && (((uintptr_t)src) & 15) == 0;
+    // four limbs per step (one 16-byte load per block when aligned)
+#pragma unroll 1
+    for (int t0 = 0; t0 < e; t0 += 4) {
+        uint32_t x[B][4];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            const int len = j == B - 1 ? lentop : b;
+            const uint32_t* sp = src + (size_t)j * b + t0;
+            if (v4 && t0 + 3 < len) {
+                const uint4 w = __ldg(reinterpret_cast<const uint4*>(sp));
+                x[j][0] = w.x; x[j][1] = w.y; x[j][2] = w.z; x[j][3] = w.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) x[j][k] = t0 + k < len ? __ldg(sp + k) : 0u;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (t0 + k >= e) break;
+            unsigned long long E = 0, O = 0;
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                const uint32_t cur = q[j] ? h1[j] : x[j][k], prv = q[j] ? h2[j] : h1[j];
+                const uint32_t sh = __funnelshift_l(prv, cur, r[j]);   // limb t of block j << (i j)
+                h2[j] = h1[j];
+                h1[j] = x[j][k];
+                if (j & 1) O += sh;
+                else E += sh;
+            }
+            const long long P = (long long)(E + O) + cp;
+            const long long M = (long long)E - (long long)O + cm;
+            const size_t o = (size_t)(t0 + k) * st;
+            op[o] = (uint32_t)P;
+            om[o] = (uint32_t)M;
+            cp = P >> 32;
+            cm = M >> 32;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
 // k_eval_top_v4<B>: the top-level evaluation of k_eval_top_rows (B = 3, 4) with
 // 16-byte staging and compile-time points.  CTA = 32 products x NP warps.
 // Chunks of 16 limbs of every block of the 32 products are copied with 16-byte
