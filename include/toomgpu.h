@@ -160,7 +160,10 @@ void toom_set_verify(int on);
 
 /* Fault injection for tests: kind 1 flips one bit of one
  * base-case product inside the fused bottom kernel, so that the next exact
- * division is inexact; 0 = off.  Never set in production.                 */
+ * division is inexact; kind 2 injects no fault but sends every product of
+ * the C2 top level (csrc/toplevel_cls.cuh) through the serial carry/borrow
+ * chain that otherwise runs only when a carry wraps a segment's limb 0;
+ * 0 = off.  Never set in production.                                      */
 void toom_debug_fault(int kind);
 
 /* Human-readable name of a status code (static string). */

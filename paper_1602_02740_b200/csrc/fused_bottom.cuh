@@ -466,7 +466,7 @@ __global__ void __maxnreg__(E <= 18 ? TG_FUSED_REG18 : TG_FUSED_REG33) k_fused_b
         }
         // fault injection (tests): one flipped bit of y_1 of the
         // CTA's first instance makes the rows' exact divisions inexact
-        if (tg_fault && blockIdx.x == 0 && lane == 0 && warp == 1) slot[3 * G] ^= 1u;
+        if (tg_fault == 1 && blockIdx.x == 0 && lane == 0 && warp == 1) slot[3 * G] ^= 1u;
     }
     __syncthreads();
 

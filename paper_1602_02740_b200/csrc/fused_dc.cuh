@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(32 * (2 * B - 1), 4) k_fused_dc(const uint32_t
         // fault injection (tests): X_0 = Dc y_0 of the first
         // parent made odd, so the division by Dc above is not exact (its
         // check of the low bits catches it)
-        const uint32_t flt = (tg_fault && s == 0 && c == 0) ? 1u : 0u;
+        const uint32_t flt = (tg_fault == 1 && s == 0 && c == 0) ? 1u : 0u;
         *po = (uint32_t)x ^ flt;
         long long d = x >> 32;   // -1, 0, +1
         cin = (long long)(int32_t)CO[s * G + lane];

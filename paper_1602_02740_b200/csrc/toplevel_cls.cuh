@@ -17,8 +17,9 @@
 //      written over the class's own columns (lo words, packed 16-bit highs)
 //   2  segment s (warp s of 14): carries with carry-in 0 -> limbs z, the carry-out
 //      and the residue of the segment's X mod o
-//   3  warp 0: the true carry-ins (a carry that wraps limb 0 ripples) and
-//      the borrow-ins, segment by segment
+//   3  warp s: its carry-in (the previous segment's carry-out) and borrow-in
+//      (closed form over the earlier segments' residues); a carry that wraps
+//      a limb 0 (~2^-17) sends the product through warp 0's serial chain
 //   4  segment s: the 2-adic division chain from its borrow-in
 //   5  all warps: w = q >> s to the row-major output (16-byte stores)
 #pragma once
@@ -55,12 +56,18 @@ static_assert(Den<true>::oinv * 2025u == 1u, "2-adic inverse");
 template <uint32_t O> struct Pw {
     uint32_t p[40];     // 2^(32 i) mod O, i = 0..39
     uint32_t ip[2];     // 2^(-32 L) mod O for L = 36, 37
+    uint32_t ps[NSEG];  // 2^(32 p_s) mod O, p_s = seg0(s)
+    uint32_t ips[NSEG]; // 2^(-32 p_s) mod O
 };
 template <uint32_t O> __host__ __device__ constexpr Pw<O> make_pw() {
     Pw<O> t{};
     for (int i = 0; i < 40; ++i) t.p[i] = modpow32(O, i);
     t.ip[0] = invmod(modpow32(O, 36), O);
     t.ip[1] = invmod(modpow32(O, 37), O);
+    for (int i = 0; i < NSEG; ++i) {
+        t.ps[i] = modpow32(O, seg0(i));
+        t.ips[i] = invmod(modpow32(O, seg0(i)), O);
+    }
     return t;
 }
 }  // namespace cls
@@ -72,7 +79,7 @@ template <> __device__ __forceinline__ const cls::Pw<45u>& cls_pw<false>() { ret
 template <> __device__ __forceinline__ const cls::Pw<2025u>& cls_pw<true>() { return tg_cls_pw2025; }
 
 __host__ __device__ constexpr size_t cls_smem_bytes() {
-    return (size_t)4 * ((size_t)cls::NP * cls::YW * cls::G + 4 * cls::NSEG * cls::G);
+    return (size_t)4 * ((size_t)cls::NP * cls::YW * cls::G + 4 * cls::NSEG * cls::G + cls::G);
 }
 
 // smem word offset (without the lane) of the lo word / packed high word of X[P]
@@ -197,11 +204,13 @@ __global__ void __launch_bounds__(32 * cls::NW, 2) k_interp_top_cls(const uint32
     uint32_t* CO = ZL + NSEG * G;              //         segment carry-out (signed)
     uint32_t* RH = CO + NSEG * G;              //         segment residue of X mod o
     uint32_t* BI = RH + NSEG * G;              //         segment borrow-in
+    uint32_t* FL = BI + NSEG * G;              // [28] a limb 0 wrapped (serial fix-up)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t c0 = (size_t)blockIdx.x * G;
     const int nin = (int)min((size_t)G, count - c0);
     const size_t SK = (size_t)NP * count;
     const bool act = lane < G;
+    if (threadIdx.x < G) FL[threadIdx.x] = 0u;   // (read after phase 3's barriers)
 
     // ---- 0: rows (k, t) of G contiguous words; row R = t * 7 + k in source
     // order, 4 rows per warp instruction (7 lanes x 16 bytes each), a warp's
@@ -261,8 +270,25 @@ __global__ void __launch_bounds__(32 * cls::NW, 2) k_interp_top_cls(const uint32
     }
     __syncthreads();
 
-    // ---- 3: true carry-ins and borrow-ins, segment by segment (one lane per product)
-    if (warp == 0 && act) {
+    // ---- 3: carry-ins and borrow-ins.  Warp s forms its own: the carry into
+    // p_s is the previous segment's carry-out (a carry-in is absorbed by the
+    // limbs unless it wraps limb 0, probability ~2^-17 per segment: then the
+    // product goes through warp 0's serial chain), the borrow-in follows from
+    // 2^(-32 p_s) sum_{s' < s} rho_s' 2^(32 p_s') mod o
+    if (act) {
+        const auto& pw = cls_pw<DEF>();
+        const long long c = warp ? (long long)(int32_t)CO[(warp - 1) * G + lane] : 0ll;
+        uint32_t acc = 0;   // < 13 * o^2 < 2^26
+        for (int s = 0; s < warp; ++s) acc += RH[s * G + lane] * pw.ps[s];
+        const uint32_t T = (acc % o) * pw.ips[warp] % o;
+        const long long cm = c % (long long)o;
+        BI[warp * G + lane] = ((uint32_t)(cm < 0 ? cm + o : cm) + o - T) % o;
+        const long long x = (long long)ZL[warp * G + lane] + c;
+        Y[cls_lo(p0) + lane] = (uint32_t)x;
+        if ((x >> 32) != 0 || tg_fault == 2) FL[lane] = 1u;   // (kind 2: tests take the serial chain)
+    }
+    __syncthreads();
+    if (warp == 0 && act && FL[lane]) {
         const auto& pw = cls_pw<DEF>();
         long long c = 0;
         uint32_t T = 0;   // 2^(-32 p_s) sum_{i < p_s} X_i 2^(32 i) mod o

@@ -102,6 +102,20 @@ def test_fault_injection_other_c2_modes(mode):
         tg.set_c2_mode(2)
 
 
+def test_c2_top_serial_carry_chain_equals_oracle():
+    """The C2 top level's rare path (csrc/toplevel_cls.cuh phase 3: a carry
+    that wraps a segment's limb 0 sends the product through the serial
+    carry/borrow chain) forced for every product (debug kind 2)."""
+    u, v = synth.config_inputs(2, batch=1000, first=7)
+    u[:4] = 0xFFFFFFFF
+    try:
+        tg.debug_fault(2)
+        w = host(tg.toom_mul_batched(dev(u), dev(v), B=4, t4=32, t3=32))
+    finally:
+        tg.debug_fault(0)
+    assert np.array_equal(w, oracle.schoolbook_batched(u, v))
+
+
 def test_fault_injection_caught_by_verify_alone():
     u, v = synth.config_inputs(2, batch=256)
     tg.set_verify(True)
