@@ -31,8 +31,9 @@
 //       separates the reads and the writes
 //   B2  warp w: carry pass over its segment of positions (carry-in 0),
 //       limbs 1.. written (interleaved), limb 0 and the carry-out kept
-//   B3  warp 0: the segments' carries in order; limb 0 written, a carry
-//       that wraps limb 0 (probability ~2^-17) ripples through the segment
+//   B3  warp s: limb 0 plus the previous segment's carry-out; a carry that
+//       wraps limb 0 (probability ~2^-17) sends the parent through warp 0's
+//       serial pass with the ripple
 #pragma once
 
 namespace tg {
@@ -309,6 +310,8 @@ __global__ void __launch_bounds__(32 * (2 * B - 1), 4) k_fused_dc(const uint32_t
     for (int r = warp; r < BB; r += NP) dc_class<B>(r, Y, SG, lane);
     __syncthreads();
 
+    if (warp == 0) SG[lane] = 0u;   // the wrap flags of B3 (SG is dead after B1)
+
     // ---- B2: carry pass over segment `warp` with carry-in 0, in runs of
     // constant m = P / b (consecutive cells at stride G)
     {
@@ -331,22 +334,35 @@ __global__ void __launch_bounds__(32 * (2 * B - 1), 4) k_fused_dc(const uint32_t
     }
     __syncthreads();
 
-    // ---- B3: carries between the segments (one lane per parent)
-    if (warp != 0 || !valid) return;
+    // ---- B3: carries between the segments.  Warp s adds the previous
+    // segment's carry-out to its limb 0 (a carry-in is absorbed unless it
+    // wraps limb 0, probability ~2^-17: then warp 0 redoes the parent's
+    // segments in order with the ripple)
+    uint32_t* FL = SG;   // [32] (SG is dead after B1)
+    if (valid) {
+        const int P0 = Gm::seg0(warp);
+        const long long x =
+            (long long)L0[warp * G + lane] + (warp ? (long long)(int32_t)CO[(warp - 1) * G + lane] : 0ll);
+        // fault injection (tests, SPEC.md:443): X_0 = Dc y_0 of the first
+        // parent made odd, so the division by Dc above is not exact (its
+        // check of the low bits catches it)
+        const uint32_t flt = (tg_fault == 1 && warp == 0 && c == 0) ? 1u : 0u;
+        out[(size_t)P0 * count + c] = (uint32_t)x ^ flt;
+        if ((x >> 32) != 0) FL[lane] = 1u;
+    }
+    __syncthreads();
+    if (warp != 0 || !valid || !FL[lane]) return;
     long long cin = 0;
 #pragma unroll 1
     for (int s = 0; s < NSEG; ++s) {
         const int P0 = Gm::seg0(s), L = Gm::seg0(s + 1) - P0;
         const long long x = (long long)L0[s * G + lane] + cin;
         uint32_t* po = out + (size_t)P0 * count + c;
-        // fault injection (tests, SPEC.md:443): X_0 = Dc y_0 of the first
-        // parent made odd, so the division by Dc above is not exact (its
-        // check of the low bits catches it)
         const uint32_t flt = (tg_fault == 1 && s == 0 && c == 0) ? 1u : 0u;
         *po = (uint32_t)x ^ flt;
         long long d = x >> 32;   // -1, 0, +1
         cin = (long long)(int32_t)CO[s * G + lane];
-        if (d != 0) {            // rare: limb 0 wrapped
+        if (d != 0) {            // limb 0 wrapped: ripple
             for (int q = 1; q < L && d != 0; ++q) {
                 po += count;
                 const uint32_t v = *po;
