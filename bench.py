@@ -458,21 +458,29 @@ def main():
             a5, b5 = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         ops = tgdist.CudaOps()
         reps5 = 3
+        # one GPU: the single-product entry point (Toom-16 top, lazy Toom-4
+        # levels, deferred Toom-3 bottom in one plan); N > 1: the 31 top-level
+        # products sharded over the ranks (Eq. 2.5) through dist.sharded_mul
+        if world == 1:
+            mul5 = lambda: tg.toom_mul(a5, b5, B=16)
+        else:
+            mul5 = lambda: tgdist.sharded_mul(a5, b5, n5, ops)
         for _ in range(1):
-            tgdist.sharded_mul(a5, b5, n5, ops)
+            mul5()
         torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(reps5):
-            w5 = tgdist.sharded_mul(a5, b5, n5, ops)
+            w5 = mul5()
         e1.record(stream)
         torch.cuda.synchronize()
         ms5 = max_over_ranks(e0.elapsed_time(e1) / reps5)
         lp5 = algorithmic_lp(n5, 16)
         c5 = {"workload": "C5: one product of two 2^24-limb (512-Mbit) uniform operands, 31-point Toom-16 top level, "
                           "its 31 products sharded over the ranks (BASELINE.json configs[4])",
+              "path": "toom_mul (one GPU)" if world == 1 else "dist.sharded_mul (NCCL scatter / gather)",
               "ms_per_product": ms5, "reps": reps5, "ranks": world,
               "products_per_rank": [hi_ - lo_ for lo_, hi_ in tgdist.shard_bounds(31, world)[0]],
               "frac_of_alu_whole_job": lp5 / (ms5 * 1e-3) / (lp_rate * world)}
