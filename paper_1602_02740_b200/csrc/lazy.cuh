@@ -84,6 +84,36 @@ __device__ __forceinline__ constexpr long long lz_comb(int j, int k) {
     else return tg_combA_cx_T4(j, k);
 }
 
+// the 2B - 1 point values of one position from the blocks' values v_j
+// (|v_j| < 2^34): Toom-4 with the +-x pairs sharing E = v0 + x^2 v2 and
+// O = x v1 + x^3 v3 (Eqs. 4.3-4.4; the coefficients are powers of two, so
+// shifts and adds); the generic form otherwise
+template <int B>
+__device__ __forceinline__ void lz_points(const long long (&v)[B], long long (&lin)[2 * B - 1]) {
+    if constexpr (B == 4) {
+        static_assert(tg_evalc_cx_T4(1, 1) == 1 && tg_evalc_cx_T4(2, 1) == -1 && tg_evalc_cx_T4(3, 3) == 8 &&
+                          tg_evalc_cx_T4(4, 3) == -8 && tg_evalc_cx_T4(5, 0) == 8 && tg_evalc_cx_T4(6, 3) == 1,
+                      "point order 0, 1, -1, 2, -2, 1/2 (homogeneous), inf");
+        const long long E1 = v[0] + v[2], O1 = v[1] + v[3];
+        const long long E2 = v[0] + v[2] * 4, O2 = v[1] * 2 + v[3] * 8;
+        lin[0] = v[0];
+        lin[1] = E1 + O1;
+        lin[2] = E1 - O1;
+        lin[3] = E2 + O2;
+        lin[4] = E2 - O2;
+        lin[5] = v[0] * 8 + v[1] * 4 + v[2] * 2 + v[3];
+        lin[6] = v[3];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 2 * B - 1; ++k) {
+            long long x = 0;
+#pragma unroll
+            for (int j = 0; j < B; ++j) x += lz_evalc<B>(k, j) * v[j];
+            lin[k] = x;
+        }
+    }
+}
+
 // ---- a2: evaluation of one lazy level -------------------------------------
 // child k of parent c at position t: lin = sum_j c_kj par_j[t], block j =
 // parent positions [j b, j b + len_j); written to the interleaved lazy family
@@ -100,33 +130,24 @@ __global__ void __launch_bounds__(256) k_lz_eval(LzSrc pu, LzSrc pv, uint32_t* _
     const LzSrc& S = blockIdx.y ? pv : pu;
     uint32_t* lo = blockIdx.y ? vlo : ulo;
     uint32_t* hi = blockIdx.y ? vhi : uhi;
-    uint32_t xl[B];
-    int xh[B], xs[B];
+    long long v[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
         const int len = (j == B - 1) ? lentop : b;
-        xl[j] = 0;
-        xh[j] = 0;
-        xs[j] = 0;
-        if (t < len) lz_get2(S, c, j * b + (int)t, xl[j], xh[j], xs[j]);
+        uint32_t xl = 0;
+        int xh = 0, xs = 0;
+        if (t < len) lz_get2(S, c, j * b + (int)t, xl, xh, xs);
+        v[j] = (long long)xl + xh + ((long long)xs << 32);
     }
+    long long lin[NP];
+    lz_points<B>(v, lin);
     const long long rows = NP * count;
     uint32_t* pl = lo + t * rows + c;
     uint32_t* ph = hi + (t + 1) * rows + c;
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
-        uint64_t P = 0, N = 0;
-        int H = 0, Hs = 0;
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-            const long long m = lz_evalc<B>(k, j);
-            if (m > 0) P += (uint64_t)m * xl[j];
-            else if (m < 0) N += (uint64_t)(-m) * xl[j];
-            if (m != 0) { H += (int)m * xh[j]; Hs += (int)m * xs[j]; }
-        }
-        const long long lin = (long long)(P - N) + (long long)H + ((long long)Hs << 32);
-        pl[k * count] = (uint32_t)lin;
-        if (t + 1 < e) ph[k * count] = (uint32_t)(int)(lin >> 32);
+        pl[k * count] = (uint32_t)lin[k];
+        if (t + 1 < e) ph[k * count] = (uint32_t)(int)(lin[k] >> 32);
         if (t == 0) hi[k * count + c] = 0u;
     }
 }
@@ -148,6 +169,9 @@ __global__ void __launch_bounds__(128) k_lz_eval_last(LzSrc pu, LzSrc pv, uint32
     long long cy[NP];
 #pragma unroll
     for (int k = 0; k < NP; ++k) cy[k] = 0;
+    // (the even-odd sharing of lz_points measured slower here: 318 -> 341 us
+    // on C4's deepest level, whose per-thread carry chains favour these
+    // independent sums)
 #pragma unroll 2
     for (int t = 0; t < e; ++t) {
         uint32_t xl[B];
