@@ -464,7 +464,8 @@ def main():
         if world == 1:
             mul5 = lambda: tg.toom_mul(a5, b5, B=16)
         else:
-            mul5 = lambda: tgdist.sharded_mul(a5, b5, n5, ops)
+            dev5 = torch.device("cuda", torch.cuda.current_device())
+            mul5 = lambda: tgdist.sharded_mul(a5, b5, n5, ops, device=dev5)
         for _ in range(1):
             mul5()
         torch.cuda.synchronize()
@@ -480,7 +481,7 @@ def main():
         lp5 = algorithmic_lp(n5, 16)
         c5 = {"workload": "C5: one product of two 2^24-limb (512-Mbit) uniform operands, 31-point Toom-16 top level, "
                           "its 31 products sharded over the ranks (BASELINE.json configs[4])",
-              "path": "toom_mul (one GPU)" if world == 1 else "dist.sharded_mul (NCCL scatter / gather)",
+              "path": "toom_mul (one GPU)" if world == 1 else "dist.sharded_mul (NCCL broadcast / gather)",
               "ms_per_product": ms5, "reps": reps5, "ranks": world,
               "products_per_rank": [hi_ - lo_ for lo_, hi_ in tgdist.shard_bounds(31, world)[0]],
               "frac_of_alu_whole_job": lp5 / (ms5 * 1e-3) / (lp_rate * world)}

@@ -290,6 +290,14 @@ int toom_npoints(int B);
 toom_status toom_eval_points(uint32_t *out, const uint32_t *a, size_t n, size_t batch, int B,
                              int is_signed, void *stream);
 
+/* As toom_eval_points for the points k0 <= k < k1 only (0 <= k0 <= k1 <=
+ * 2B-1): out[k - k0][i][0..e).  Each rank of the sharded top level (Eq. 2.5,
+ * PAPER.md:44-46) evaluates its own points from broadcast operands.  An
+ * empty range (k0 == k1) is a no-op and out may be null.
+ * Errors: TOOM_EINVAL (range, pointers, overlap), TOOM_ECUDA.               */
+toom_status toom_eval_points_range(uint32_t *out, const uint32_t *a, size_t n, size_t batch, int B,
+                                   int is_signed, int k0, int k1, void *stream);
+
 /* Steps a4+a5: from the 2B-1 pointwise products y[k][i][0..2e) (Eq. 2.1,
  * two's complement), interpolate the coefficients w_0..w_{2B-2} (even-odd
  * method, Eqs. 4.5-4.6, with the listings PAPER.md:114-120, 154-158 or their

@@ -67,6 +67,7 @@ SIGNATURES = {
     "toom_probe_limb_products": (ctypes.c_double, [ctypes.POINTER(ctypes.c_double), _P]),
     "toom_probe_carry_chain": (ctypes.c_double, [ctypes.POINTER(ctypes.c_double), _P]),
     "toom_eval_points": (_I, [_P, _P, _SZ, _SZ, _I, _I, _P]),
+    "toom_eval_points_range": (_I, [_P, _P, _SZ, _SZ, _I, _I, _I, _I, _P]),
     "toom_interp_recompose": (_I, [_P, _P, _SZ, _SZ, _I, _P]),
     "toom_mul_signed_batched": (_I, [_P, _P, _P, _SZ, _SZ, ctypes.POINTER(ToomPlan), _P]),
     "toom_product_width_point": (_SZ, [_SZ, _I]),
@@ -232,6 +233,19 @@ def eval_points(a: torch.Tensor, B: int, signed: bool = False, stream=None) -> t
     out = torch.empty((npts, batch, e), dtype=a.dtype, device=a.device)
     _check(lib().toom_eval_points(_dev(out, "out"), _dev(a, "a"), n, batch, B, 1 if signed else 0, _stream(stream)),
            "toom_eval_points")
+    return out
+
+
+def eval_points_range(a: torch.Tensor, B: int, k0: int, k1: int, signed: bool = False, stream=None) -> torch.Tensor:
+    """As eval_points for the points k0 <= k < k1: -> [k1-k0][batch][e]."""
+    batch, n = a.shape
+    e = lib().toom_eval_width(n, B)
+    out = torch.empty((max(0, k1 - k0), batch, e), dtype=a.dtype, device=a.device)
+    if k1 <= k0:
+        return out
+    _check(lib().toom_eval_points_range(_dev(out, "out"), _dev(a, "a"), n, batch, B, 1 if signed else 0, k0, k1,
+                                        _stream(stream)),
+           "toom_eval_points_range")
     return out
 
 

@@ -1328,12 +1328,14 @@ static LVec child_vec(const Plan& plan, size_t l, const uint8_t* ws, size_t off,
 // evaluation ops of one long level: U(x_k) for every point k of one operand
 // family `par` (Eq. 1.1 split as slices, homogeneous point values)
 template <class ChildF>
-static void long_eval_ops(const Level& L, const LVec& par, ChildF child, std::vector<LOpDev>& out) {
+static void long_eval_ops(const Level& L, const LVec& par, ChildF child, std::vector<LOpDev>& out, int k0 = 0,
+                          int k1 = INT_MAX) {
     LongTables T;
     long_tables(L.B, T);
     for (int k = 0; k < T.neo; ++k) {
         const tg_lop& o = T.eo[k];
-        LVec dv = child(o.dst);
+        if (o.dst < k0 || o.dst >= k1) continue;   // (a range of points: the sharded top level)
+        LVec dv = child(o.dst - k0);
         LOpBuilder b((uint32_t*)dv.base, dv.is, dv.ls, L.e, (int)L.count);
         for (int t = 0; t < o.nt; ++t) {
             const tg_lterm& tm = T.et[o.t0 + t];
@@ -2733,6 +2735,32 @@ toom_status toom_eval_points(uint32_t* out, const uint32_t* a, size_t n, size_t 
     s = run_long_standalone(0, long_tiles(batch, L.e), (size_t)T.neo,
                             [&](uint32_t*, std::vector<LOpDev>& ops) {
                                 long_eval_ops(L, par, [&](int k) { return LVec{out + (size_t)k * batch * L.e, L.e, 1, L.e, 1}; }, ops);
+                            },
+                            (cudaStream_t)stream);
+    if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;
+    return fail(s);
+}
+
+toom_status toom_eval_points_range(uint32_t* out, const uint32_t* a, size_t n, size_t batch, int B, int is_signed,
+                                   int k0, int k1, void* stream) {
+    t_launches = 0;
+    Level L;
+    if (!a || !long_top_level(n, batch, B, L) || k0 < 0 || k1 > L.npts || k0 > k1) return fail(TOOM_EINVAL);
+    if (batch == 0 || k0 == k1) return TOOM_OK;   // (an empty range: out may be null)
+    if (!out) return fail(TOOM_EINVAL);
+    if (overlaps(out, (size_t)(k1 - k0) * batch * L.e * 4, a, n * batch * 4)) return fail(TOOM_EINVAL);
+    toom_status s = check_device();
+    if (s) return fail(s);
+    LongTables T;
+    long_tables(B, T);
+    // every evaluation op writes one point (the programs' eval ops are one per point)
+    for (int k = 0; k < T.neo; ++k)
+        if (T.eo[k].dst < 0 || T.eo[k].dst >= L.npts) return fail(TOOM_EUNSUPPORTED);
+    const LVec par{a, (long long)n, 1, (int)n, is_signed ? 1 : 0};
+    s = run_long_standalone(0, long_tiles(batch, L.e), (size_t)T.neo,
+                            [&](uint32_t*, std::vector<LOpDev>& ops) {
+                                long_eval_ops(L, par, [&](int k) { return LVec{out + (size_t)k * batch * L.e, L.e, 1, L.e, 1}; },
+                                              ops, k0, k1);
                             },
                             (cudaStream_t)stream);
     if (s == TOOM_OK && cudaGetLastError() != cudaSuccess) s = TOOM_ECUDA;

@@ -5,13 +5,16 @@ The paper puts the 2B-1 top-level products of one multiplication on P
 processors (Eq. 2.5: T = (1/P) N^alpha).  Here the processors
 are GPUs, one process per GPU:
 
-  1. rank 0 evaluates u and v at the 2B-1 points        (toom_eval_points)
-  2. scatter: rank r receives the evaluated pairs of its points
-     k in [r m, (r+1) m), m = ceil((2B-1)/P)           (NCCL over NVLink)
+  1. broadcast: u and v reach every rank               (NCCL over NVLink)
+  2. rank r evaluates u and v at its own points
+     k in [r m, (r+1) m), m = ceil((2B-1)/P)           (toom_eval_points_range)
   3. every rank multiplies its pairs (recursive Toom-4/3 on the GPU,
      toom_mul_signed_batched)
   4. gather: the products y_k return to rank 0         (NCCL)
   5. rank 0 interpolates and recomposes w              (toom_interp_recompose)
+Rank 0's serial part is the interpolation alone: the evaluation is split P
+ways (the broadcast moves 2n limbs, the scatter of evaluated pairs moved
+(2B-1)(n/B) x 2).
 
 The compute steps are the C-ABI calls of libtoomgpu; this module only moves
 tensors between ranks.  `ops` can be replaced (tests run the exchange logic
@@ -29,8 +32,8 @@ class CudaOps:
     """The product path: libtoomgpu's long-path stage exports."""
 
     def __init__(self, B: int = 16, t4: int = 256, t3: int = 64):
-        from . import eval_points, interp_recompose, lib, mul_signed_batched
-        self._ev, self._ir, self._mul = eval_points, interp_recompose, mul_signed_batched
+        from . import eval_points, eval_points_range, interp_recompose, lib, mul_signed_batched
+        self._ev, self._evr, self._ir, self._mul = eval_points, eval_points_range, interp_recompose, mul_signed_batched
         self.B, self.t4, self.t3 = B, t4, t3
         self.lib = lib()
 
@@ -39,6 +42,9 @@ class CudaOps:
 
     def eval_points(self, a: torch.Tensor) -> torch.Tensor:          # [n] -> [npts][e]
         return self._ev(a.view(1, -1), self.B)[:, 0, :].contiguous()
+
+    def eval_range(self, a: torch.Tensor, k0: int, k1: int) -> torch.Tensor:   # [n] -> [k1-k0][e]
+        return self._evr(a.view(1, -1), self.B, k0, k1)[:, 0, :].contiguous()
 
     def mul(self, U: torch.Tensor, V: torch.Tensor) -> torch.Tensor:   # [m][e] x2 -> [m][2e]
         if U.shape[0] == 0:
@@ -68,25 +74,22 @@ def sharded_mul(u, v, n: int, ops, group=None, device=None):
     if world == 1:
         return ops.interp(ops.mul(ops.eval_points(u), ops.eval_points(v)), n)
 
-    # 1 + 2: evaluate on rank 0, scatter equal-size (zero-padded) shards;
-    # limbs travel as int32 (same bits)
+    # 1: broadcast u, v (limbs travel as int32: same bits); 2: evaluate this
+    # rank's points
     i32 = torch.int32
-    recvU = torch.empty((m, e), dtype=i32, device=dev)
-    recvV = torch.empty((m, e), dtype=i32, device=dev)
     if rank == 0:
-        U = ops.eval_points(u).view(i32)
-        V = ops.eval_points(v).view(i32)
-        pad = torch.zeros((m * world - npts, e), dtype=i32, device=U.device)
-        Up, Vp = torch.cat([U, pad]), torch.cat([V, pad])
-        dist.scatter(recvU, list(Up.split(m)), src=0, group=group)
-        dist.scatter(recvV, list(Vp.split(m)), src=0, group=group)
+        ub, vb = u.contiguous().view(i32), v.contiguous().view(i32)
     else:
-        dist.scatter(recvU, None, src=0, group=group)
-        dist.scatter(recvV, None, src=0, group=group)
+        ub = torch.empty(n, dtype=i32, device=dev)
+        vb = torch.empty(n, dtype=i32, device=dev)
+    dist.broadcast(ub, src=0, group=group)
+    dist.broadcast(vb, src=0, group=group)
     lo, hi = bounds[rank]
     k = hi - lo
-    # 3: this rank's products (real rows only; the padding is never multiplied)
-    Y = ops.mul(recvU[:k].view(torch.uint32), recvV[:k].view(torch.uint32))
+    # 3: this rank's products (real rows only; the gather pads to m rows)
+    U = ops.eval_range(ub.view(torch.uint32), lo, hi)
+    V = ops.eval_range(vb.view(torch.uint32), lo, hi)
+    Y = ops.mul(U, V)
     Ysend = torch.zeros((m, 2 * e), dtype=i32, device=dev)
     if k:
         Ysend[:k] = Y.view(i32)

@@ -1,7 +1,7 @@
 """Multi-process (world_size 2 and 3, gloo on CPU) test of the sharded top
-level of C5 (paper_1602_02740_b200/dist.py): rank 0 evaluates, scatters the
-evaluated pairs, every rank multiplies its share, the products are gathered
-and interpolated on rank 0 (Eq. 2.5).
+level of C5 (paper_1602_02740_b200/dist.py): u and v are broadcast, every
+rank evaluates and multiplies its own points, the products are gathered and
+interpolated on rank 0 (Eq. 2.5).
 
 The compute steps are exact-integer stand-ins written here from the
 definitions (test infrastructure): homogeneous evaluation
@@ -60,6 +60,9 @@ class IntOps:
         blk = self.blocks(a, n)
         rows = [to_limbs(sum(c * p**j * q ** (B - 1 - j) for j, c in enumerate(blk)), e) for p, q in POINTS]
         return torch.from_numpy(np.stack(rows))
+
+    def eval_range(self, a, k0, k1):
+        return self.eval_points(a)[k0:k1].contiguous()
 
     def mul(self, U, V):
         e = U.shape[1]

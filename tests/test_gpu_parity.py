@@ -473,8 +473,10 @@ def test_c5_full_oracle():
 @pytest.mark.parametrize("B,n", [(16, 5000), (4, 3001), (3, 2500), (8, 4100)])
 def test_stage_exports_compose(B, n):
     """eval_points -> per-point signed products -> interp_recompose == u*v,
-    with the products computed in rank-sized shards (single-GPU emulation of
-    the P=8 partition of dist.sharded_mul; ranks do not wait on one another)."""
+    with the evaluation (eval_points_range, equal to the slices of
+    eval_points) and the products in rank-sized shards (single-GPU emulation
+    of the P=8 partition of dist.sharded_mul; ranks do not wait on one
+    another)."""
     from paper_1602_02740_b200 import dist as tgdist
     rng = np.random.default_rng(B * 1000 + n)
     u = rng.integers(0, 2**32, (1, n), dtype=np.uint64).astype(np.uint32)
@@ -485,8 +487,12 @@ def test_stage_exports_compose(B, n):
     Ys = []
     bounds, _ = tgdist.shard_bounds(npts, 8)
     for lo, hi in bounds:
-        if hi > lo:
-            Ys.append(tg.mul_signed_batched(U[lo:hi, 0].contiguous(), V[lo:hi, 0].contiguous(), B=4))
+        # each rank evaluates its own points (toom_eval_points_range) ...
+        Ur = tg.eval_points_range(dev(u), B, lo, hi)
+        Vr = tg.eval_points_range(dev(v), B, lo, hi)
+        assert torch.equal(Ur, U[lo:hi]) and torch.equal(Vr, V[lo:hi])
+        if hi > lo:   # ... and multiplies them
+            Ys.append(tg.mul_signed_batched(Ur[:, 0].contiguous(), Vr[:, 0].contiguous(), B=4))
     Y = torch.cat([y.view(torch.int32) for y in Ys]).view(torch.uint32)
     w = host(tg.interp_recompose(Y.view(npts, 1, -1).contiguous(), n, B))
     assert np.array_equal(w[0], oracle.schoolbook(u[0], v[0]))
