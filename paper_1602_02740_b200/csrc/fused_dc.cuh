@@ -92,8 +92,98 @@ __device__ __forceinline__ void dc_column(const uint32_t (&y)[2 * B - 1], uint64
     }
 }
 
+// ---- the class sums on the FP64 pipe (TG_DC_FP64, default): the IMAD.WIDE
+// pipe carries the base products, the DFMA pipe is otherwise idle and twice
+// as fast (measured 63 vs 30 per clock and SM, and the two overlap).  Exact:
+// y_k[t] < 2^32 and |A'_jk| <= 2520 < 2^12 give terms below 2^44, and an
+// accumulator sums at most 3 * 7 of them (< 2^49 < 2^53), so every DFMA
+// result is an integer below 2^53, represented exactly.
+#ifndef TG_DC_FP64
+#define TG_DC_FP64 1
+#endif
+__device__ __forceinline__ double dc_u2d(uint32_t y) {   // exact: 2^52 + y - 2^52
+    return __hiloint2double(0x43300000, (int)y) - 4503599627370496.0;
+}
+__device__ __forceinline__ long long dc_d2ll(double x) {   // exact for |x| < 2^51 (integer-valued)
+    return __double_as_longlong(x + 6755399441055744.0) - 0x4338000000000000ll;
+}
+template <int B, int J, int K>
+__device__ __forceinline__ void dc_dterm(double y, double& a) {
+    constexpr long long A = DcShape<B>::A(J, K);
+    if constexpr (A != 0) a = fma((double)A, y, a);
+}
+template <int B, int J>
+__device__ __forceinline__ void dc_drow(const double (&y)[2 * B - 1], double& a) {
+    dc_dterm<B, J, 0>(y[0], a);
+    dc_dterm<B, J, 1>(y[1], a);
+    dc_dterm<B, J, 2>(y[2], a);
+    dc_dterm<B, J, 3>(y[3], a);
+    dc_dterm<B, J, 4>(y[4], a);
+    if constexpr (B == 4) {
+        dc_dterm<B, J, 5>(y[5], a);
+        dc_dterm<B, J, 6>(y[6], a);
+    }
+}
+template <int B, int I, int J = 0>
+__device__ __forceinline__ void dc_dcolumn(const double (&y)[2 * B - 1], double (&a)[DcGeo<B>::MMAX + 1]) {
+    if constexpr (J < 2 * B - 1 && I + J <= DcGeo<B>::MMAX) {
+        dc_drow<B, J>(y, a[I + J]);
+        dc_dcolumn<B, I, J + 1>(y, a);
+    }
+}
+static_assert(3 * 7 * 2520.0 * 4294967295.0 < 2251799813685248.0, "class sums below 2^51: exact in doubles and dc_d2ll");
+
+template <int B>
+__device__ __forceinline__ void dc_class_fp64(int r, uint32_t* Y, const uint32_t* SG, int lane) {
+    using Gm = DcGeo<B>;
+    constexpr int NP = Gm::NP, G = Gm::G, W2 = Gm::W2, BB = Gm::BB, MM = Gm::MMAX + 1;
+    double a[MM];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) a[m] = 0.0;
+    uint32_t* col0 = Y + r * G + lane;          // cells (k, t = r)
+    uint32_t* col1 = col0 + BB * G;             // cells (k, t = r + b)
+    {
+        double y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = dc_u2d(col0[k * W2 * G]);
+        dc_dcolumn<B, 0>(y, a);
+    }
+    {
+        double y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = dc_u2d(col1[k * W2 * G]);
+        dc_dcolumn<B, 1>(y, a);
+    }
+    if (r < 2) {            // t = r + 2b (the stored columns 2b, 2b + 1)
+        double y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = dc_u2d(col1[(k * W2 + BB) * G]);
+        dc_dcolumn<B, 2>(y, a);
+    } else if (r == 2) {    // t = 2b + 2: the sign terms, y_k = -s_k (two's complement products)
+        double y[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = -(double)SG[k * G + lane];
+        dc_dcolumn<B, 2>(y, a);
+    }
+    uint32_t hw[MM + 1];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+        const long long x = dc_d2ll(a[m]);
+        if (m < MM - 1) col0[m * W2 * G] = (uint32_t)x;
+        else if (r + BB * (MM - 1) < Gm::WOUT) col1[0] = (uint32_t)x;
+        hw[m] = (uint32_t)((unsigned long long)x >> 32) & 0xFFFFu;
+    }
+    hw[MM] = 0u;
+#pragma unroll
+    for (int h = 0; 2 * h < MM; ++h) col1[(1 + h) * W2 * G] = hw[2 * h] | (hw[2 * h + 1] << 16);
+}
+
 template <int B>
 __device__ __forceinline__ void dc_class(int r, uint32_t* Y, const uint32_t* SG, int lane) {
+    if constexpr (TG_DC_FP64) {
+        dc_class_fp64<B>(r, Y, SG, lane);
+        return;
+    }
     using Gm = DcGeo<B>;
     constexpr int NP = Gm::NP, G = Gm::G, W2 = Gm::W2, BB = Gm::BB, MM = Gm::MMAX + 1;
     uint64_t aP[MM], aN[MM];
