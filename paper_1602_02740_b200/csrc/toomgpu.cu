@@ -948,6 +948,10 @@ static int g_rows_max_count = [] {
     return e ? atoi(e) : 24000;   // C4's 16807-instance level: 4.59 -> 4.29 ms of interpolation
 }();
 
+static bool g_p8_rows_split = [] {   // TOOM_P8_ROWS_SPLIT=0: the generic-multiplier row kernel (A/B timing)
+    const char* e = getenv("TOOM_P8_ROWS_SPLIT");
+    return e ? atoi(e) != 0 : true;
+}();
 static toom_status launch_interp(int B, bool top, const uint32_t* Pc, uint32_t* W, uint32_t* out, size_t count,
                                  int ywidth, int Lw, int b, int wout, cudaStream_t st) {
     if (count == 0) return TOOM_OK;
@@ -987,7 +991,8 @@ static toom_status launch_interp(int B, bool top, const uint32_t* Pc, uint32_t* 
                 // rows in parallel (one thread per row and product), then the
                 // segment-parallel recomposition (row 0's scratch holds the carries)
                 const int nseg = (wout + b - 1) / b;
-                k_interp_rows_p8<<<nblk(14 * count), 128, 0, st>>>(Pc, W, count, ywidth, Lw);
+                if (g_p8_rows_split) k_interp_rows_p8s<<<(unsigned)(14 * ((count + 127) / 128)), 128, 0, st>>>(Pc, W, count, ywidth, Lw);
+                else k_interp_rows_p8<<<nblk(14 * count), 128, 0, st>>>(Pc, W, count, ywidth, Lw);
                 RecompArgs A{Pc, W, out, (long long)wout, 1, W, count, 15, Lw, b, wout, nseg, 0};
                 k_recomp_seg<<<nblk((size_t)nseg * count), 128, 0, st>>>(A);
                 k_recomp_fix<<<nblk(count), 128, 0, st>>>(W, count, nseg);

@@ -1192,6 +1192,124 @@ __global__ void __launch_bounds__(128, 4) k_interp_rows_p8(const uint32_t* __res
     }
 }
 
+// The same rows with the multipliers as compile-time constants: |m_jk| =
+// h 2^27 + l, each part one IMAD.WIDE.U32 (immediate x limb) into 64-bit sums
+// separated by the sign of m_jk (every sum < 2^61: toomgen asserts it), so a
+// row limb costs 2 multiply-adds per term instead of a generic 64 x 32 -> 128
+// multiply.  The linear combination, carries, divisions and output are those
+// of k_interp_rows_p8 (the same integers).  One CTA = one row x 128
+// products (CTA-uniform row constants).
+template <int J, int K>
+__device__ __forceinline__ void p8s_term(uint32_t y, uint64_t& lp, uint64_t& hp, uint64_t& ln, uint64_t& hn) {
+    constexpr long long M = tg_brow_cx_P8(J, K);
+    constexpr unsigned long long A = M < 0 ? (unsigned long long)(-M) : (unsigned long long)M;
+    constexpr uint32_t L = (uint32_t)(A & ((1ull << tg_brow_split_P8) - 1)), H = (uint32_t)(A >> tg_brow_split_P8);
+    static_assert((A >> tg_brow_split_P8) < (1ull << 32), "27-bit split: high part one word");
+    if constexpr (M > 0) {
+        if constexpr (L != 0) lp = tg_madw(L, y, lp);
+        if constexpr (H != 0) hp = tg_madw(H, y, hp);
+    } else if constexpr (M < 0) {
+        if constexpr (L != 0) ln = tg_madw(L, y, ln);
+        if constexpr (H != 0) hn = tg_madw(H, y, hn);
+    }
+}
+template <int J, int K = 0>
+__device__ __forceinline__ void p8s_terms(const uint32_t (&y)[15], uint64_t& lp, uint64_t& hp, uint64_t& ln, uint64_t& hn) {
+    if constexpr (K < 15) {
+        p8s_term<J, K>(y[K], lp, hp, ln, hn);
+        p8s_terms<J, K + 1>(y, lp, hp, ln, hn);
+    }
+}
+template <int J>
+__device__ __forceinline__ void p8s_row(const uint32_t* __restrict__ P1, uint32_t* __restrict__ W, size_t count, size_t c,
+                                        int ywidth, int Lw) {
+    constexpr int NP = 15;
+    const size_t S = (size_t)NP * count;
+    const uint32_t* yb = P1 + c;
+    uint32_t fill[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) fill[k] = (__ldg(yb + (size_t)(ywidth - 1) * S + (size_t)k * count) >> 31) ? 0xFFFFFFFFu : 0u;
+    long long corr = 0;   // exactness check: a negative y_k read modulo 2^(32 window) adds -m_k 2^(32 window)
+    if (tg_check_on) {
+#pragma unroll
+        for (int k = 0; k < NP; ++k) corr += tg_brow_cx_P8(J, k) * (long long)(fill[k] & 1u);
+    }
+    const uint32_t o1 = tg_brow_o1_P8[J], o2 = tg_brow_o2_P8[J], i1 = tg_brow_i1_P8[J], i2 = tg_brow_i2_P8[J];
+    const int sh = tg_brow_s_P8[J], a = sh >> 5, r = sh & 31;
+    long long acc = 0;
+    uint32_t b1 = 0, b2 = 0, qp = 0;
+    uint32_t* dst = W + (size_t)J * Lw * count + c;
+    const int tend = Lw + a + (r ? 1 : 0);
+    auto ld = [&](int t, uint32_t (&y)[NP]) {
+        if (t < ywidth) {
+            const uint32_t* yt = yb + (size_t)t * S;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) y[k] = __ldg(yt + (size_t)k * count);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NP; ++k) y[k] = fill[k];
+        }
+    };
+    const int tlast = tend + (tg_check_on ? 3 : 0);
+    auto step = [&](int t, const uint32_t (&y)[NP]) {
+        uint64_t lp = 0, hp = 0, ln = 0, hn = 0;
+        p8s_terms<J>(y, lp, hp, ln, hn);
+        const __int128 lin = (__int128)(long long)(lp - ln) + ((__int128)(long long)(hp - hn) << tg_brow_split_P8) + acc;
+        acc = (long long)(lin >> 32);
+        uint32_t q = tg_divexact_step((uint32_t)lin, b1, i1, o1);
+        if (o2 > 1) q = tg_divexact_step(q, b2, i2, o2);
+        const int u = t - a - (r ? 1 : 0);
+        if (u >= 0 && u < Lw) dst[(size_t)u * count] = r ? __funnelshift_r(qp, q, r) : q;
+        if (t <= a && tg_check_on) tg_check_low(t < a ? (q ? 1u : 0u) : q, t < a ? 1 : r);
+        qp = q;
+    };
+    // three limbs in flight: buffer X is refilled for limb t + 3 right after
+    // limb t used it (no register moves between the load and its use)
+    uint32_t yA[NP], yB[NP], yC[NP];
+    ld(0, yA);
+    ld(1, yB);
+    ld(2, yC);
+#pragma unroll 1
+    for (int t = 0; t < tlast; t += 3) {
+        step(t, yA);
+        ld(t + 3, yA);
+        if (t + 1 >= tlast) break;
+        step(t + 1, yB);
+        ld(t + 4, yB);
+        if (t + 2 >= tlast) break;
+        step(t + 2, yC);
+        ld(t + 5, yC);
+    }
+    if (tg_check_on) {
+        const long long ac = acc - corr;
+        tg_check_end((uint64_t)ac, b1, o1);
+        if (o2 > 1) tg_check_end((uint64_t)((ac - (long long)b1) / (long long)o1), b2, o2);
+    }
+}
+__global__ void __launch_bounds__(128) k_interp_rows_p8s(const uint32_t* __restrict__ P1, uint32_t* __restrict__ W,
+                                                         size_t count, int ywidth, int Lw) {
+    const unsigned nb = (unsigned)((count + 127) / 128);   // CTAs per row
+    const int row = 1 + (int)(blockIdx.x / nb);
+    const size_t c = (size_t)(blockIdx.x % nb) * 128 + threadIdx.x;
+    if (c >= count) return;
+    switch (row) {
+        case 1: p8s_row<1>(P1, W, count, c, ywidth, Lw); break;
+        case 2: p8s_row<2>(P1, W, count, c, ywidth, Lw); break;
+        case 3: p8s_row<3>(P1, W, count, c, ywidth, Lw); break;
+        case 4: p8s_row<4>(P1, W, count, c, ywidth, Lw); break;
+        case 5: p8s_row<5>(P1, W, count, c, ywidth, Lw); break;
+        case 6: p8s_row<6>(P1, W, count, c, ywidth, Lw); break;
+        case 7: p8s_row<7>(P1, W, count, c, ywidth, Lw); break;
+        case 8: p8s_row<8>(P1, W, count, c, ywidth, Lw); break;
+        case 9: p8s_row<9>(P1, W, count, c, ywidth, Lw); break;
+        case 10: p8s_row<10>(P1, W, count, c, ywidth, Lw); break;
+        case 11: p8s_row<11>(P1, W, count, c, ywidth, Lw); break;
+        case 12: p8s_row<12>(P1, W, count, c, ywidth, Lw); break;
+        case 13: p8s_row<13>(P1, W, count, c, ywidth, Lw); break;
+        default: p8s_row<14>(P1, W, count, c, ywidth, Lw); break;
+    }
+}
+
 // recomposition pass 1: thread per (segment s, product c), carry-in 0.
 // Coefficient j: w_0 = y_0 and (last_copy) w_{NP-1} = y_inf come from the
 // products (interleaved [ywidth][NP*count]), the others from W [NP][Lw][count];

@@ -1343,6 +1343,25 @@ def emit_bigrow_tables(ps: PointSet) -> str:
     L.append(f"TG_CONST unsigned tg_brow_i2_{nm}[{NP}] = {{" + ", ".join(f"0x{_inv32(x):08X}u" for x in O2) + "};")
     L.append(f"TG_CONST int tg_brow_s_{nm}[{NP}] = {{" + ", ".join(str(x) for x in S) + "};")
     L.append(f"constexpr int tg_brow_maxs_{nm} = {max(S)};")
+    # the same multipliers as compile-time constants (k_interp_rows_p8s: one
+    # IMAD.WIDE.U32 per 27-bit part of |m| into sign-separated 64-bit sums;
+    # with limbs below 2^32 every such sum stays below 2^61)
+    SPLIT = 27
+    for r in M[1:]:
+        for sg in (1, -1):
+            lo = sum((abs(m) & ((1 << SPLIT) - 1)) for m in r if m * sg > 0) * 0xFFFFFFFF
+            hi = sum((abs(m) >> SPLIT) for m in r if m * sg > 0) * 0xFFFFFFFF
+            assert lo < (1 << 61) and hi < (1 << 61), (nm, r)
+    L.append(f"constexpr int tg_brow_split_{nm} = {SPLIT};")
+    L.append(f"TG_HD constexpr long long tg_brow_cx_{nm}(int j, int k) {{")
+    L.append(f"  switch (j * {NP} + k) {{")
+    for j, r in enumerate(M):
+        for k, m in enumerate(r):
+            if m:
+                L.append(f"    case {j * NP + k}: return {m}ll;")
+    L.append("    default: return 0ll;")
+    L.append("  }")
+    L.append("}")
     return "\n".join(L)
 
 
