@@ -1259,7 +1259,10 @@ __device__ __forceinline__ void p8s_row(const uint32_t* __restrict__ P1, uint32_
         uint32_t q = tg_divexact_step((uint32_t)lin, b1, i1, o1);
         if (o2 > 1) q = tg_divexact_step(q, b2, i2, o2);
         const int u = t - a - (r ? 1 : 0);
-        if (u >= 0 && u < Lw) dst[(size_t)u * count] = r ? __funnelshift_r(qp, q, r) : q;
+        if (u >= 0 && u < Lw) {   // output limbs in order: one pointer step each
+            *dst = r ? __funnelshift_r(qp, q, r) : q;
+            dst += count;
+        }
         if (t <= a && tg_check_on) tg_check_low(t < a ? (q ? 1u : 0u) : q, t < a ? 1 : r);
         qp = q;
     };

@@ -117,7 +117,80 @@ __device__ __forceinline__ void cls_column(const uint32_t (&y)[7], uint64_t (&aP
     if constexpr (I + 6 <= 8) cls_row<6>(y, aP[I + 6], aN[I + 6]);
 }
 
+// the class sums on the FP64 pipe (TG_CLS_FP64, default; as the bottom's,
+// csrc/fused_dc.cuh): y < 2^32 and |A'_jk| <= 720 < 2^10 give terms below
+// 2^42 and |X| < 2^45 (each accumulator sums at most 21 of them), so every
+// DFMA result is an integer below 2^53, exact; the IMAD pipe is left to the
+// division and carry phases of the other resident CTA
+#ifndef TG_CLS_FP64
+#define TG_CLS_FP64 1
+#endif
+template <int J>
+__device__ __forceinline__ void cls_drow(const double (&y)[7], double& a) {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const long long A = tg_combA_cx_T4(J, k);
+        if (A != 0) a = fma((double)A, y[k], a);
+    }
+}
+template <int I, int J = 0>
+__device__ __forceinline__ void cls_dcolumn(const double (&y)[7], double (&a)[9]) {
+    if constexpr (J < 7 && I + J <= 8) {
+        cls_drow<J>(y, a[I + J]);
+        cls_dcolumn<I, J + 1>(y, a);
+    }
+}
+static_assert(21.0 * 720.0 * 4294967295.0 < 2251799813685248.0, "class sums below 2^51: exact in doubles and dc_d2ll");
+
+__device__ __forceinline__ void cls_class_fp64(int r, uint32_t* Y, int lane) {
+    using namespace cls;
+    double a[9];
+#pragma unroll
+    for (int m = 0; m < 9; ++m) a[m] = 0.0;
+    uint32_t* c0 = Y + r * G + lane;       // cells (k, r)
+    uint32_t* c1 = c0 + 64 * G;            // cells (k, r + 64)
+    {
+        double y[7];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = dc_u2d(c0[k * YW * G]);
+        cls_dcolumn<0>(y, a);
+    }
+    {
+        double y[7];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = dc_u2d(c1[k * YW * G]);
+        cls_dcolumn<1>(y, a);
+    }
+    if (r < 2) {            // t = r + 128 (columns 128, 129: never overwritten)
+        double y[7];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = dc_u2d(c1[(k * YW + 64) * G]);
+        cls_dcolumn<2>(y, a);
+    } else if (r == 2) {    // t = 130: y_k = -s_k, the sign of limb 129
+        double y[7];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) y[k] = -(double)(Y[(k * YW + YW - 1) * G + lane] >> 31);
+        cls_dcolumn<2>(y, a);
+    }
+    uint32_t hw[9];
+#pragma unroll
+    for (int m = 0; m < 9; ++m) {
+        const uint64_t x = (uint64_t)dc_d2ll(a[m]);
+        hw[m] = (uint32_t)(x >> 32) & 0xFFFFu;
+        if (m <= 6) c0[m * YW * G] = (uint32_t)x;
+        else if (m == 7) c1[0] = (uint32_t)x;
+        else if (r == 0) c1[YW * G] = (uint32_t)x;   // P = 512
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) c1[(2 + h) * YW * G] = hw[2 * h] | (hw[2 * h + 1] << 16);
+    if (r == 0) c1[6 * YW * G] = hw[8];
+}
+
 __device__ __forceinline__ void cls_class(int r, uint32_t* Y, int lane) {
+    if constexpr (TG_CLS_FP64) {
+        cls_class_fp64(r, Y, lane);
+        return;
+    }
     using namespace cls;
     uint64_t aP[9], aN[9];
 #pragma unroll
