@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) k_lz_eval(LzSrc pu, LzSrc pv, uint32_t* _
 // each with its own carry chain, written as e two's-complement limbs to the
 // interleaved family [e][NP*count] (the fused bottom level's MODE 0 input).
 template <int B>
-__global__ void __launch_bounds__(128) k_lz_eval_last(LzSrc pu, LzSrc pv, uint32_t* __restrict__ du,
+__global__ void __launch_bounds__(64, 25) k_lz_eval_last(LzSrc pu, LzSrc pv, uint32_t* __restrict__ du,
                                                       uint32_t* __restrict__ dv, long long count, int b, int lentop,
                                                       int e) {
     constexpr int NP = 2 * B - 1;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(128) k_lz_eval_last(LzSrc pu, LzSrc pv, uint32
     const LzSrc& S = blockIdx.y ? pv : pu;
     uint32_t* dst = (blockIdx.y ? dv : du) + c;
     const long long rows = NP * count;
-    long long cy[NP];
+    int cy[NP];   // |lin| < 2^37 (|c_kj| sums to <= 15, lazy carries small): carries fit 32 bits
 #pragma unroll
     for (int k = 0; k < NP; ++k) cy[k] = 0;
     // (the even-odd sharing of lz_points measured slower here: 318 -> 341 us
@@ -196,9 +196,9 @@ __global__ void __launch_bounds__(128) k_lz_eval_last(LzSrc pu, LzSrc pv, uint32
                 else if (m < 0) N += (uint64_t)(-m) * xl[j];
                 if (m != 0) { H += (int)m * xh[j]; Hs += (int)m * xs[j]; }
             }
-            const long long lin = cy[k] + (long long)(P - N) + (long long)H + ((long long)Hs << 32);
+            const long long lin = (long long)cy[k] + (long long)(P - N) + (long long)H + ((long long)Hs << 32);
             d[k * count] = (uint32_t)lin;
-            cy[k] = lin >> 32;
+            cy[k] = (int)(lin >> 32);
         }
     }
 }

@@ -2097,11 +2097,15 @@ static toom_status launch_lazy(const Plan& plan, size_t l, bool down, uint32_t* 
         const unsigned ny = plan.square ? 1 : 2;
         if (deepest && il) {   // evaluation + carry normalisation, interleaved children
             ProfScope ps(CAT_EVAL, st);
-            dim3 grid((unsigned)((L.count + 127) / 128), ny);
+            // 64-thread CTAs at 32 registers (launch bounds 64 x 25): all of
+            // C4's 2 x 117649 chains resident at once (measured: 128-thread
+            // CTAs at 48 registers 327 us, 40 registers without spills 343 us,
+            // 32 registers 268 us)
+            dim3 grid((unsigned)((L.count + 63) / 64), ny);
             uint32_t* du = (uint32_t*)(ws + L.offU);
             uint32_t* dv = (uint32_t*)(ws + L.offV);
-            if (L.B == 3) k_lz_eval_last<3><<<grid, 128, 0, st>>>(pu, pv, du, dv, cnt, L.b, L.lentop, L.e);
-            else k_lz_eval_last<4><<<grid, 128, 0, st>>>(pu, pv, du, dv, cnt, L.b, L.lentop, L.e);
+            if (L.B == 3) k_lz_eval_last<3><<<grid, 64, 0, st>>>(pu, pv, du, dv, cnt, L.b, L.lentop, L.e);
+            else k_lz_eval_last<4><<<grid, 64, 0, st>>>(pu, pv, du, dv, cnt, L.b, L.lentop, L.e);
             ps.done(st);
             ++t_launches;
             return cudaGetLastError() == cudaSuccess ? TOOM_OK : TOOM_ECUDA;
