@@ -108,7 +108,31 @@ struct L2Smem {
 // Pass 1 / pass 2 of one output of one tile.  lin: this thread's CH
 // positions p0 = tstart + tid*CH.  P.st_base + tile*st_stride is the tile's
 // LTile record.
-template <typename Acc, int CH, class HaloF>
+// sum of v over the lanes of a warp (every lane gets it)
+__device__ __forceinline__ long long lv2_warp_sum(long long v) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+__device__ __forceinline__ __int128 lv2_warp_sum(__int128 v) {
+    unsigned long long lo = (unsigned long long)v;
+    long long hi = (long long)(v >> 64);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, d);
+        const long long h2 = __shfl_xor_sync(0xffffffffu, hi, d);
+        const unsigned long long sl = lo + l2;
+        hi += h2 + (sl < lo ? 1 : 0);
+        lo = sl;
+    }
+    return ((__int128)hi << 64) | (__int128)lo;
+}
+
+// COOP: halo_fn(h, lane) is lane's share of the terms of halo position h,
+// summed over the last warp (the halo of a multi-output op, a serial loop
+// over every term on one thread otherwise, was the tail of pass 2:
+// profiles/r02_c5top_*); else halo_fn(hl) fills all positions on one thread.
+template <typename Acc, int CH, bool COOP = false, class HaloF>
 __device__ __forceinline__ void lv2_tile(const Acc (&lin)[CH], const LMod& M, const LFinish& P, unsigned tile,
                                          int tstart, L2Smem& sh, uint32_t* Q, HaloF halo_fn, int phase) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -241,17 +265,32 @@ __device__ __forceinline__ void lv2_tile(const Acc (&lin)[CH], const LMod& M, co
         Q[tid * (CH + 1) + q] = xq;   // padded: conflict-free (position i at i + i / CH)
     }
     const int halo = P.sa + (P.sr ? 1 : 0);
-    if (tid == NT - 1 && halo > 0) {
-        Acc hl[LV_MAXHALO];
-        halo_fn(hl);
+    if constexpr (COOP) {
+        if (warp == NW - 1) {
+#pragma unroll 1
+            for (int h = 0; h < halo; ++h) {
+                const Acc v = lv2_warp_sum(halo_fn(h, lane)) + (Acc)c;   // (c, beta: lane 31's, the tile's last thread)
+                if (lane == 31) {
+                    uint32_t xq = (uint32_t)v;
+                    c = (long long)(v >> 32);
+                    if (o > 1) xq = tg_divexact_step(xq, beta, P.oinv, o);
+                    Q[TL + h + (TL + h) / CH] = xq;
+                }
+            }
+        }
+    } else {
+        if (tid == NT - 1 && halo > 0) {
+            Acc hl[LV_MAXHALO];
+            halo_fn(hl);
 #pragma unroll
-        for (int h = 0; h < LV_MAXHALO; ++h) {
-            if (h >= halo) break;
-            const Acc v = hl[h] + (Acc)c;
-            uint32_t xq = (uint32_t)v;
-            c = (long long)(v >> 32);
-            if (o > 1) xq = tg_divexact_step(xq, beta, P.oinv, o);
-            Q[TL + h + (TL + h) / CH] = xq;
+            for (int h = 0; h < LV_MAXHALO; ++h) {
+                if (h >= halo) break;
+                const Acc v = hl[h] + (Acc)c;
+                uint32_t xq = (uint32_t)v;
+                c = (long long)(v >> 32);
+                if (o > 1) xq = tg_divexact_step(xq, beta, P.oinv, o);
+                Q[TL + h + (TL + h) / CH] = xq;
+            }
         }
     }
     __syncthreads();
@@ -421,19 +460,16 @@ __global__ void __launch_bounds__(LV_NT, WIDE ? 2 : 3) k_lmulti2(const LMultiDev
             for (int q = 0; q < CH; ++q) lin[q] += (Acc)m * (Acc)sj[q * NP1];
         }
         const LMod M{O.o, O.orcp};
-        lv2_tile<Acc, CH>(lin, M,
+        lv2_tile<Acc, CH, true>(lin, M,
                           LFinish{O.oinv, O.p32, O.Mch, O.mi, O.sa, O.sr, d.W,
                                   reinterpret_cast<LStatus*>(tiles + o), d.no, O.dst + inst * d.dst_is, d.dst_ls},
                           tile, tstart, s_sh, Q,
-                          [&](Acc (&hl)[LV_MAXHALO]) {
-#pragma unroll
-                              for (int h = 0; h < LV_MAXHALO; ++h) {
-                                  Acc v = 0;
-                                  const int i = TL + h;
-                                  for (int s2 = 0; s2 < d.ns; ++s2)
-                                      v += (Acc)d.m[o][s2] * (Acc)Sb[(size_t)s2 * CH * NP1 + (i % CH) * NP1 + i / CH];
-                                  hl[h] = v;
-                              }
+                          [&](int h, int part) -> Acc {   // lane `part`: the sources s2 = part (mod 32)
+                              Acc v = 0;
+                              const int i = TL + h;
+                              for (int s2 = part; s2 < d.ns; s2 += 32)
+                                  v += (Acc)d.m[o][s2] * (Acc)Sb[(size_t)s2 * CH * NP1 + (i % CH) * NP1 + i / CH];
+                              return v;
                           },
                           phase);
         __syncthreads();   // Q / s_sh reuse by the next output
@@ -720,19 +756,16 @@ __global__ void __launch_bounds__(128, 3) k_lbig2(const LBigDev* __restrict__ dp
 #pragma unroll
         for (int q = 0; q < CH; ++q) lin[q] = (Acc)P0[q] + ((Acc)(long long)(P1[q] - N1[q]) << 16);
         const LMod M{O.o, O.orcp};
-        lv2_tile<Acc, CH>(lin, M,
+        lv2_tile<Acc, CH, true>(lin, M,
                           LFinish{O.oinv, O.p32, O.Mch, O.mi, O.sa, O.sr, d.W,
                                   reinterpret_cast<LStatus*>(tiles + o), d.no, O.dst + inst * d.dst_is, d.dst_ls},
                           tile, tstart, s_sh, Q,
-                          [&](Acc (&hl)[LV_MAXHALO]) {
-#pragma unroll
-                              for (int h = 0; h < LV_MAXHALO; ++h) {
-                                  Acc v = 0;
-                                  for (int s2 = 0; s2 < d.ns; ++s2)
-                                      for (int dd = 0; dd < d.nd[o][s2]; ++dd)
-                                          v += (Acc)((long long)d.a[o][s2][dd] * (long long)staged(s2, TL + h - dd + LB_PRE));
-                                  hl[h] = v;
-                              }
+                          [&](int h, int part) -> Acc {   // lane `part`: the sources s2 = part (mod 32)
+                              Acc v = 0;
+                              for (int s2 = part; s2 < d.ns; s2 += 32)
+                                  for (int dd = 0; dd < d.nd[o][s2]; ++dd)
+                                      v += (Acc)((long long)d.a[o][s2][dd] * (long long)staged(s2, TL + h - dd + LB_PRE));
+                              return v;
                           },
                           phase);
         __syncthreads();

@@ -1,17 +1,21 @@
 """Hot-spot summary of an ncu report's SASS source page:
-python scripts/sass_hot.py report.ncu-rep kernel_regex"""
+python scripts/sass_hot.py report.ncu-rep kernel_regex [instance]   (instance: which matching launch, default 0)"""
 import collections, csv, subprocess, sys
 rep, kre = sys.argv[1], sys.argv[2]
+want = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kre, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hdr = None
 data = []
+seen = -1
 for r in rows:
     if "Address" in r and "Source" in r:
-        if hdr is not None and data:
-            break          # first kernel only
+        if hdr is not None and data and seen == want:
+            break          # one launch only
         hdr = r
+        data = []
+        seen += 1
         continue
     if hdr and len(r) == len(hdr):
         data.append(r)
@@ -39,5 +43,8 @@ for i, r in enumerate(data):
     else:
         runs.append([c, i, 1, float(r[wi])])
 runs.sort(key=lambda x: -x[0] * x[2])
+srt = sorted(range(len(data)), key=lambda i: -float(data[i][wi]))
+for i in srt[:25]:
+    print("stall %5.1f%% exec %9d at %d: %s" % (100 * float(data[i][wi]) / ws, float(data[i][ei]), i, data[i][si].strip()[:70]))
 for c, i, n, w in runs[:15]:
     print("exec %9d x %4d = %5.1f%% stalls %5.1f%% at %d: %s" % (c, n, 100 * c * n / tot, 100 * w / ws, i, data[i][si].strip()[:50]))
