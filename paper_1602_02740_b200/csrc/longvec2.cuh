@@ -16,7 +16,7 @@
 //           limbs, shifted.
 // No tile ever waits for another (the look-back chains of the single-pass
 // executor were the bottleneck: 25% warps active, 7-8 barrier stalls per
-// issue, ncu profiles/r02_t16op_ncu.csv).
+// issue in the ncu full set of an earlier session of round 2; round 1 counters: profiles/r01_c4_launches_summary.txt).
 //
 // The borrow of the exact division never needs the normalised limbs of the
 // predecessors: with L_p = sum_{i<p} lin_i 2^(32 i) (unnormalised) and c_p the
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(128, 3) k_lbig2(const LBigDev* __restrict__ dp
     const int tstart = kt * TL;
     // staging: every thread issues the loads of two sources before storing
     // (a load-store loop per element was latency-bound: 11 long-scoreboard
-    // stalls per issue, profiles/r02_lbig2_ncu.csv)
+    // stalls per issue, ncu full set of an earlier session; the current counters: profiles/r02_c5top_*)
     constexpr int EX = (LB_PRE + LM_HALO + 31) / 32;   // extra elements past TL, per warp lane
     for (int s0 = 0; s0 < d.ns; s0 += 2) {
         uint32_t xv[2][CH + EX];

@@ -1402,10 +1402,12 @@ static void long_interp_ops(const Level& L, YF yv, uint32_t* slots, uint32_t* ds
 // tile shape of a multi-output op: the largest tile within the shared-memory
 // budget that pads the vector by at most 1/8
 // multi-output ops staging at least this many sources use 4 limbs per thread
-// (off by default: C5 106.0 ms at 16 limbs vs 107.6 ms with 4 from 8 sources)
+// (16: the Toom-16 evaluation, whose 16 staged sources leave a 16-limb tile 2
+// warps per CTA; C5 69.36 ms at 16 limbs, 68.74 ms with 4 from 16 sources,
+// 69.23 ms with 4 from 8 sources, gpurun_out/ch4_time.log of round 2)
 static int g_multi_ch4_ns = [] {
     const char* e = getenv("TOOM_MULTI_CH4_NS");
-    return e ? atoi(e) : 1 << 20;
+    return e ? atoi(e) : 16;
 }();
 
 static bool multi_shape(LMultiDev& d) {
