@@ -152,6 +152,63 @@ __global__ void __launch_bounds__(256) k_lz_eval(LzSrc pu, LzSrc pv, uint32_t* _
     }
 }
 
+// The same for the first level of a single product (COUNT parents): a warp's
+// stores of one child are runs of `count` words 7 count apart (28 sectors
+// per store at count = 1: the level was bound by the store path, 34 us for
+// 38 MB, profiles/r02_c4_ncu_raw_summary.csv), so the CTA's outputs, one
+// contiguous range of the family, are staged in shared memory and copied
+// out in address order.
+// (COUNT at compile time, 32-bit indices: the divisions of the copy-out by
+// runtime values cost more than the stores saved, 24 -> 39 us at count = 7)
+template <int B, int COUNT>
+__global__ void __launch_bounds__(256) k_lz_eval_small(LzSrc pu, LzSrc pv, uint32_t* __restrict__ ulo, uint32_t* __restrict__ uhi,
+                                                       uint32_t* __restrict__ vlo, uint32_t* __restrict__ vhi, int b,
+                                                       int lentop, int e) {
+    constexpr int NP = 2 * B - 1, NT = 256;
+    constexpr unsigned count = COUNT, rows = NP * COUNT;
+    constexpr int CAP = NP * (NT + 2 * COUNT);
+    __shared__ uint32_t slo[CAP], shi[CAP];
+    const unsigned g0 = blockIdx.x * NT;          // (e * count < 2^31: the host's launch condition)
+    const unsigned g = g0 + threadIdx.x;
+    const unsigned t = g / count, c = g - t * count;
+    const unsigned t_first = g0 / count;
+    const LzSrc& S = blockIdx.y ? pv : pu;
+    uint32_t* lo = blockIdx.y ? vlo : ulo;
+    uint32_t* hi = blockIdx.y ? vhi : uhi;
+    if (t < (unsigned)e) {
+        long long v[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            const int len = (j == B - 1) ? lentop : b;
+            uint32_t xl = 0;
+            int xh = 0, xs = 0;
+            if ((int)t < len) lz_get2(S, c, j * b + (int)t, xl, xh, xs);
+            v[j] = (long long)xl + xh + ((long long)xs << 32);
+        }
+        long long lin[NP];
+        lz_points<B>(v, lin);
+        const unsigned r0 = (t - t_first) * rows + c;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            slo[r0 + k * count] = (uint32_t)lin[k];
+            shi[r0 + k * count] = (uint32_t)(int)(lin[k] >> 32);
+        }
+    }
+    __syncthreads();
+    const unsigned t_last = (g0 + NT - 1) / count;
+    const unsigned region = (t_last - t_first + 1) * rows;
+    for (unsigned r = threadIdx.x; r < region; r += NT) {
+        const unsigned tt = r / rows, rem = r - tt * rows;
+        const unsigned cc = rem % count;
+        const unsigned t2 = t_first + tt;
+        const unsigned g2 = t2 * count + cc;
+        if (g2 < g0 || g2 >= g0 + NT || t2 >= (unsigned)e) continue;
+        lo[(size_t)t2 * rows + rem] = slo[r];
+        if (t2 + 1 < (unsigned)e) hi[(size_t)(t2 + 1) * rows + rem] = shi[r];
+        if (t2 == 0) hi[rem] = 0u;
+    }
+}
+
 // ---- a2 of the deepest lazy level: evaluation + carry normalisation --------
 // One thread per (parent, operand): the 2B-1 children position by position,
 // each with its own carry chain, written as e two's-complement limbs to the
