@@ -1359,15 +1359,16 @@ __global__ void __launch_bounds__(128) k_recomp_seg(RecompArgs A) {
     uint64_t carry = 0;
     uint32_t ones = 0xFFFFFFFFu, l0 = 0;
     uint32_t* o = A.out + (long long)c * A.out_is + (long long)s * b * A.out_ls;
-    for (int r0 = 0; r0 < len; r0 += 4) {
-        uint32_t xa[4], xb[4];
+    constexpr int RQ = 8;   // limbs loaded ahead (4: 121 us on C3, latency-bound at 21 % warps active)
+    for (int r0 = 0; r0 < len; r0 += RQ) {
+        uint32_t xa[RQ], xb[RQ];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < RQ; ++q) {
             xa[q] = (hA && r0 + q < len) ? wl(s, r0 + q) : 0u;
             xb[q] = (hB && r0 + q < len) ? wl(s - 1, b + r0 + q) : 0u;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < RQ; ++q) {
             if (r0 + q < len) {
                 const uint64_t y = carry + xa[q] + xb[q] + (r0 + q > 0 ? k1 : k0);
                 const uint32_t lo = (uint32_t)y;
@@ -1388,14 +1389,24 @@ __global__ void __launch_bounds__(128) k_recomp_fix(uint32_t* __restrict__ R, si
     const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= count) return;
     uint32_t cin = 0;
-    for (int s = 0; s < nseg; ++s) {
-        uint32_t cout = R[(size_t)s * count + c];
-        if (cin) {
-            const uint32_t l0 = R[((size_t)nseg + s) * count + c];
-            if (l0 + cin < l0 && R[((size_t)2 * nseg + s) * count + c]) cout += 1;
+    for (int s0 = 0; s0 < nseg; s0 += 8) {   // the records of 8 segments loaded ahead of the chain
+        uint32_t co[8], l0[8], on[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const bool in = s0 + q < nseg;
+            co[q] = in ? R[(size_t)(s0 + q) * count + c] : 0u;
+            l0[q] = in ? R[((size_t)nseg + s0 + q) * count + c] : 0u;
+            on[q] = in ? R[((size_t)2 * nseg + s0 + q) * count + c] : 0u;
         }
-        R[(size_t)s * count + c] = cin;
-        cin = cout;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (s0 + q < nseg) {
+                uint32_t cout = co[q];
+                if (cin && l0[q] + cin < l0[q] && on[q]) cout += 1;
+                R[(size_t)(s0 + q) * count + c] = cin;
+                cin = cout;
+            }
+        }
     }
 }
 
@@ -1411,11 +1422,31 @@ __global__ void __launch_bounds__(128) k_recomp_apply(RecompArgs A) {
     if (!cc) return;
     uint32_t* o = A.out + (long long)c * A.out_is + (long long)s * A.b * A.out_ls;
     const int len = min(A.b, A.wout - s * A.b);
-    for (int r = 0; r < len && cc; ++r) {
-        const uint32_t x = o[(long long)r * A.out_ls];
-        const uint32_t y = x + cc;
-        o[(long long)r * A.out_ls] = y;
-        cc = (y < x) ? 1u : 0u;
+    {
+        // the carry wraps limb 0 and every other limb is all ones (pass 1's
+        // records; C3's all-ones quarter): the segment becomes limb 0 + carry
+        // and zeros, stored without reading it back
+        const uint32_t l0 = A.R[((size_t)A.nseg + s) * count + c];
+        if (l0 + cc < l0 && A.R[((size_t)2 * A.nseg + s) * count + c]) {
+            o[0] = l0 + cc;
+            for (int r = 1; r < len; ++r) o[(long long)r * A.out_ls] = 0u;
+            return;
+        }
+    }
+    // 8 limbs loaded ahead of the ripple (one load -> store chain per limb
+    // was a serial run of L2 latencies: 53 us on C3's all-ones quarter)
+    for (int r = 0; r < len && cc; r += 8) {
+        uint32_t x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = (r + q < len) ? o[(long long)(r + q) * A.out_ls] : 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (r + q < len && cc) {
+                const uint32_t y = x[q] + cc;
+                o[(long long)(r + q) * A.out_ls] = y;
+                cc = (y < x[q]) ? 1u : 0u;
+            }
+        }
     }
 }
 
