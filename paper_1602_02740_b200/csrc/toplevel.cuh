@@ -1359,6 +1359,7 @@ __global__ void __launch_bounds__(128) k_recomp_seg(RecompArgs A) {
     uint64_t carry = 0;
     uint32_t ones = 0xFFFFFFFFu, l0 = 0;
     uint32_t* o = A.out + (long long)c * A.out_is + (long long)s * b * A.out_ls;
+    const bool v4 = A.out_ls == 1 && ((reinterpret_cast<uintptr_t>(o)) & 15) == 0;
     constexpr int RQ = 8;   // limbs loaded ahead (4: 121 us on C3, latency-bound at 21 % warps active)
     for (int r0 = 0; r0 < len; r0 += RQ) {
         uint32_t xa[RQ], xb[RQ];
@@ -1367,15 +1368,26 @@ __global__ void __launch_bounds__(128) k_recomp_seg(RecompArgs A) {
             xa[q] = (hA && r0 + q < len) ? wl(s, r0 + q) : 0u;
             xb[q] = (hB && r0 + q < len) ? wl(s - 1, b + r0 + q) : 0u;
         }
+        uint32_t z[RQ];
 #pragma unroll
         for (int q = 0; q < RQ; ++q) {
+            z[q] = 0u;
             if (r0 + q < len) {
                 const uint64_t y = carry + xa[q] + xb[q] + (r0 + q > 0 ? k1 : k0);
                 const uint32_t lo = (uint32_t)y;
                 if (r0 + q == 0) l0 = lo; else ones &= lo;
-                o[(long long)(r0 + q) * A.out_ls] = lo;
+                z[q] = lo;
                 carry = y >> 32;
             }
+        }
+        if (v4 && r0 + RQ <= len) {   // row-major output: one 32-byte sector per thread and step
+            uint4* o4 = reinterpret_cast<uint4*>(o + r0);
+            o4[0] = make_uint4(z[0], z[1], z[2], z[3]);
+            o4[1] = make_uint4(z[4], z[5], z[6], z[7]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < RQ; ++q)
+                if (r0 + q < len) o[(long long)(r0 + q) * A.out_ls] = z[q];
         }
     }
     A.R[(size_t)s * count + c] = (uint32_t)carry;
