@@ -1441,7 +1441,12 @@ __global__ void __launch_bounds__(128) k_recomp_apply(RecompArgs A) {
         const uint32_t l0 = A.R[((size_t)A.nseg + s) * count + c];
         if (l0 + cc < l0 && A.R[((size_t)2 * A.nseg + s) * count + c]) {
             o[0] = l0 + cc;
-            for (int r = 1; r < len; ++r) o[(long long)r * A.out_ls] = 0u;
+            int r = 1;
+            if (A.out_ls == 1 && ((reinterpret_cast<uintptr_t>(o)) & 15) == 0) {   // 16-byte zero stores
+                for (; r < 4 && r < len; ++r) o[r] = 0u;
+                for (; r + 4 <= len; r += 4) *reinterpret_cast<uint4*>(o + r) = make_uint4(0u, 0u, 0u, 0u);
+            }
+            for (; r < len; ++r) o[(long long)r * A.out_ls] = 0u;
             return;
         }
     }
