@@ -350,7 +350,7 @@ struct LzFin {
 };
 
 template <int CH>
-__global__ void __launch_bounds__(LV_NT, 3) k_lz_fin(LzFin F, LTile* __restrict__ tiles, int phase) {
+__global__ void __launch_bounds__(LV_NT, 4) k_lz_fin(LzFin F, LTile* __restrict__ tiles, int phase) {
     __shared__ L2Smem s_sh;
     extern __shared__ uint32_t Q[];
     const int tid = threadIdx.x, NT = blockDim.x, TL = NT * CH;
